@@ -1,0 +1,278 @@
+"""Pins of the fp64 oracle against what the paper and mathematics fix.
+
+Every check here is independent of the oracle's own code path: printed paper
+values (tests/golden/paper_values.json, each with its citation), brute force
+from the *definition* (enumeration of warping paths / matchings), library
+routines for special cases, closed forms and the paper's inequalities.
+Integer-valued samples keep fp64 arithmetic exact where equality is asserted.
+"""
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")))
+RNG = np.random.default_rng(20260101)
+
+
+def lp(a, b, p):
+    d = np.abs(np.asarray(a, float) - np.asarray(b, float))
+    return d.max() if p == 0 else (d ** p).sum() ** (1.0 / p)
+
+
+# ---------------------------------------------------------------- brute force
+def dtw_by_matchings(x, y, w, p):
+    """DTW from the definition: the minimum over all
+    monotone many-to-many matchings Gamma inside the band |i-j| <= w that cover
+    every index of x and of y, of the l_p norm of {x_i - y_j}.  Enumerates every
+    subset of band cells (tiny n only)."""
+    n = len(x)
+    cells = [(i, j) for i in range(n) for j in range(n) if abs(i - j) <= w]
+    best = math.inf
+    for r in range(1, len(cells) + 1):
+        for gamma in itertools.combinations(cells, r):
+            if {i for i, _ in gamma} != set(range(n)) or {j for _, j in gamma} != set(range(n)):
+                continue
+            mono = all(not (a[0] < b[0] and a[1] > b[1]) and not (a[0] > b[0] and a[1] < b[1])
+                       for a in gamma for b in gamma)
+            if not mono:
+                continue
+            d = [abs(x[i] - y[j]) for i, j in gamma]
+            cost = max(d) if p == 0 else sum(v ** p for v in d)
+            best = min(best, cost)
+    return best  # p-th power (or max for p = inf)
+
+
+def dtw_by_paths(x, y, w, p):
+    """DTW as the minimum over explicit monotone lattice paths (0,0)->(n-1,n-1)
+    with unit steps, inside the band; enumerated path by path (no DP)."""
+    n = len(x)
+    best = [math.inf]
+
+    def rec(i, j, acc):
+        c = abs(x[i] - y[j])
+        acc = max(acc, c) if p == 0 else acc + c ** p
+        if acc >= best[0]:
+            return
+        if i == n - 1 and j == n - 1:
+            best[0] = acc
+            return
+        for di, dj in ((1, 0), (0, 1), (1, 1)):
+            a, b = i + di, j + dj
+            if a < n and b < n and abs(a - b) <= w:
+                rec(a, b, acc)
+
+    rec(0, 0, 0.0)
+    return best[0]
+
+
+def rand_int_series(n):
+    return RNG.integers(-2, 3, size=n).astype(float)
+
+
+# ---------------------------------------------------------------- envelope
+@pytest.mark.parametrize("case", GOLDEN["envelope"], ids=lambda c: c["cite"][:30])
+def test_envelope_golden(case):
+    U, L = oracle.envelope(case["y"], case["w"])
+    assert U.tolist() == case["U"] and L.tolist() == case["L"]
+    U2, L2, _ = oracle.envelope_stream(case["y"], case["w"])
+    assert U2.tolist() == case["U"] and L2.tolist() == case["L"]
+
+
+def _env_numpy(y, w):
+    from numpy.lib.stride_tricks import sliding_window_view
+    n = len(y)
+    w = min(w, n - 1)
+    pad_hi = np.concatenate([np.full(w, -np.inf), y, np.full(w, -np.inf)])
+    pad_lo = np.concatenate([np.full(w, np.inf), y, np.full(w, np.inf)])
+    return (sliding_window_view(pad_hi, 2 * w + 1).max(axis=1),
+            sliding_window_view(pad_lo, 2 * w + 1).min(axis=1))
+
+
+def test_envelope_vs_library_and_streaming():
+    """Definition == numpy sliding-window max/min; corrected Alg. 1 == definition
+    with <= 3n comparisons; w = 0 gives y; w >= n-1 gives global max/min."""
+    for _ in range(3000):
+        n = int(RNG.integers(1, 40))
+        w = int(RNG.integers(0, n + 3))
+        kind = RNG.integers(0, 4)
+        if kind == 0:
+            y = RNG.standard_normal(n)
+        elif kind == 1:
+            y = RNG.integers(-2, 3, size=n).astype(float)  # many ties
+        elif kind == 2:
+            y = np.arange(n, dtype=float) * (1 if RNG.random() < 0.5 else -1)  # monotone
+        else:
+            y = np.full(n, 1.5)
+        U, L = oracle.envelope(y, w)
+        Un, Ln = _env_numpy(y, w)
+        assert np.array_equal(U, Un) and np.array_equal(L, Ln)
+        Us, Ls, cmp = oracle.envelope_stream(y, w)
+        assert np.array_equal(U, Us) and np.array_equal(L, Ls)
+        assert cmp <= 3 * n
+        if w == 0:
+            assert np.array_equal(U, y) and np.array_equal(L, y)
+        if w >= n - 1:
+            assert np.all(U == y.max()) and np.all(L == y.min())
+
+
+def test_envelope_monotone_in_w():
+    for _ in range(300):
+        n = int(RNG.integers(2, 30))
+        y = RNG.standard_normal(n)
+        w1 = int(RNG.integers(0, n))
+        w2 = int(RNG.integers(w1, n + 2))
+        U1, L1 = oracle.envelope(y, w1)
+        U2, L2 = oracle.envelope(y, w2)
+        assert np.all(U1 <= U2) and np.all(L1 >= L2) and np.all(L1 <= y) and np.all(y <= U1)
+
+
+# ---------------------------------------------------------------- DTW
+@pytest.mark.parametrize("case", GOLDEN["dtw"], ids=lambda c: c["cite"][:30])
+def test_dtw_golden(case):
+    if "rooted" in case:
+        assert oracle.dtw(case["x"], case["y"], case["w"], case["p"]) == pytest.approx(case["rooted"], abs=1e-12)
+    else:
+        assert oracle.dtw_pow(case["x"], case["y"], case["w"], case["p"]) == pytest.approx(case["value_pow"], abs=1e-12)
+
+
+def test_dtw_equals_definition_by_matchings():
+    """Exhaustive over all band matchings for n <= 3 (every w), several n = 4."""
+    for n in (1, 2, 3):
+        for _ in range(60):
+            x, y = rand_int_series(n), rand_int_series(n)
+            for w in range(0, n + 1):
+                for p in (1, 2, 0):
+                    assert oracle.dtw_pow(x, y, w, p) == dtw_by_matchings(x, y, w, p)
+    for _ in range(6):
+        x, y = rand_int_series(4), rand_int_series(4)
+        for w in (1, 3):
+            for p in (1, 2):
+                assert oracle.dtw_pow(x, y, w, p) == dtw_by_matchings(x, y, w, p)
+
+
+def test_dtw_equals_path_enumeration():
+    """All monotone lattice paths in the band, n <= 7, integer samples (exact)."""
+    for _ in range(400):
+        n = int(RNG.integers(1, 8))
+        x, y = rand_int_series(n), rand_int_series(n)
+        w = int(RNG.integers(0, n + 1))
+        for p in (1, 2, 0):
+            assert oracle.dtw_pow(x, y, w, p) == dtw_by_paths(x, y, w, p)
+
+
+def test_dtw_properties():
+    for _ in range(500):
+        n = int(RNG.integers(1, 24))
+        x, y = RNG.standard_normal(n), RNG.standard_normal(n)
+        for p in (1, 2):
+            d0 = oracle.dtw(x, y, 0, p)
+            assert d0 == pytest.approx(lp(x, y, p), rel=1e-12)                 # w=0 => l_p
+            prev = d0
+            for w in range(1, min(n, 6) + 1):
+                d = oracle.dtw(x, y, w, p)
+                assert d <= prev * (1 + 1e-12)                                 # non-increasing in w
+                assert d == pytest.approx(oracle.dtw(y, x, w, p), rel=1e-12)   # symmetric
+                b = RNG.standard_normal()
+                assert d == pytest.approx(oracle.dtw(x + b, y + b, w, p), rel=1e-9, abs=1e-12)
+                prev = d
+            assert oracle.dtw(x, y, n, p) <= lp(x, y, p) * (1 + 1e-12)         # DTW <= l_p
+            c = RNG.standard_normal()
+            w = int(RNG.integers(0, n + 1))
+            assert oracle.dtw(x, np.full(n, c), w, p) == pytest.approx(lp(x, np.full(n, c), p), rel=1e-12)
+        if n > 1:                                                              # P:1027-1029, p=1,q=2
+            w = int(RNG.integers(0, n + 1))
+            assert math.sqrt(2 * n - 2) * oracle.dtw(x, y, w, 2) >= oracle.dtw(x, y, w, 1) * (1 - 1e-12)
+
+
+def test_prop1_value_separation():
+    """x >= c >= y => DTW_1 = ||x - y||_1 (Prop. 1)."""
+    for _ in range(300):
+        n = int(RNG.integers(1, 20))
+        c = RNG.standard_normal()
+        x = c + np.abs(RNG.standard_normal(n))
+        y = c - np.abs(RNG.standard_normal(n))
+        w = int(RNG.integers(0, n + 1))
+        assert oracle.dtw(x, y, w, 1) == pytest.approx(np.abs(x - y).sum(), rel=1e-12)
+        assert oracle.dtw(y, x, w, 1) == pytest.approx(np.abs(x - y).sum(), rel=1e-12)
+
+
+def test_weak_triangle_inequality():
+    """DTW(x,y) + DTW(y,z) >= DTW(x,z) / min(2w+1, n)^(1/p)."""
+    for _ in range(300):
+        n = int(RNG.integers(1, 16))
+        x, y, z = (RNG.standard_normal(n) for _ in range(3))
+        w = int(RNG.integers(0, n + 1))
+        for p in (1, 2):
+            lhs = oracle.dtw(x, y, w, p) + oracle.dtw(y, z, w, p)
+            assert lhs >= oracle.dtw(x, z, w, p) / min(2 * w + 1, n) ** (1.0 / p) * (1 - 1e-12)
+
+
+# ---------------------------------------------------------------- bounds
+@pytest.mark.parametrize("case", GOLDEN["bounds"], ids=lambda c: c["cite"][:30])
+def test_bounds_golden(case):
+    x, y, w, p = case["x"], case["y"], case["w"], case["p"]
+    assert oracle.lb_keogh(x, y, w, p) ** p == pytest.approx(case["keogh_pow"], abs=1e-12)
+    assert oracle.lb_improved(x, y, w, p) ** p == pytest.approx(case["improved_pow"], abs=1e-12)
+    if "dtw_pow" in case:
+        assert oracle.dtw_pow(x, y, w, p) == pytest.approx(case["dtw_pow"], abs=1e-12)
+        assert dtw_by_paths(np.array(x, float), np.array(y, float), w, p) == case["dtw_pow"]
+    if "H" in case:
+        U, L = oracle.envelope(y, w)
+        assert oracle.projection(x, U, L).tolist() == case["H"]
+
+
+def test_bound_chain_and_paper_inequalities():
+    """LB_Keogh <= LB_Improved <= DTW;
+    LB_Keogh^p + DTW(H,y)^p <= DTW^p (Theorem 1, P:292-299 with h = H);
+    DTW - LB_Keogh <= ||H - y||_p (Prop. 2);
+    DTW - LB_Keogh <= ||max(U - y, y - L)||_p (corollary);
+    x inside the envelope => LB_Keogh = 0; w = 0 => LB_Keogh = l_p."""
+    for _ in range(1500):
+        n = int(RNG.integers(1, 12))
+        integer = RNG.random() < 0.5
+        x = rand_int_series(n) if integer else RNG.standard_normal(n)
+        y = rand_int_series(n) if integer else RNG.standard_normal(n)
+        w = int(RNG.integers(0, n + 1))
+        U, L = oracle.envelope(y, w)
+        H = oracle.projection(x, U, L)
+        for p in (1, 2):
+            kb = oracle.lb_keogh(x, y, w, p)
+            ib = oracle.lb_improved(x, y, w, p)
+            d = oracle.dtw(x, y, w, p)
+            tol = 1e-12 * (1 + d)
+            assert kb <= ib + tol and ib <= d + tol
+            if integer:
+                assert dtw_by_paths(x, y, w, p) == pytest.approx(d ** p, abs=1e-9)
+            assert kb ** p + oracle.dtw_pow(H, y, w, p) <= d ** p + 1e-9 * (1 + d ** p)
+            assert d - kb <= lp(H, y, p) + tol
+            assert d - kb <= lp(np.maximum(U - y, y - L), 0, p) + tol
+            if w == 0:
+                assert kb == pytest.approx(lp(x, y, p), rel=1e-12, abs=1e-12)
+        inside = np.clip(RNG.standard_normal(n), L, U)
+        assert oracle.lb_keogh(inside, y, w, 1) == 0.0
+        assert oracle.lb_keogh(y, y, w, 2) == 0.0 and oracle.lb_improved(y, y, w, 2) == 0.0
+
+
+def test_value_separated_error_is_exact():
+    """x >= c >= y: DTW_1 = ||x-H||_1 + ||H-y||_1 exactly."""
+    for _ in range(200):
+        n = int(RNG.integers(1, 15))
+        c = float(RNG.integers(-3, 4))
+        x = c + RNG.integers(0, 4, size=n).astype(float)
+        y = c - RNG.integers(0, 4, size=n).astype(float)
+        w = n  # full-width window
+        U, L = oracle.envelope(y, w)
+        H = oracle.projection(x, U, L)
+        d = oracle.dtw(x, y, w, 1)
+        assert d == np.abs(x - y).sum()
+        assert d == np.abs(x - H).sum() + np.abs(H - y).sum()
+
+
+def test_lb_improved_rejects_infinity():
+    assert math.isnan(oracle.lb_improved([1, 2], [2, 1], 1, 0))
