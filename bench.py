@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 two-pass DTW k-NN engine.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
+
+One STEP = one full pass of the hot path (query envelopes, LB_Keogh over the
+whole database, LB_Improved on survivors, banded DTW, top-k, and for N > 1 the
+NCCL all-gather + shard merge) over the whole workload of the config, with the
+inputs resident in HBM.  Metric: query-candidate pairs/s (BASELINE.json); DTW
+cells/s is reported beside it.  For N > 1 (torchrun) each rank owns a
+contiguous shard of the database (total work fixed: strong scaling); time is
+the max over ranks of CUDA-event time on the launching stream.
+
+`--impl reference` times the fp64 CPU oracle (the paper's Algorithm 3 scan,
+oracle/) on this box's host cores over a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import datagen  # noqa: E402
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def shard_rows(N, G, r):
+    lo = r * N // G
+    hi = (r + 1) * N // G
+    return lo, hi
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def oracle_sample(cfg, qs, db, budget_s=15.0, threads=None):
+    """Time the fp64 oracle (Alg. 3 scan, as it stands) on a bounded query sample."""
+    import oracle
+    threads = threads or os.cpu_count() or 1
+    t0 = time.perf_counter()
+    oracle.nn_twopass(qs[:1], db, cfg.w, cfg.p, cfg.k, threads=1)
+    per_q = max(time.perf_counter() - t0, 1e-3)
+    nq = int(max(1, min(len(qs) - 1, round(budget_s * threads / per_q))))
+    nq = max(threads, nq // threads * threads) if nq >= threads else nq
+    nq = min(nq, len(qs) - 1)
+    t0 = time.perf_counter()
+    oracle.nn_twopass(qs[1:1 + nq], db, cfg.w, cfg.p, cfg.k, threads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": nq * len(db) / dt, "unit": "pairs/s", "cores": min(threads, nq), "kind": "oracle",
+            "sample": f"{nq} of {cfg.Q} queries x all {len(db)} database series (Alg. 3 fp64 scan, "
+                      f"{min(threads, nq)} threads, {dt:.1f} s)", "seconds": dt}
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = _dist_env()
+    if rank != 0:
+        return 0
+    qs, db = datagen.make(cfg)
+    threads = os.cpu_count() or 1
+    import oracle
+    t0 = time.perf_counter()
+    oracle.nn_twopass(qs[:1], db, cfg.w, cfg.p, cfg.k, threads=1)
+    per_q = max(time.perf_counter() - t0, 1e-3)
+    # bounded sample per step: ~20 s of wall time over all cores for K+W steps
+    per_step_s = max(2.0, 150.0 / max(1, args.steps + args.warmup))
+    nq = int(max(1, min(cfg.Q, round(per_step_s * threads / per_q))))
+    times = []
+    for s in range(args.warmup + args.steps):
+        lo = (s * nq) % max(1, cfg.Q - nq)
+        t0 = time.perf_counter()
+        oracle.nn_twopass(qs[lo:lo + nq], db, cfg.w, cfg.p, cfg.k, threads=threads)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    dt = statistics.mean(times)
+    value = nq * cfg.N / dt
+    line = {"impl": "reference", "metric": "query-candidate pairs/s (exact DTW k-NN)", "value": value,
+            "unit": "pairs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "Q": cfg.Q, "N": cfg.N, "n": cfg.n, "w": cfg.w, "p": cfg.p,
+                       "k": cfg.k, "sample_queries_per_step": nq},
+            "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": min(threads, nq), "kind": "oracle",
+                             "sample": f"{nq} of {cfg.Q} queries x {cfg.N} series per step"},
+            "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+    from paper_0811_3301_b200 import binding as B
+
+    ws, rank, local = _dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if ws > 1 else 0)
+    torch.cuda.set_device(dev)
+    st = torch.cuda.current_stream()
+    lo, hi = shard_rows(cfg.N, ws, rank)
+    qs_h, _ = datagen.make(cfg, N=0)
+    db_h = datagen.series(cfg.family, hi - lo, cfg.n, cfg.seed, datagen.ROLE_DB, cfg.znorm, start=lo)
+    qs = torch.from_numpy(qs_h).to(dev)
+    db = torch.from_numpy(db_h).to(dev)
+    Nl = hi - lo
+    k = cfg.k
+    idx = torch.empty((cfg.Q, k), dtype=torch.int64, device=dev)
+    dst = torch.empty((cfg.Q, k), dtype=torch.float32, device=dev)
+    if ws > 1:
+        g_idx = torch.empty((ws, cfg.Q, k), dtype=torch.int64, device=dev)
+        g_dst = torch.empty((ws, cfg.Q, k), dtype=torch.float32, device=dev)
+
+    def step(stats=False):
+        r = B.nn_search(qs, db, cfg.w, cfg.p, k, index_base=lo, out=(idx, dst), return_stats=stats)
+        if ws > 1:
+            dist.all_gather_into_tensor(g_idx, idx)
+            dist.all_gather_into_tensor(g_dst, dst)
+            B.nn_merge(g_idx, g_dst)
+        return r[2] if stats else None
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    stats_all = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        barrier()
+        ev0.record(st)
+        for _ in range(args.steps):
+            stats_all.append(step(stats=True))
+        ev1.record(st)
+        barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ms_t = torch.tensor([ms], device=dev)
+    if ws > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+
+    # ---- e2e: host (pinned) buffers through the same public call, copies inside the timed region ----
+    qs_pin = torch.from_numpy(qs_h).pin_memory()
+    db_pin = torch.from_numpy(db_h).pin_memory()
+    h_idx = torch.empty((cfg.Q, k), dtype=torch.int64).pin_memory()
+    h_dst = torch.empty((cfg.Q, k), dtype=torch.float32).pin_memory()
+    e2e_steps = max(1, min(args.steps, 3))
+    B.nn_search(qs_pin, db_pin, cfg.w, cfg.p, k, index_base=lo, out=(h_idx, h_dst))
+    barrier()
+    ev0.record(st)
+    for _ in range(e2e_steps):
+        B.nn_search(qs_pin, db_pin, cfg.w, cfg.p, k, index_base=lo, out=(h_idx, h_dst))
+    ev1.record(st)
+    barrier()
+    e2e_ms = torch.tensor([ev0.elapsed_time(ev1) / e2e_steps], device=dev)
+    if ws > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_ms.item())
+
+    # ---- aggregate counters over ranks ----
+    def tot(key):
+        v = torch.tensor([float(sum(s[key] for s in stats_all) / len(stats_all))], device=dev,
+                         dtype=torch.float64)
+        if ws > 1:
+            dist.all_reduce(v)
+        return float(v.item())
+
+    keogh_ms = torch.tensor([statistics.mean(s["ms_keogh"] for s in stats_all)], device=dev)
+    if ws > 1:
+        dist.all_reduce(keogh_ms, op=dist.ReduceOp.MAX)
+    keogh_ms = float(keogh_ms.item())
+    pairs = cfg.Q * cfg.N
+    improved = tot("improved_evaluated")
+    dtw_eval = tot("dtw_evaluated")
+    dtw_ab = tot("dtw_abandoned")
+    cells_nom = tot("dtw_cells_nominal")
+    cells_cmp = tot("dtw_cells_computed")
+    launches = int(round(statistics.mean(s["kernel_launches"] for s in stats_all)))
+    if rank == 0:
+        pk = _peaks()
+        sm_clock = 1965.0 if not pk else float(pk.get("sm_max_mhz", 1965.0))
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        # ALU roofline of the dominant kernel (LB_Keogh pass): 4 SASS lane-ops per
+        # pair-element (FADD, FADD, FMNMX3, FADD|FFMA), peak = SMs x 128 FP32 lanes x clock
+        ops = 4.0 * (cfg.Q * (cfg.N // ws)) * cfg.n
+        achieved = ops / (keogh_ms * 1e-3) / 1e12
+        peak = n_sm * 128 * sm_clock * 1e6 / 1e12
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tpath):
+            try:
+                traffic = json.load(open(tpath)).get(cfg.name)
+            except Exception:
+                traffic = None
+        clocks = clk.summary()
+        line = {
+            "metric": "query-candidate pairs/s (exact DTW k-NN)",
+            "value": pairs / (ms_max * 1e-3),
+            "unit": "pairs/s",
+            "n_gpus": ws,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_max,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": cfg.name, "Q": cfg.Q, "N": cfg.N, "n": cfg.n, "w": cfg.w, "p": cfg.p,
+                       "k": cfg.k, "family": cfg.family, "parallelism": f"db-shard{ws}",
+                       "l2": f"inputs larger than L2 ({cfg.N * cfg.n * 4 / 1e9:.2f} GB database)"},
+            "dtw_cells_per_s": cells_cmp / (ms_max * 1e-3),
+            "dtw_cells_nominal_per_s": cells_nom / (ms_max * 1e-3),
+            "prune": {"keogh_pruned_frac": 1 - improved / pairs,
+                      "improved_evaluated_frac": improved / pairs,
+                      "dtw_evaluated_frac": dtw_eval / pairs,
+                      "dtw_abandoned_frac_of_evaluated": dtw_ab / max(1.0, dtw_eval)},
+            "stage_ms": {k2: statistics.mean(s[k2] for s in stats_all)
+                         for k2 in ("ms_envelope", "ms_keogh", "ms_select", "ms_improved", "ms_dtw", "ms_total")},
+            "roofline": {"kernel": "keogh_tile_kernel (LB_Keogh pass)", "bound": "alu", "achieved": achieved,
+                         "peak": peak, "unit": "Tlane-op/s", "frac": achieved / peak, "traffic": traffic,
+                         "peak_note": f"{n_sm} SMs x 128 FP32 lanes x {sm_clock:.0f} MHz (guide unit counts, "
+                                      "MEASURED_PEAKS sm_max_mhz); 4 lane-ops per pair-element",
+                         "keogh_ms": keogh_ms},
+            "e2e": {"value": pairs / (e2e_ms * 1e-3), "unit": "pairs/s",
+                    "h2d_bytes_per_step": int(qs_h.nbytes + db_h.nbytes),
+                    "d2h_bytes_per_step": int(cfg.Q * k * 12)},
+            "gpu_launches": launches * args.steps + (0 if ws == 1 else args.steps),
+            "clocks": clocks,
+        }
+        if ws == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = oracle_sample(cfg, qs_h, db_h, budget_s=args.cpu_budget)
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C5", choices=sorted(datagen.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    cfg = datagen.CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,146 @@
+/*
+ * dtwlb.h -- C ABI of the B200-native two-pass DTW k-NN library (libdtwlb.so).
+ *
+ * Method: D. Lemire, "Faster Retrieval with a Two-Pass Dynamic-Time-Warping
+ * Lower Bound" (arXiv:0811.3301).  "P:n" = line n of the paper's LaTeX source
+ * (PAPER.md), with the section / equation / algorithm named alongside.
+ *
+ * Conventions for every entry point
+ * ---------------------------------
+ * - Series are float32, row-major [count][n] (n contiguous), indexed 0..n-1
+ *   (the paper indexes 1..n).  x is the candidate (database row),
+ *   y the query (Alg. 3).
+ * - Pointers are CUDA DEVICE pointers unless a function says otherwise;
+ *   nn_search additionally accepts host pointers (see there).
+ * - The caller owns all memory.  The library never frees a caller pointer and
+ *   keeps none after return (it may cache its own device workspace).
+ * - `stream` is a cudaStream_t (NULL = legacy default stream).  The per-kernel
+ *   entry points are stream-ordered and asynchronous; nn_search returns when
+ *   its outputs are complete.
+ * - p is the exponent of DTW_p / LB_p: 1 or 2 (DTW_p of P:193-201).  The
+ *   locality constraint w (Sakoe-Chiba band |i-j| <= w) may be any
+ *   w >= 0; w >= n is clamped to n-1 (the window saturates).
+ * - Return value: DTWLB_OK (0) or a dtwlb_status.  dtwlb_last_error() returns a
+ *   thread-local message describing the last failure.  No C++ exception ever
+ *   crosses this boundary; there is no CPU fallback: without a usable sm_100
+ *   device every call returns DTWLB_ECUDA.
+ * - Distances/bounds returned are ROOTED (DTW_p = q_{1,1}^(1/p));
+ *   internally everything is accumulated in p-th-power space.
+ */
+#ifndef DTWLB_H
+#define DTWLB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum dtwlb_status {
+    DTWLB_OK = 0,
+    DTWLB_EINVAL = 1,       /* bad size / pointer / argument combination      */
+    DTWLB_EUNSUPPORTED = 2, /* p not in {1,2}; k above DTWLB_MAX_K             */
+    DTWLB_ENOMEM = 3,       /* device workspace allocation failed              */
+    DTWLB_ECUDA = 4,        /* CUDA runtime error or no sm_100 device          */
+    DTWLB_ENCCL = 5         /* NCCL error in the sharded path                  */
+} dtwlb_status;
+
+#define DTWLB_MAX_K 1024
+
+/* Warping envelope (section "Computing Lower Bounds on the DTW"):
+ *   U_i = max{x_k : |k-i| <= w},  L_i = min{x_k : |k-i| <= w},
+ * window clipped to [0, n-1].  x, U, L: device [count][n].  Exact (min/max
+ * do not round), so results are bit-identical to the definition.
+ * Errors: EINVAL if n < 1, w < 0, count < 0, or a NULL pointer with count > 0. */
+int lb_envelope(const float *x, int32_t n, int32_t w, float *U, float *L, int64_t count,
+                void *stream);
+
+/* LB_Keogh_p (section "LB_Keogh"; Alg. 2 lines P:507-514):
+ *   out[q][c] = ( sum_i d(x_c,i , [L_q,i , U_q,i])^p )^(1/p)
+ * = ||x_c - H(x_c, y_q)||_p with H the projection of Eq. (1).
+ * q_env: device [2][Q][n] (the U block of all Q queries, then the L block), as
+ * written by lb_envelope into a contiguous buffer.  db: device [N][n].
+ * out: device [Q][N] float32.  This is the dense (test / inspection) form of
+ * the bound pass that nn_search fuses.
+ * Errors: EINVAL (sizes, NULL, n < 1), EUNSUPPORTED (p not 1 or 2). */
+int lb_keogh(const float *q_env, const float *db, int64_t Q, int64_t N, int32_t n, int32_t p,
+             float *out, void *stream);
+
+/* LB_Improved_p (section "LB_Improved"; Alg. 3 lines P:587-606):
+ *   out[q][c]^p = LB_Keogh_p(x_c, y_q)^p + LB_Keogh_p(y_q, H(x_c, y_q))^p,
+ * i.e. the first pass plus the distance of y to the envelope of the
+ * projection H, both with locality constraint w.  q: device [Q][n] queries;
+ * q_env: device [2][Q][n] envelope of q with the same w; db: device [N][n];
+ * out: device [Q][N].  Dense form; nn_search evaluates it only on LB_Keogh
+ * survivors.  Errors: as lb_keogh, plus EINVAL for w < 0. */
+int lb_improved(const float *q, const float *q_env, const float *db, int64_t Q, int64_t N,
+                int32_t n, int32_t w, int32_t p, float *out, void *stream);
+
+/* Banded DTW_p of row pairs (section "Dynamic Time Warping"):
+ *   out[r] = DTW_p(x[r], y[r]) with the band |i-j| <= w, rooted.
+ * x, y: device [count][n]; out: device [count].
+ * Errors: EINVAL (sizes, NULL, n < 1, w < 0), EUNSUPPORTED (p not 1 or 2). */
+int dtw_band(const float *x, const float *y, int32_t n, int32_t w, int32_t p, float *out,
+             int64_t count, void *stream);
+
+/* Options of nn_search (all fields optional: pass NULL for defaults). */
+typedef struct nn_opts {
+    float eps;             /* prune iff bound > tau*(1+eps), tau = current k-th best
+                              (p-th-power space); default 1e-3 (reading c13) */
+    int64_t index_base;    /* added to every returned index (database shards)        */
+    int32_t query_block;   /* queries per pipeline block; 0 = automatic              */
+    int32_t flags;         /* DTWLB_KEOGH_ONLY: skip the LB_Improved pass (Alg. 2)   */
+    int32_t reserved[4];
+} nn_opts;
+
+#define DTWLB_KEOGH_ONLY 1
+
+/* Counters of one nn_search call (host struct, filled on return). */
+typedef struct nn_stats {
+    int64_t pairs;            /* Q*N query-candidate pairs                            */
+    int64_t keogh_evaluated;  /* LB_Keogh evaluations (= pairs)                       */
+    int64_t improved_evaluated; /* LB_Improved evaluations (LB_Keogh survivors seen)  */
+    int64_t dtw_evaluated;    /* DTW evaluations started                              */
+    int64_t dtw_abandoned;    /* ... of which early-abandoned                         */
+    int64_t dtw_cells_nominal;  /* band cells of every evaluated pair                 */
+    int64_t dtw_cells_computed; /* cells actually executed (early abandon)            */
+    double ms_envelope, ms_keogh, ms_select, ms_improved, ms_dtw, ms_total;
+    int64_t kernel_launches;    /* kernels this call launched                         */
+} nn_stats;
+
+/* Exact k-nearest-neighbour search under banded DTW_p: for each query y_q,
+ * the k database rows with the smallest (DTW_p(y_q, x_c), c) in lexicographic
+ * order (ties to the smaller index), by the paper's cascade (Alg. 3,
+ * P:578-620, generalised to p in {1,2}, k >= 1 and many queries): query
+ * envelope -> LB_Keogh over the whole database -> LB_Improved on survivors ->
+ * banded DTW on what remains, each gate pruning only when the bound exceeds
+ * the current k-th best times (1+eps).
+ *   queries: [Q][n] float32, db: [N][n] float32 -- device OR host pointers
+ *            (host buffers are staged to the device inside the call);
+ *   out_idx: [Q][k] int64 (index_base + row), out_dist: [Q][k] float32 rooted
+ *            DTW_p, ascending -- device or host pointers.
+ * Errors: EINVAL (n < 1, w < 0, k < 1, Q < 0, N < 1, k > N, NULL pointers),
+ * EUNSUPPORTED (p not 1 or 2, k > DTWLB_MAX_K), ENOMEM, ECUDA.  Q == 0 is a
+ * no-op.  Synchronous with respect to `stream`. */
+int nn_search(const float *queries, int64_t Q, const float *db, int64_t N, int32_t n, int32_t w,
+              int32_t p, int32_t k, int64_t *out_idx, float *out_dist, const nn_opts *opts,
+              nn_stats *stats, void *stream);
+
+/* Merge G per-shard k-NN lists into the global k-NN (sharded search, SURVEY
+ * 8(e)): in_idx/in_dist are device [G][Q][k] (shard lists, global indices,
+ * padded with (+inf, -1)); out_* device [Q][k].  The k smallest by
+ * (dist, idx) of the G*k entries per query.  Stream-ordered. */
+int nn_merge(const int64_t *in_idx, const float *in_dist, int32_t G, int64_t Q, int32_t k,
+             int64_t *out_idx, float *out_dist, void *stream);
+
+/* Last error message of the calling thread ("" if none). */
+const char *dtwlb_last_error(void);
+
+/* Release the library's cached device workspace (optional). */
+void dtwlb_release_workspace(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DTWLB_H */

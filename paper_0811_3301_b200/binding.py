@@ -1,0 +1,195 @@
+"""Thin ctypes binding over libdtwlb.so (include/dtwlb.h).
+
+Argument marshalling only: every step of the method runs in the library's CUDA
+kernels.  Names and argument order follow the C ABI.  Tensors are torch tensors
+(device memory from PyTorch; the current torch stream is passed as `stream`).
+There is no CPU fallback: if the library or a CUDA device is missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdtwlb.so")
+
+STATUS = {0: "OK", 1: "EINVAL", 2: "EUNSUPPORTED", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL"}
+KEOGH_ONLY = 1
+MAX_K = 1024
+
+
+class DtwlbError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{STATUS.get(status, status)}: {message}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class NnOpts(ctypes.Structure):
+    _fields_ = [("eps", ctypes.c_float), ("index_base", ctypes.c_int64), ("query_block", ctypes.c_int32),
+                ("flags", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
+
+
+class NnStats(ctypes.Structure):
+    _fields_ = [("pairs", ctypes.c_int64), ("keogh_evaluated", ctypes.c_int64),
+                ("improved_evaluated", ctypes.c_int64), ("dtw_evaluated", ctypes.c_int64),
+                ("dtw_abandoned", ctypes.c_int64), ("dtw_cells_nominal", ctypes.c_int64),
+                ("dtw_cells_computed", ctypes.c_int64), ("ms_envelope", ctypes.c_double),
+                ("ms_keogh", ctypes.c_double), ("ms_select", ctypes.c_double),
+                ("ms_improved", ctypes.c_double), ("ms_dtw", ctypes.c_double), ("ms_total", ctypes.c_double),
+                ("kernel_launches", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+EXPORTS = ["lb_envelope", "lb_keogh", "lb_improved", "dtw_band", "nn_search", "nn_merge",
+           "dtwlb_last_error", "dtwlb_release_workspace"]
+
+_lib = None
+
+
+def load():
+    """Load libdtwlb.so (raises if it has not been built: no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_0811_3301_b200.build`")
+        lib = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        lib.lb_envelope.argtypes = [vp, i32, i32, vp, vp, i64, vp]
+        lib.lb_keogh.argtypes = [vp, vp, i64, i64, i32, i32, vp, vp]
+        lib.lb_improved.argtypes = [vp, vp, vp, i64, i64, i32, i32, i32, vp, vp]
+        lib.dtw_band.argtypes = [vp, vp, i32, i32, i32, vp, i64, vp]
+        lib.nn_search.argtypes = [vp, i64, vp, i64, i32, i32, i32, i32, vp, vp,
+                                  ctypes.POINTER(NnOpts), ctypes.POINTER(NnStats), vp]
+        lib.nn_merge.argtypes = [vp, vp, i32, i64, i32, vp, vp, vp]
+        for f in ("lb_envelope", "lb_keogh", "lb_improved", "dtw_band", "nn_search", "nn_merge"):
+            getattr(lib, f).restype = ctypes.c_int
+        lib.dtwlb_last_error.restype = ctypes.c_char_p
+        lib.dtwlb_last_error.argtypes = []
+        lib.dtwlb_release_workspace.restype = None
+        _lib = lib
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise DtwlbError(status, load().dtwlb_last_error().decode())
+
+
+def _stream():
+    if not torch.cuda.is_available():
+        return None  # the library reports ECUDA itself
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dev(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != torch.float32:
+        raise TypeError(f"{name} must be float32")
+    return t.contiguous()
+
+
+def lb_envelope(x: torch.Tensor, w: int):
+    """U, L = envelope of each row of x [count][n]."""
+    x = _dev(x, "x")
+    n = x.shape[-1]
+    count = x.numel() // n if n else 0
+    U = torch.empty_like(x)
+    L = torch.empty_like(x)
+    _check(load().lb_envelope(x.data_ptr(), n, w, U.data_ptr(), L.data_ptr(), count, _stream()))
+    return U, L
+
+
+def lb_keogh(q_env: torch.Tensor, db: torch.Tensor, p: int) -> torch.Tensor:
+    """[Q][N] LB_Keogh_p (rooted); q_env is [2][Q][n] (U block, then L block)."""
+    q_env = _dev(q_env, "q_env")
+    db = _dev(db, "db")
+    Q, n = q_env.shape[1], q_env.shape[2]
+    N = db.shape[0]
+    out = torch.empty((Q, N), dtype=torch.float32, device=db.device)
+    _check(load().lb_keogh(q_env.data_ptr(), db.data_ptr(), Q, N, n, p, out.data_ptr(), _stream()))
+    return out
+
+
+def lb_improved(q: torch.Tensor, q_env: torch.Tensor, db: torch.Tensor, w: int, p: int) -> torch.Tensor:
+    """[Q][N] LB_Improved_p (rooted)."""
+    q, q_env, db = _dev(q, "q"), _dev(q_env, "q_env"), _dev(db, "db")
+    Q, n = q.shape
+    N = db.shape[0]
+    out = torch.empty((Q, N), dtype=torch.float32, device=db.device)
+    _check(load().lb_improved(q.data_ptr(), q_env.data_ptr(), db.data_ptr(), Q, N, n, w, p, out.data_ptr(),
+                              _stream()))
+    return out
+
+
+def dtw_band(x: torch.Tensor, y: torch.Tensor, w: int, p: int) -> torch.Tensor:
+    """DTW_p(x[r], y[r]) for each row pair (rooted)."""
+    x, y = _dev(x, "x"), _dev(y, "y")
+    count, n = x.shape
+    out = torch.empty(count, dtype=torch.float32, device=x.device)
+    _check(load().dtw_band(x.data_ptr(), y.data_ptr(), n, w, p, out.data_ptr(), count, _stream()))
+    return out
+
+
+def _opts(eps, index_base, query_block, keogh_only):
+    o = NnOpts()
+    o.eps = eps
+    o.index_base = index_base
+    o.query_block = query_block
+    o.flags = KEOGH_ONLY if keogh_only else 0
+    return o
+
+
+def nn_search(queries, db, w: int, p: int, k: int, *, eps: float = 1e-3, index_base: int = 0,
+              query_block: int = 0, keogh_only: bool = False, out=None, return_stats: bool = False):
+    """Exact k-NN under banded DTW_p.  Returns (idx int64 [Q][k], dist float32 [Q][k]).
+
+    queries/db may be CUDA tensors (device path) or host tensors / numpy arrays
+    (pinned host path: the library stages them; outputs are then host tensors).
+    ``out`` optionally supplies (idx, dist) output tensors.
+    """
+    host = not (isinstance(queries, torch.Tensor) and queries.is_cuda)
+    if host:
+        queries = torch.as_tensor(np.ascontiguousarray(queries, dtype=np.float32)) \
+            if not isinstance(queries, torch.Tensor) else queries.contiguous()
+        db = torch.as_tensor(np.ascontiguousarray(db, dtype=np.float32)) \
+            if not isinstance(db, torch.Tensor) else db.contiguous()
+    else:
+        queries, db = _dev(queries, "queries"), _dev(db, "db")
+    Q, n = queries.shape
+    N = db.shape[0]
+    if out is None:
+        dev = "cpu" if host else queries.device
+        idx = torch.empty((Q, k), dtype=torch.int64, device=dev, pin_memory=host)
+        dist = torch.empty((Q, k), dtype=torch.float32, device=dev, pin_memory=host)
+    else:
+        idx, dist = out
+    o = _opts(eps, index_base, query_block, keogh_only)
+    st = NnStats()
+    _check(load().nn_search(queries.data_ptr(), Q, db.data_ptr(), N, n, w, p, k, idx.data_ptr(),
+                            dist.data_ptr(), ctypes.byref(o), ctypes.byref(st) if return_stats else None,
+                            _stream()))
+    if return_stats:
+        return idx, dist, st.as_dict()
+    return idx, dist
+
+
+def nn_merge(in_idx: torch.Tensor, in_dist: torch.Tensor):
+    """Merge [G][Q][k] shard lists into the global [Q][k] (k smallest by (dist, idx))."""
+    G, Q, k = in_idx.shape
+    in_idx = in_idx.contiguous()
+    in_dist = _dev(in_dist, "in_dist")
+    idx = torch.empty((Q, k), dtype=torch.int64, device=in_idx.device)
+    dist = torch.empty((Q, k), dtype=torch.float32, device=in_idx.device)
+    _check(load().nn_merge(in_idx.data_ptr(), in_dist.data_ptr(), G, Q, k, idx.data_ptr(), dist.data_ptr(),
+                           _stream()))
+    return idx, dist
+
+
+def release_workspace():
+    load().dtwlb_release_workspace()

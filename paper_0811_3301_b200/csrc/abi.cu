@@ -1,0 +1,235 @@
+// abi.cu -- the extern "C" boundary of libdtwlb (declared in include/dtwlb.h):
+// argument validation, the thread-local error model, and dispatch to the kernels.
+#include <cstring>
+#include <mutex>
+
+#include "kernels.cuh"
+
+namespace dtwlb {
+
+int nn_search_impl(const float *queries, int64_t Q, const float *db, int64_t N, int n, int w, int p, int k,
+                   int64_t *out_idx, float *out_dist, const nn_opts *opts, nn_stats *stats, cudaStream_t st);
+int nn_merge_impl(const int64_t *in_idx, const float *in_dist, int G, int64_t Q, int k, int64_t *out_idx,
+                  float *out_dist, cudaStream_t st);
+int launch_dtw_generic(const DtwArgs &a, const float *yraw, float *scratch, int p, bool walk, cudaStream_t st);
+int ws_get_bytes(int slot, size_t bytes, void **out);
+std::mutex &api_mutex();
+void release_workspace();
+
+unsigned long long g_launches = 0;
+static thread_local char g_err[512] = "";
+
+void set_error(int code, const char *fmt, ...) {
+    (void)code;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char *what, const char *file, int line) {
+    set_error(DTWLB_ECUDA, "CUDA error %s (%s) at %s:%d in %s", cudaGetErrorName(e), cudaGetErrorString(e),
+              file, line, what);
+    return DTWLB_ECUDA;
+}
+
+int require_device() {
+    static int state = -1;  // -1 unknown, 0 ok, else status
+    static char msg[512];
+    if (state < 0) {
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        cudaDeviceProp prop;
+        if (e == cudaSuccess) e = cudaGetDeviceProperties(&prop, dev);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            snprintf(msg, sizeof(msg), "no usable CUDA device: %s", cudaGetErrorString(e));
+            state = DTWLB_ECUDA;
+        } else if (prop.major != 10) {
+            snprintf(msg, sizeof(msg), "device %s is sm_%d%d; libdtwlb is built for sm_100a only", prop.name,
+                     prop.major, prop.minor);
+            state = DTWLB_ECUDA;
+        } else {
+            state = DTWLB_OK;
+        }
+    }
+    if (state != DTWLB_OK) set_error(state, "%s", msg);
+    return state;
+}
+
+}  // namespace dtwlb
+
+using namespace dtwlb;
+
+#define CHECK_ARG(cond, ...)                      \
+    do {                                          \
+        if (!(cond)) {                            \
+            set_error(DTWLB_EINVAL, __VA_ARGS__); \
+            return DTWLB_EINVAL;                  \
+        }                                         \
+    } while (0)
+
+static int check_p(int p) {
+    if (p != 1 && p != 2) {
+        set_error(DTWLB_EUNSUPPORTED, "p = %d unsupported (p must be 1 or 2)", p);
+        return DTWLB_EUNSUPPORTED;
+    }
+    return DTWLB_OK;
+}
+
+extern "C" {
+
+const char *dtwlb_last_error(void) { return g_err; }
+
+void dtwlb_release_workspace(void) { release_workspace(); }
+
+int lb_envelope(const float *x, int32_t n, int32_t w, float *U, float *L, int64_t count, void *stream) {
+    g_err[0] = 0;
+    CHECK_ARG(n >= 1, "lb_envelope: n = %d < 1", n);
+    CHECK_ARG(w >= 0, "lb_envelope: w = %d < 0", w);
+    CHECK_ARG(count >= 0, "lb_envelope: count < 0");
+    if (count == 0) return DTWLB_OK;
+    CHECK_ARG(x && U && L, "lb_envelope: NULL pointer");
+    CHECK_ARG(U != L && (const float *)U != x && (const float *)L != x, "lb_envelope: outputs alias");
+    DTWLB_TRY(require_device());
+    return launch_envelope(x, n, w, U, L, count, as_stream(stream));
+}
+
+int lb_keogh(const float *q_env, const float *db, int64_t Q, int64_t N, int32_t n, int32_t p, float *out,
+             void *stream) {
+    g_err[0] = 0;
+    CHECK_ARG(n >= 1, "lb_keogh: n = %d < 1", n);
+    CHECK_ARG(Q >= 0 && N >= 0, "lb_keogh: negative size");
+    DTWLB_TRY(check_p(p));
+    if (Q == 0 || N == 0) return DTWLB_OK;
+    CHECK_ARG(q_env && db && out, "lb_keogh: NULL pointer");
+    DTWLB_TRY(require_device());
+    return launch_keogh(q_env, q_env + Q * n, db, Q, N, n, p, true, out, N, as_stream(stream));
+}
+
+int lb_improved(const float *q, const float *q_env, const float *db, int64_t Q, int64_t N, int32_t n,
+                int32_t w, int32_t p, float *out, void *stream) {
+    g_err[0] = 0;
+    CHECK_ARG(n >= 1, "lb_improved: n = %d < 1", n);
+    CHECK_ARG(w >= 0, "lb_improved: w = %d < 0", w);
+    CHECK_ARG(Q >= 0 && N >= 0, "lb_improved: negative size");
+    DTWLB_TRY(check_p(p));
+    if (Q == 0 || N == 0) return DTWLB_OK;
+    CHECK_ARG(q && q_env && db && out, "lb_improved: NULL pointer");
+    DTWLB_TRY(require_device());
+    const int epl = improved_epl(n);
+    if (epl == 0) {
+        set_error(DTWLB_EUNSUPPORTED, "lb_improved: n = %d > 1024 unsupported", n);
+        return DTWLB_EUNSUPPORTED;
+    }
+    std::lock_guard<std::mutex> lock(api_mutex());
+    cudaStream_t st = as_stream(stream);
+    const int npadE = 32 * epl;
+    const int64_t ldb = (N + 3) / 4 * 4;
+    float *beta1, *env, *qpad, *dbenv;
+    DTWLB_TRY(ws_get_bytes(0, sizeof(float) * Q * ldb, (void **)&beta1));
+    DTWLB_TRY(ws_get_bytes(1, sizeof(float) * 3 * Q * n, (void **)&env));
+    DTWLB_TRY(ws_get_bytes(2, sizeof(float) * 3 * Q * npadE, (void **)&qpad));
+    DTWLB_TRY(ws_get_bytes(3, sizeof(float) * 2 * N * n, (void **)&dbenv));
+    const float *U = q_env, *L = q_env + Q * n;
+    float *LU = env, *UL = env + Q * n, *scr = env + 2 * Q * n;
+    DTWLB_TRY(launch_keogh(U, L, db, Q, N, n, p, false, beta1, ldb, st));
+    DTWLB_TRY(launch_envelope(L, n, w, LU, scr, Q, st));
+    DTWLB_TRY(launch_envelope(U, n, w, scr, UL, Q, st));
+    DTWLB_TRY(launch_envelope(db, n, w, dbenv, dbenv + N * n, N, st));
+    // padded query-side arrays (host loop of copies: Q*n is small next to Q*N)
+    DTWLB_CUDA(cudaMemsetAsync(qpad, 0, sizeof(float) * 3 * Q * npadE, st));
+    DTWLB_CUDA(cudaMemcpy2DAsync(qpad, npadE * 4, q, n * 4, n * 4, Q, cudaMemcpyDeviceToDevice, st));
+    DTWLB_CUDA(cudaMemcpy2DAsync(qpad + Q * npadE, npadE * 4, LU, n * 4, n * 4, Q, cudaMemcpyDeviceToDevice, st));
+    DTWLB_CUDA(cudaMemcpy2DAsync(qpad + 2 * Q * npadE, npadE * 4, UL, n * 4, n * 4, Q, cudaMemcpyDeviceToDevice, st));
+    ImprovedArgs a{};
+    a.yq = qpad;
+    a.LUq = qpad + Q * npadE;
+    a.ULq = qpad + 2 * Q * npadE;
+    a.Ux = dbenv;
+    a.Lx = dbenv + N * n;
+    a.beta1 = beta1;
+    a.ldb = ldb;
+    a.Qb = Q;
+    a.N = N;
+    a.n = n;
+    a.npadE = npadE;
+    a.dense = out;
+    a.ldd = N;
+    DTWLB_TRY(launch_improved(a, p, false, true, st));
+    DTWLB_CUDA(cudaStreamSynchronize(st));  // workspace reuse safety
+    return DTWLB_OK;
+}
+
+int dtw_band(const float *x, const float *y, int32_t n, int32_t w, int32_t p, float *out, int64_t count,
+             void *stream) {
+    g_err[0] = 0;
+    CHECK_ARG(n >= 1, "dtw_band: n = %d < 1", n);
+    CHECK_ARG(w >= 0, "dtw_band: w = %d < 0", w);
+    CHECK_ARG(count >= 0, "dtw_band: count < 0");
+    DTWLB_TRY(check_p(p));
+    if (count == 0) return DTWLB_OK;
+    CHECK_ARG(x && y && out, "dtw_band: NULL pointer");
+    DTWLB_TRY(require_device());
+    std::lock_guard<std::mutex> lock(api_mutex());
+    cudaStream_t st = as_stream(stream);
+    w = w > n - 1 ? n - 1 : w;
+    DtwArgs a{};
+    a.db = x;
+    a.n = n;
+    a.w = w;
+    a.total = count;
+    a.res = out;
+    if (w > 64) {
+        float *scratch;
+        DTWLB_TRY(ws_get_bytes(4, sizeof(float) * count * (2 * w + 2), (void **)&scratch));
+        DTWLB_TRY(launch_dtw_generic(a, y, scratch, p, false, st));
+    } else {
+        const int LP = dtw_padded_len(n);
+        float *ysh;
+        DTWLB_TRY(ws_get_bytes(5, sizeof(float) * 4 * count * LP, (void **)&ysh));
+        DTWLB_TRY(launch_build_ysh(y, count, n, ysh, LP, st));
+        a.ysh = ysh;
+        a.ysh_stride_s = count * LP;
+        a.LP = LP;
+        DTWLB_TRY(launch_dtw(a, p, false, st));
+    }
+    DTWLB_CUDA(cudaStreamSynchronize(st));
+    return DTWLB_OK;
+}
+
+int nn_search(const float *queries, int64_t Q, const float *db, int64_t N, int32_t n, int32_t w, int32_t p,
+              int32_t k, int64_t *out_idx, float *out_dist, const nn_opts *opts, nn_stats *stats, void *stream) {
+    g_err[0] = 0;
+    if (stats) memset(stats, 0, sizeof(*stats));
+    CHECK_ARG(n >= 1, "nn_search: n = %d < 1", n);
+    CHECK_ARG(w >= 0, "nn_search: w = %d < 0", w);
+    CHECK_ARG(k >= 1, "nn_search: k = %d < 1", k);
+    CHECK_ARG(Q >= 0, "nn_search: Q < 0");
+    CHECK_ARG(N >= 1, "nn_search: empty database (N = %lld)", (long long)N);
+    CHECK_ARG(k <= N, "nn_search: k = %d > N = %lld", k, (long long)N);
+    CHECK_ARG(N <= 0xffffffffLL, "nn_search: N above 2^32 per shard");
+    DTWLB_TRY(check_p(p));
+    if (k > DTWLB_MAX_K) {
+        set_error(DTWLB_EUNSUPPORTED, "nn_search: k = %d > DTWLB_MAX_K = %d", k, DTWLB_MAX_K);
+        return DTWLB_EUNSUPPORTED;
+    }
+    if (Q == 0) return DTWLB_OK;
+    CHECK_ARG(queries && db && out_idx && out_dist, "nn_search: NULL pointer");
+    CHECK_ARG(opts == nullptr || opts->eps >= 0.f, "nn_search: eps < 0");
+    DTWLB_TRY(require_device());
+    return nn_search_impl(queries, Q, db, N, n, w, p, k, out_idx, out_dist, opts, stats, as_stream(stream));
+}
+
+int nn_merge(const int64_t *in_idx, const float *in_dist, int32_t G, int64_t Q, int32_t k, int64_t *out_idx,
+             float *out_dist, void *stream) {
+    g_err[0] = 0;
+    CHECK_ARG(G >= 1 && G <= 64, "nn_merge: G = %d outside [1, 64]", G);
+    CHECK_ARG(Q >= 0 && k >= 1, "nn_merge: bad sizes");
+    if (Q == 0) return DTWLB_OK;
+    CHECK_ARG(in_idx && in_dist && out_idx && out_dist, "nn_merge: NULL pointer");
+    DTWLB_TRY(require_device());
+    return nn_merge_impl(in_idx, in_dist, G, Q, k, out_idx, out_dist, as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,78 @@
+// common.cuh -- shared plumbing of libdtwlb (error model, small device helpers).
+// Product code only: nothing here is shared with oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/dtwlb.h"
+
+namespace dtwlb {
+
+// ---- error model: thread-local message, status codes never exceptions ----
+void set_error(int code, const char *fmt, ...);
+int cuda_fail(cudaError_t e, const char *what, const char *file, int line);
+
+#define DTWLB_CUDA(call)                                                           \
+    do {                                                                           \
+        cudaError_t e_ = (call);                                                   \
+        if (e_ != cudaSuccess) return ::dtwlb::cuda_fail(e_, #call, __FILE__, __LINE__); \
+    } while (0)
+
+// every kernel launch site is followed by DTWLB_LAUNCH_CHECK(), which also counts
+// the launch (nn_stats.kernel_launches reports the count of one nn_search call)
+extern unsigned long long g_launches;
+#define DTWLB_LAUNCH_CHECK()                                   \
+    do {                                                       \
+        __atomic_fetch_add(&::dtwlb::g_launches, 1ull, __ATOMIC_RELAXED); \
+        DTWLB_CUDA(cudaGetLastError());                        \
+    } while (0)
+
+#define DTWLB_TRY(expr)            \
+    do {                           \
+        int s_ = (expr);           \
+        if (s_ != DTWLB_OK) return s_; \
+    } while (0)
+
+// One-time device check: an sm_100 device must be current.
+int require_device();
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+constexpr float kInf = __builtin_huge_valf();
+
+// ---- device helpers ----
+__device__ __forceinline__ float min3f(float a, float b, float c) { return fminf(fminf(a, b), c); }
+__device__ __forceinline__ float max3f(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
+
+// |t|^P for P in {1,2}: the cost term |x_i - y_j|^p of P:207 and the bound terms.
+template <int P>
+__device__ __forceinline__ float powp(float t) {
+    if constexpr (P == 1) return fabsf(t);
+    else return t * t;
+}
+// acc + d^P with d >= 0 (one FADD or one FFMA).
+template <int P>
+__device__ __forceinline__ float accp(float acc, float d) {
+    if constexpr (P == 1) return acc + d;
+    else return fmaf(d, d, acc);
+}
+template <int P>
+__device__ __forceinline__ float rootp(float v) {
+    if constexpr (P == 1) return v;
+    else return sqrtf(v);
+}
+
+// (dist, idx) ordering key: non-negative float bits are monotone (reading c17: -0 -> +0).
+__device__ __forceinline__ unsigned long long pack_key(float d, uint32_t idx) {
+    d = fmaxf(d, 0.0f);
+    return (static_cast<unsigned long long>(__float_as_uint(d)) << 32) | idx;
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace dtwlb

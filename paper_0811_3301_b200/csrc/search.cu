@@ -1,0 +1,655 @@
+// search.cu -- nn_search: exact k-NN under banded DTW_p by the paper's cascade
+// (Alg. 3), generalised to p in {1,2}, k >= 1 and many queries.
+//
+// Host runtime (per block of Qb queries, all device-side data):
+//   a1  envelopes U,L of the queries (+ LU = U(L), UL = L(U) for LB_Improved) and
+//       U(x), L(x) of the database (once per call)                  [envelope.cu]
+//   a2  beta1 = LB_Keogh^p for every (query, candidate) pair          [keogh.cu]
+//   a3  best-first ordering:  a sampled quantile t_S of each query's beta1 row
+//       splits its candidates into a small first range (beta1 <= t_S, ~S pairs)
+//       and the rest.  Range 1 is bounded, sorted by LB_Improved and walked in
+//       ascending order with growing DTW batches; this drives tau (the k-th best)
+//       down to ~its final value.  Range 2 (t_S < beta1 <= tau(1+eps)) is then
+//       filtered by LB_Improved against that tau, sorted, and walked the same way.
+//       Correctness never depends on the order: every candidate with
+//       beta1 <= tau_final(1+eps) is in range 1 or range 2.
+//   a4  LB_Improved on each range's survivors -> per-query key lists (beta_lb, c)
+//                                                                     [improved.cu]
+//   a5  DTW walk: rounds of (plan -> DTW batch with early abandon -> top-k merge);
+//       a query stops when its next sorted bound exceeds tau(1+eps)     [dtw.cu]
+//   a6  finalize: k smallest by (DTW^p, index), rooted.
+// Pruning rule (reading c3/c13): a bound prunes only if bound > tau^p (1 + eps).
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace dtwlb {
+
+int launch_dtw_generic(const DtwArgs &a, const float *yraw, float *scratch, int p, bool walk,
+                       cudaStream_t st);
+
+// ------------------------------------------------------------------ workspace
+namespace {
+
+struct Workspace {
+    std::vector<void *> ptr;
+    std::vector<size_t> size;
+    ~Workspace() { release(); }
+    void release() {
+        for (void *p : ptr)
+            if (p) cudaFree(p);
+        ptr.clear();
+        size.clear();
+    }
+    int get(int slot, size_t bytes, void **out) {
+        if ((int)ptr.size() <= slot) { ptr.resize(slot + 1, nullptr); size.resize(slot + 1, 0); }
+        bytes = std::max<size_t>(bytes, 256);
+        if (size[slot] < bytes) {
+            if (ptr[slot]) { cudaDeviceSynchronize(); cudaFree(ptr[slot]); ptr[slot] = nullptr; size[slot] = 0; }
+            cudaError_t e = cudaMalloc(&ptr[slot], bytes);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                set_error(DTWLB_ENOMEM, "device workspace: cannot allocate %zu bytes (%s)", bytes,
+                          cudaGetErrorString(e));
+                return DTWLB_ENOMEM;
+            }
+            size[slot] = bytes;
+        }
+        *out = ptr[slot];
+        return DTWLB_OK;
+    }
+};
+
+Workspace &ws() {
+    static Workspace w;
+    return w;
+}
+std::mutex &ws_mutex() {
+    static std::mutex m;
+    return m;
+}
+
+enum Slot {
+    S_QSTAGE, S_DBSTAGE, S_ENV, S_QPAD, S_YSH, S_DBENV, S_BETA1, S_LIST, S_RES, S_STATE, S_TOPK,
+    S_OUTSTAGE, S_SCRATCH, S_TMP, S_COUNT
+};
+
+template <typename T>
+int wsget(int slot, size_t count, T **out) {
+    void *p = nullptr;
+    DTWLB_TRY(ws().get(slot, count * sizeof(T), &p));
+    *out = static_cast<T *>(p);
+    return DTWLB_OK;
+}
+
+// ------------------------------------------------------------------ kernels
+// Padded copies of the query-side LB_Improved arrays: [Q][npadE], zero padded.
+__global__ void pad_rows_kernel(const float *__restrict__ src, int64_t rows, int n, float *__restrict__ dst,
+                                int npad) {
+    const int64_t total = rows * (int64_t)npad;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = t / npad;
+        int i = (int)(t - r * npad);
+        dst[t] = i < n ? src[r * n + i] : 0.f;
+    }
+}
+
+// Sampled quantile of each query's beta1 row: t_S such that ~S candidates have
+// beta1 <= t_S (selection threshold only -- correctness does not depend on it).
+constexpr int kSample = 2048;
+__global__ void __launch_bounds__(512) sample_threshold_kernel(const float *__restrict__ beta1, int64_t ldb,
+                                                               int64_t N, int64_t S, float *__restrict__ tS) {
+    __shared__ float v[kSample];
+    const int64_t q = blockIdx.x;
+    const int M = N < kSample ? (int)N : kSample;
+    for (int s = threadIdx.x; s < kSample; s += blockDim.x) {
+        int64_t c = (int64_t)s * N / M;
+        v[s] = s < M ? beta1[q * ldb + c] : kInf;
+    }
+    __syncthreads();
+    // bitonic sort of kSample floats
+    for (int k = 2; k <= kSample; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int t = threadIdx.x; t < kSample; t += blockDim.x) {
+                int u = t ^ j;
+                if (u > t) {
+                    bool up = (t & k) == 0;
+                    float a = v[t], b = v[u];
+                    if ((a > b) == up) { v[t] = b; v[u] = a; }
+                }
+            }
+            __syncthreads();
+        }
+    if (threadIdx.x == 0) {
+        float t;
+        if (S >= N) t = kInf;
+        else {
+            int64_t r = (S * M + N - 1) / N;  // rank in the sample
+            r = r < 1 ? 1 : (r > M ? M : r);
+            t = v[r - 1];
+        }
+        tS[q] = t;
+    }
+}
+
+// Bitonic sort of runs of kRun u64 keys per query list (ascending (beta_lb, c)).
+constexpr int kRun = 4096;
+__global__ void __launch_bounds__(1024) sort_runs_kernel(unsigned long long *__restrict__ list, int64_t cap,
+                                                         const int *__restrict__ run_q,
+                                                         const int *__restrict__ run_idx,
+                                                         const int *__restrict__ len) {
+    __shared__ unsigned long long v[kRun];
+    const int q = run_q[blockIdx.x], r = run_idx[blockIdx.x];
+    const int64_t base = (int64_t)q * cap + (int64_t)r * kRun;
+    const int m = min(kRun, len[q] - r * kRun);
+    int P2 = 1;
+    while (P2 < m) P2 <<= 1;
+    for (int t = threadIdx.x; t < P2; t += blockDim.x) v[t] = t < m ? list[base + t] : ~0ull;
+    __syncthreads();
+    for (int k = 2; k <= P2; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int t = threadIdx.x; t < P2; t += blockDim.x) {
+                int u = t ^ j;
+                if (u > t) {
+                    bool up = (t & k) == 0;
+                    unsigned long long a = v[t], b = v[u];
+                    if ((a > b) == up) { v[t] = b; v[u] = a; }
+                }
+            }
+            __syncthreads();
+        }
+    for (int t = threadIdx.x; t < m; t += blockDim.x) list[base + t] = v[t];
+}
+
+struct QState {
+    float *thr;      // tau^p (1+eps) (+inf until k results)
+    float *lo, *hi;  // current range of beta1
+    float *tS;
+    int *len, *pos, *rnd, *active;
+    int *item_off;   // [Qb+1]
+    int *counters;   // [0] total items of the round, [1] active queries
+    unsigned long long *topk;  // [Qb][k]
+    int *topk_n;
+    unsigned long long *stat;  // [0] improved evals, [1] dtw items started, [2] cells, [3] abandoned
+};
+
+__global__ void init_state_kernel(QState s, int Qb, int k) {
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < Qb; q += gridDim.x * blockDim.x) {
+        s.thr[q] = kInf;
+        s.topk_n[q] = 0;
+        for (int j = 0; j < k; ++j) s.topk[(int64_t)q * k + j] = ~0ull;
+    }
+}
+
+__global__ void set_range_kernel(QState s, int Qb, int macro) {
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < Qb; q += gridDim.x * blockDim.x) {
+        s.lo[q] = macro == 0 ? -kInf : s.tS[q];
+        s.hi[q] = macro == 0 ? s.tS[q] : kInf;
+        s.len[q] = 0;
+    }
+}
+
+__global__ void start_walk_kernel(QState s, int Qb) {
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < Qb; q += gridDim.x * blockDim.x) {
+        s.pos[q] = 0;
+        s.rnd[q] = 0;
+        s.active[q] = s.len[q] > 0;
+    }
+}
+
+// Per-round plan: items of each active query = min(D0 * 2^round, remaining); exclusive scan.
+constexpr int kD0 = 32, kDMax = 65536;
+__global__ void __launch_bounds__(1024) plan_kernel(QState s, int Qb) {
+    __shared__ int warp_sums[32];
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < Qb; base += blockDim.x) {
+        const int q = base + threadIdx.x;
+        int cnt = 0;
+        if (q < Qb && s.active[q]) {
+            int d = kD0 << min(s.rnd[q], 11);
+            d = min(d, kDMax);
+            cnt = min(d, s.len[q] - s.pos[q]);
+        }
+        // block-wide inclusive scan
+        int v = cnt;
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += t;
+        }
+        if (lane == 31) warp_sums[wid] = v;
+        __syncthreads();
+        if (wid == 0) {
+            int ws_ = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int t = __shfl_up_sync(0xffffffffu, ws_, o);
+                if (lane >= o) ws_ += t;
+            }
+            warp_sums[lane] = ws_;
+        }
+        __syncthreads();
+        const int excl = carry + v - cnt + (wid ? warp_sums[wid - 1] : 0);
+        if (q < Qb) s.item_off[q] = excl;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry = excl + cnt;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        s.item_off[Qb] = carry;
+        s.counters[0] = carry;
+    }
+}
+
+// Merge a round's DTW results into each query's top-k; advance its walk.
+__global__ void merge_kernel(QState s, int Qb, int k, float eps, const unsigned long long *__restrict__ list,
+                             int64_t cap, const float *__restrict__ res) {
+    const int lane = threadIdx.x & 31;
+    const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (q >= Qb) return;
+    const int o0 = s.item_off[q], o1 = s.item_off[q + 1];
+    if (o0 == o1) return;
+    unsigned long long *tk = s.topk + (int64_t)q * k;
+    const unsigned long long *lq = list + (int64_t)q * cap;
+    const int p0 = s.pos[q];
+    int cnt = s.topk_n[q];
+    unsigned long long kth = tk[k - 1];
+    for (int b = o0; b < o1; b += 32) {
+        const int t = b + lane;
+        unsigned long long key = ~0ull;
+        if (t < o1) {
+            const float d = res[t];
+            if (d < kInf) key = pack_key(d, (uint32_t)(lq[p0 + (t - o0)] & 0xffffffffu));
+        }
+        unsigned m = __ballot_sync(0xffffffffu, key < kth);
+        while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const unsigned long long kk = __shfl_sync(0xffffffffu, key, src);
+            if (kk >= kth) continue;  // kth may have tightened
+            if (lane == 0) {  // sorted insertion of kk, dropping the current k-th
+                int j = min(cnt, k - 1);
+                while (j > 0 && tk[j - 1] > kk) { tk[j] = tk[j - 1]; --j; }
+                tk[j] = kk;
+                cnt = min(cnt + 1, k);
+            }
+            cnt = __shfl_sync(0xffffffffu, cnt, 0);
+            __syncwarp();
+            kth = tk[k - 1];
+        }
+    }
+    if (lane == 0) {
+        s.topk_n[q] = cnt;
+        float thr = kInf;
+        if (cnt >= k) thr = __uint_as_float((uint32_t)(kth >> 32)) * (1.0f + eps);
+        s.thr[q] = thr;
+        // advance; skip the rest of a sorted run once its next bound exceeds thr
+        int pos = p0 + (o1 - o0);
+        const int len = s.len[q];
+        while (pos < len && __uint_as_float((uint32_t)(lq[pos] >> 32)) > thr)
+            pos = (pos / kRun + 1) * kRun;
+        s.pos[q] = pos;
+        s.rnd[q] += 1;
+        s.active[q] = pos < len;
+    }
+}
+
+__global__ void finalize_kernel(const unsigned long long *__restrict__ topk, int Qb, int k, int p,
+                                int64_t index_base, int64_t *__restrict__ out_idx, float *__restrict__ out_dist) {
+    const int64_t total = (int64_t)Qb * k;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long key = topk[t];
+        if (key == ~0ull) { out_idx[t] = -1; out_dist[t] = kInf; continue; }
+        const float d = __uint_as_float((uint32_t)(key >> 32));
+        out_dist[t] = p == 1 ? d : sqrtf(d);
+        out_idx[t] = index_base + (int64_t)(key & 0xffffffffu);
+    }
+}
+
+// k-way shard merge: k smallest by (dist, idx) of G lists per query.
+__global__ void nn_merge_kernel(const int64_t *__restrict__ in_idx, const float *__restrict__ in_dist, int G,
+                                int64_t Q, int k, int64_t *__restrict__ out_idx, float *__restrict__ out_dist) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= Q) return;
+    // G-way merge of sorted lists (each list ascending in (dist, idx))
+    int head[64];
+    for (int g = 0; g < G; ++g) head[g] = 0;
+    for (int r = 0; r < k; ++r) {
+        int best = -1;
+        float bd = kInf;
+        int64_t bi = 0x7fffffffffffffffLL;
+        for (int g = 0; g < G; ++g) {
+            if (head[g] >= k) continue;
+            const int64_t o = ((int64_t)g * Q + q) * k + head[g];
+            const int64_t ii = in_idx[o];
+            if (ii < 0) continue;
+            const float dd = in_dist[o];
+            if (best < 0 || dd < bd || (dd == bd && ii < bi)) { best = g; bd = dd; bi = ii; }
+        }
+        if (best < 0) { out_idx[q * k + r] = -1; out_dist[q * k + r] = kInf; continue; }
+        ++head[best];
+        out_idx[q * k + r] = bi;
+        out_dist[q * k + r] = bd;
+    }
+}
+
+bool is_device_ptr(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+struct Timer {
+    bool on;
+    cudaStream_t st;
+    cudaEvent_t e[8];
+    int n = 0;
+    Timer(bool on_, cudaStream_t s) : on(on_), st(s) {
+        if (on) for (auto &x : e) cudaEventCreate(&x);
+    }
+    ~Timer() { if (on) for (auto &x : e) cudaEventDestroy(x); }
+    void mark() { if (on && n < 8) cudaEventRecord(e[n++], st); }
+    double ms(int a, int b) {
+        float v = 0;
+        if (on && b < n) cudaEventElapsedTime(&v, e[a], e[b]);
+        return v;
+    }
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------ pipeline
+int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64_t N, int n, int w, int p,
+                   int k, int64_t *out_idx_in, float *out_dist_in, const nn_opts *opts, nn_stats *stats,
+                   cudaStream_t st) {
+    std::lock_guard<std::mutex> lock(ws_mutex());
+    const float eps = opts ? opts->eps : 1e-3f;
+    const int64_t index_base = opts ? opts->index_base : 0;
+    const bool keogh_only = opts && (opts->flags & DTWLB_KEOGH_ONLY);
+    w = std::min(w, n - 1);
+    Timer tm(stats != nullptr, st);
+    tm.mark();  // 0
+    const unsigned long long launches0 = __atomic_load_n(&g_launches, __ATOMIC_RELAXED);
+
+    // ---- stage host inputs (e2e path) ----
+    const float *queries = queries_in, *db = db_in;
+    if (!is_device_ptr(queries_in)) {
+        float *d;
+        DTWLB_TRY(wsget(S_QSTAGE, (size_t)Q * n, &d));
+        DTWLB_CUDA(cudaMemcpyAsync(d, queries_in, sizeof(float) * Q * n, cudaMemcpyHostToDevice, st));
+        queries = d;
+    }
+    if (!is_device_ptr(db_in)) {
+        float *d;
+        DTWLB_TRY(wsget(S_DBSTAGE, (size_t)N * n, &d));
+        DTWLB_CUDA(cudaMemcpyAsync(d, db_in, sizeof(float) * N * n, cudaMemcpyHostToDevice, st));
+        db = d;
+    }
+    const bool out_dev = is_device_ptr(out_idx_in) && is_device_ptr(out_dist_in);
+    int64_t *out_idx = out_idx_in;
+    float *out_dist = out_dist_in;
+    if (!out_dev) {
+        char *d;
+        DTWLB_TRY(wsget(S_OUTSTAGE, (size_t)Q * k * 12, &d));
+        out_idx = reinterpret_cast<int64_t *>(d);
+        out_dist = reinterpret_cast<float *>(d + (size_t)Q * k * 8);
+    }
+
+    // ---- a1: envelopes ----
+    const int epl = improved_epl(n);
+    const int npadE = 32 * std::max(epl, 4);
+    const bool fast_improved = epl != 0;
+    float *env;  // U, L, LU, UL, scratch: [5][Q][n]
+    DTWLB_TRY(wsget(S_ENV, (size_t)5 * Q * n, &env));
+    float *U = env, *L = env + (size_t)Q * n, *LU = env + 2 * (size_t)Q * n, *UL = env + 3 * (size_t)Q * n,
+          *scr = env + 4 * (size_t)Q * n;
+    DTWLB_TRY(launch_envelope(queries, n, w, U, L, Q, st));
+    DTWLB_TRY(launch_envelope(L, n, w, LU, scr, Q, st));   // LU = U(L(y))
+    DTWLB_TRY(launch_envelope(U, n, w, scr, UL, Q, st));   // UL = L(U(y))
+    float *qpad;  // y, LU, UL padded: [3][Q][npadE]
+    DTWLB_TRY(wsget(S_QPAD, (size_t)3 * Q * npadE, &qpad));
+    {
+        const int grid = (int)std::min<int64_t>(ceil_div(Q * npadE, 256), 148 * 8);
+        pad_rows_kernel<<<grid, 256, 0, st>>>(queries, Q, n, qpad, npadE);
+        DTWLB_LAUNCH_CHECK();
+        pad_rows_kernel<<<grid, 256, 0, st>>>(LU, Q, n, qpad + (size_t)Q * npadE, npadE);
+        DTWLB_LAUNCH_CHECK();
+        pad_rows_kernel<<<grid, 256, 0, st>>>(UL, Q, n, qpad + 2 * (size_t)Q * npadE, npadE);
+        DTWLB_LAUNCH_CHECK();
+    }
+    const bool generic_dtw = w > 64;
+    const int LP = dtw_padded_len(n);
+    float *ysh = nullptr;
+    if (!generic_dtw) {
+        DTWLB_TRY(wsget(S_YSH, (size_t)4 * Q * LP, &ysh));
+        DTWLB_TRY(launch_build_ysh(queries, Q, n, ysh, LP, st));
+    }
+    float *dbenv;  // U(x), L(x): [2][N][n]
+    DTWLB_TRY(wsget(S_DBENV, (size_t)2 * N * n, &dbenv));
+    if (!keogh_only) DTWLB_TRY(launch_envelope(db, n, w, dbenv, dbenv + (size_t)N * n, N, st));
+    tm.mark();  // 1
+
+    // ---- query block size from free memory: beta1 (4N) + list (8N) + res (4N) per query ----
+    size_t free_b = 0, total_b = 0;
+    DTWLB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const size_t per_q = (size_t)N * 16 + 4096;
+    int64_t Qb = opts && opts->query_block > 0 ? opts->query_block : (int64_t)(free_b * 0.45 / per_q);
+    Qb = std::max<int64_t>(1, std::min<int64_t>(Qb, Q));
+    if (Qb >= 64) Qb = Qb / 64 * 64;
+    const int64_t cap = N;
+    const int64_t ldb = (N + 3) / 4 * 4;
+
+    float *beta1;
+    unsigned long long *list;
+    float *res;
+    DTWLB_TRY(wsget(S_BETA1, (size_t)Qb * ldb, &beta1));
+    DTWLB_TRY(wsget(S_LIST, (size_t)Qb * cap, &list));
+    const int64_t res_cap = std::min<int64_t>(Qb * cap, Qb * (int64_t)kDMax);
+    DTWLB_TRY(wsget(S_RES, (size_t)res_cap, &res));
+    char *stb;
+    const size_t st_bytes = 16 * ((size_t)Qb * 4 * 8 + (Qb + 1) * 4 + 64 + 64 + 16 * 16) / 16;
+    DTWLB_TRY(wsget(S_STATE, st_bytes, &stb));
+    QState s;
+    {
+        char *p_ = stb;
+        auto take = [&](size_t bytes) { char *r = p_; p_ += (bytes + 15) / 16 * 16; return r; };
+        s.stat = reinterpret_cast<unsigned long long *>(take(8 * 8));
+        s.counters = reinterpret_cast<int *>(take(64));
+        s.thr = reinterpret_cast<float *>(take(Qb * 4));
+        s.lo = reinterpret_cast<float *>(take(Qb * 4));
+        s.hi = reinterpret_cast<float *>(take(Qb * 4));
+        s.tS = reinterpret_cast<float *>(take(Qb * 4));
+        s.len = reinterpret_cast<int *>(take(Qb * 4));
+        s.pos = reinterpret_cast<int *>(take(Qb * 4));
+        s.rnd = reinterpret_cast<int *>(take(Qb * 4));
+        s.active = reinterpret_cast<int *>(take(Qb * 4));
+        s.item_off = reinterpret_cast<int *>(take((Qb + 1) * 4));
+    }
+    DTWLB_TRY(wsget(S_TOPK, (size_t)Qb * k, &s.topk));
+    int *topk_n;
+    DTWLB_TRY(wsget(S_TMP, (size_t)Qb + 64, &topk_n));
+    s.topk_n = topk_n;
+    float *scratch = nullptr;
+    if (generic_dtw) DTWLB_TRY(wsget(S_SCRATCH, (size_t)res_cap * (2 * w + 2), &scratch));
+    DTWLB_CUDA(cudaMemsetAsync(s.stat, 0, 8 * 8, st));
+
+    // target size of the first (best-first) range
+    const int64_t S = std::max<int64_t>(std::max<int64_t>(256, 4LL * k), std::min<int64_t>(8192, N / 64));
+
+    std::vector<int> h_len(Qb), run_q, run_idx;
+    int *d_runs;
+    double ms_keogh = 0, ms_select = 0, ms_improved = 0, ms_dtw = 0;
+    cudaEvent_t ev[4];
+    if (stats) for (auto &e : ev) cudaEventCreate(&e);
+
+    for (int64_t qb0 = 0; qb0 < Q; qb0 += Qb) {
+        const int64_t qn = std::min<int64_t>(Qb, Q - qb0);
+        // ---- a2: LB_Keogh for the block ----
+        if (stats) cudaEventRecord(ev[0], st);
+        DTWLB_TRY(launch_keogh(U + qb0 * n, L + qb0 * n, db, qn, N, n, p, false, beta1, ldb, st));
+        if (stats) cudaEventRecord(ev[1], st);
+        init_state_kernel<<<(unsigned)ceil_div(qn, 256), 256, 0, st>>>(s, (int)qn, k);
+        DTWLB_LAUNCH_CHECK();
+        sample_threshold_kernel<<<(unsigned)qn, 512, 0, st>>>(beta1, ldb, N, S, s.tS);
+        DTWLB_LAUNCH_CHECK();
+        if (stats) {
+            cudaEventRecord(ev[2], st);
+            cudaEventSynchronize(ev[2]);
+            float a = 0, b = 0;
+            cudaEventElapsedTime(&a, ev[0], ev[1]);
+            cudaEventElapsedTime(&b, ev[1], ev[2]);
+            ms_keogh += a;
+            ms_select += b;
+        }
+
+        for (int macro = 0; macro < 2; ++macro) {
+            set_range_kernel<<<(unsigned)ceil_div(qn, 256), 256, 0, st>>>(s, (int)qn, macro);
+            DTWLB_LAUNCH_CHECK();
+            if (stats) cudaEventRecord(ev[0], st);
+            // ---- a4: LB_Improved on the range's LB_Keogh survivors ----
+            if (fast_improved) {
+                ImprovedArgs ia{};
+                ia.yq = qpad + qb0 * npadE;
+                ia.LUq = qpad + (size_t)Q * npadE + qb0 * npadE;
+                ia.ULq = qpad + 2 * (size_t)Q * npadE + qb0 * npadE;
+                ia.Ux = dbenv;
+                ia.Lx = dbenv + (size_t)N * n;
+                ia.beta1 = beta1;
+                ia.ldb = ldb;
+                ia.Qb = qn;
+                ia.N = N;
+                ia.n = n;
+                ia.npadE = npadE;
+                ia.lo = s.lo;
+                ia.hi = s.hi;
+                ia.thr = s.thr;
+                ia.list = list;
+                ia.cap = cap;
+                ia.list_len = s.len;
+                ia.n_eval = s.stat + 0;
+                DTWLB_TRY(launch_improved(ia, p, keogh_only, false, st));
+            } else {
+                set_error(DTWLB_EUNSUPPORTED, "nn_search: n = %d > 1024 not supported", n);
+                return DTWLB_EUNSUPPORTED;
+            }
+            // ---- a3: sort each query's list in runs ----
+            DTWLB_CUDA(cudaMemcpyAsync(h_len.data(), s.len, sizeof(int) * qn, cudaMemcpyDeviceToHost, st));
+            DTWLB_CUDA(cudaStreamSynchronize(st));
+            run_q.clear();
+            run_idx.clear();
+            for (int q = 0; q < qn; ++q)
+                for (int r = 0; r * kRun < h_len[q]; ++r) { run_q.push_back(q); run_idx.push_back(r); }
+            if (!run_q.empty()) {
+                const size_t nr = run_q.size();
+                DTWLB_TRY(wsget(S_COUNT, nr * 2 + 64, &d_runs));
+                DTWLB_CUDA(cudaMemcpyAsync(d_runs, run_q.data(), nr * 4, cudaMemcpyHostToDevice, st));
+                DTWLB_CUDA(cudaMemcpyAsync(d_runs + nr, run_idx.data(), nr * 4, cudaMemcpyHostToDevice, st));
+                sort_runs_kernel<<<(unsigned)nr, 1024, 0, st>>>(list, cap, d_runs, d_runs + nr, s.len);
+                DTWLB_LAUNCH_CHECK();
+            }
+            if (stats) cudaEventRecord(ev[1], st);
+            // ---- a5: DTW walk ----
+            start_walk_kernel<<<(unsigned)ceil_div(qn, 256), 256, 0, st>>>(s, (int)qn);
+            DTWLB_LAUNCH_CHECK();
+            for (int round = 0;; ++round) {
+                plan_kernel<<<1, 1024, 0, st>>>(s, (int)qn);
+                DTWLB_LAUNCH_CHECK();
+                int total = 0;
+                DTWLB_CUDA(cudaMemcpyAsync(&total, s.counters, sizeof(int), cudaMemcpyDeviceToHost, st));
+                DTWLB_CUDA(cudaStreamSynchronize(st));
+                if (total == 0) break;
+                DtwArgs da{};
+                da.ysh = ysh;
+                da.ysh_stride_s = (int64_t)Q * LP;
+                da.LP = LP;
+                da.db = db;
+                da.n = n;
+                da.w = w;
+                da.item_off = s.item_off;
+                da.pos = s.pos;
+                da.list = list;
+                da.cap = cap;
+                da.Qb = (int)qn;
+                da.thr = s.thr;
+                da.total = total;
+                da.res = res;
+                da.cells = s.stat + 2;
+                da.abandoned = s.stat + 3;
+                da.started = s.stat + 1;
+                if (generic_dtw) DTWLB_TRY(launch_dtw_generic(da, queries + qb0 * n, scratch, p, true, st));
+                else {
+                    da.ysh = ysh + qb0 * LP;
+                    DTWLB_TRY(launch_dtw(da, p, true, st));
+                }
+                merge_kernel<<<(unsigned)ceil_div(qn * 32, 256), 256, 0, st>>>(s, (int)qn, k, eps, list, cap, res);
+                DTWLB_LAUNCH_CHECK();
+            }
+            if (stats) {
+                cudaEventRecord(ev[2], st);
+                cudaEventSynchronize(ev[2]);
+                float a = 0, b = 0;
+                cudaEventElapsedTime(&a, ev[0], ev[1]);
+                cudaEventElapsedTime(&b, ev[1], ev[2]);
+                ms_improved += a;
+                ms_dtw += b;
+            }
+        }
+        finalize_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(qn * k, 256), 4096)), 256, 0, st>>>(
+            s.topk, (int)qn, k, p, index_base, out_idx + qb0 * k, out_dist + qb0 * k);
+        DTWLB_LAUNCH_CHECK();
+    }
+    if (!out_dev) {
+        DTWLB_CUDA(cudaMemcpyAsync(out_idx_in, out_idx, sizeof(int64_t) * Q * k, cudaMemcpyDeviceToHost, st));
+        DTWLB_CUDA(cudaMemcpyAsync(out_dist_in, out_dist, sizeof(float) * Q * k, cudaMemcpyDeviceToHost, st));
+    }
+    tm.mark();  // 2
+    DTWLB_CUDA(cudaStreamSynchronize(st));
+    if (stats) {
+        for (auto &e : ev) cudaEventDestroy(e);
+        unsigned long long h[8];
+        DTWLB_CUDA(cudaMemcpy(h, s.stat, sizeof(h), cudaMemcpyDeviceToHost));
+        stats->pairs = Q * N;
+        stats->keogh_evaluated = Q * N;
+        stats->improved_evaluated = (int64_t)h[0];
+        stats->dtw_cells_computed = (int64_t)h[2];
+        stats->dtw_abandoned = (int64_t)h[3];
+        stats->dtw_evaluated = (int64_t)h[1];
+        stats->dtw_cells_nominal = (int64_t)h[1] * (int64_t)(n * (2 * w + 1) - w * (w + 1));
+        stats->ms_envelope = tm.ms(0, 1);
+        stats->ms_keogh = ms_keogh;
+        stats->ms_select = ms_select;
+        stats->ms_improved = ms_improved;
+        stats->ms_dtw = ms_dtw;
+        stats->ms_total = tm.ms(0, 2);
+        stats->kernel_launches = (int64_t)(__atomic_load_n(&g_launches, __ATOMIC_RELAXED) - launches0);
+    }
+    return DTWLB_OK;
+}
+
+int nn_merge_impl(const int64_t *in_idx, const float *in_dist, int G, int64_t Q, int k, int64_t *out_idx,
+                  float *out_dist, cudaStream_t st) {
+    if (Q == 0) return DTWLB_OK;
+    nn_merge_kernel<<<(unsigned)ceil_div(Q, 128), 128, 0, st>>>(in_idx, in_dist, G, Q, k, out_idx, out_dist);
+    DTWLB_LAUNCH_CHECK();
+    return DTWLB_OK;
+}
+
+// workspace access for abi.cu (dense entry points)
+int ws_get_bytes(int slot, size_t bytes, void **out) {
+    return ws().get(S_COUNT + 1 + slot, bytes, out);
+}
+std::mutex &api_mutex() { return ws_mutex(); }
+void release_workspace() {
+    std::lock_guard<std::mutex> lock(ws_mutex());
+    cudaDeviceSynchronize();
+    ws().release();
+}
+
+}  // namespace dtwlb

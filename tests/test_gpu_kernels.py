@@ -1,0 +1,142 @@
+"""Parity of each C-ABI kernel entry point against the fp64 oracle (GPU only).
+
+Tolerances: envelope bit-exact (min/max do not round);
+LB_Keogh / LB_Improved relative 1e-5; DTW relative 1e-4 (BASELINE north_star).
+Shapes span several CTA tiles plus ragged tails (n not a multiple of 4 or 32,
+N not a multiple of the 128-candidate tile), w = 0, w >= n, w > 64 (generic DTW).
+"""
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+RNG = np.random.default_rng(11)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def series(rows, n, kind="rw"):
+    if kind == "rw":
+        return datagen.random_walks(rows, n, seed=int(RNG.integers(1 << 30)), znorm=True)
+    if kind == "ties":
+        return RNG.integers(-2, 3, size=(rows, n)).astype(np.float32)
+    if kind == "raw":
+        return datagen.random_walks(rows, n, seed=int(RNG.integers(1 << 30)), znorm=False) * 37.0
+    raise ValueError(kind)
+
+
+def close(g, o, rel, abs_=0.0):
+    g = np.asarray(g, np.float64)
+    o = np.asarray(o, np.float64)
+    err = np.abs(g - o) - (rel * np.abs(o) + abs_)
+    i = int(np.argmax(err))
+    assert err.max() <= 0, f"max violation at {np.unravel_index(i, g.shape)}: gpu {g.flat[i]!r} oracle {o.flat[i]!r}"
+
+
+ENV_CASES = [(1, 0), (1, 5), (2, 1), (3, 1), (4, 2), (7, 3), (128, 12), (256, 25), (257, 25), (512, 51),
+             (1000, 50), (100, 99), (64, 200), (33, 0), (4000, 1500)]
+
+
+@pytest.mark.parametrize("n,w", ENV_CASES)
+@pytest.mark.parametrize("kind", ["rw", "ties"])
+def test_envelope_bitwise(cuda_ok, n, w, kind):
+    from paper_0811_3301_b200 import lb_envelope
+    rows = 37
+    x = series(rows, n, kind)
+    x[0] = np.arange(n, dtype=np.float32)  # strictly monotone row
+    x[1] = 1.25                            # constant row
+    U, L = lb_envelope(dev(x), w)
+    U, L = U.cpu().numpy(), L.cpu().numpy()
+    for r in range(rows):
+        Uo, Lo = oracle.envelope(x[r].astype(np.float64), w)
+        assert np.array_equal(U[r], Uo.astype(np.float32)) and np.array_equal(L[r], Lo.astype(np.float32)), r
+
+
+BOUND_CASES = [(4, 1), (7, 3), (128, 12), (256, 25), (257, 25), (512, 51), (1000, 50), (64, 100), (33, 0)]
+
+
+def _env_dev(q, w):
+    from paper_0811_3301_b200 import lb_envelope
+    U, L = lb_envelope(dev(q), w)
+    return torch.stack([U, L]).contiguous()
+
+
+@pytest.mark.parametrize("n,w", BOUND_CASES)
+@pytest.mark.parametrize("p", [1, 2])
+def test_lb_keogh_and_improved(cuda_ok, n, w, p):
+    from paper_0811_3301_b200 import lb_improved, lb_keogh
+    Q, N = 67, 300  # > one 64-query tile, > two 128-candidate tiles, ragged
+    if n >= 512:
+        Q, N = 9, 140
+    kind = "raw" if n == 128 else "rw"
+    qs, db = series(Q, n, kind), series(N, n, kind)
+    db[5] = qs[3]                      # identical row => both bounds 0
+    q_env = _env_dev(qs, w)
+    kb = lb_keogh(q_env, dev(db), p).cpu().numpy()
+    ib = lb_improved(dev(qs), q_env, dev(db), w, p).cpu().numpy()
+    ok = np.empty((Q, N))
+    oi = np.empty((Q, N))
+    for q in range(Q):
+        for c in range(N):
+            ok[q, c] = oracle.lb_keogh(db[c], qs[q], w, p)
+            oi[q, c] = oracle.lb_improved(db[c], qs[q], w, p)
+    close(kb, ok, 1e-5, 1e-6)
+    close(ib, oi, 1e-5, 1e-6)
+    assert kb[3, 5] == 0.0 and ib[3, 5] == 0.0
+    assert np.all(ib >= kb * (1 - 1e-6))
+
+
+@pytest.mark.parametrize("n,w", [(1, 0), (2, 1), (3, 2), (4, 1), (7, 3), (128, 12), (256, 25), (257, 25),
+                                 (256, 8), (256, 17), (200, 40), (512, 51), (1000, 50), (300, 64), (128, 100),
+                                 (64, 200), (33, 0)])
+@pytest.mark.parametrize("p", [1, 2])
+def test_dtw_band(cuda_ok, n, w, p):
+    from paper_0811_3301_b200 import dtw_band
+    count = 150 if n <= 512 else 40
+    x, y = series(count, n), series(count, n)
+    x[0] = y[0]
+    out = dtw_band(dev(x), dev(y), w, p).cpu().numpy()
+    ref = np.array([oracle.dtw(x[r], y[r], w, p) for r in range(count)])
+    close(out, ref, 1e-4, 1e-6)
+    assert out[0] == 0.0
+
+
+def test_dtw_band_paper_values(cuda_ok):
+    """P:257-258 and P:1018-1019 worked values through the GPU."""
+    from paper_0811_3301_b200 import dtw_band
+    x = dev([[0, 0, 1, 0], [0, 0, 1, 0]])
+    y = dev([[2, 3, 2, 2], [2, 3, 2, 2]])
+    assert dtw_band(x, y, 3, 2).cpu().numpy().tolist() == pytest.approx([17 ** 0.5] * 2, rel=1e-6)
+    assert dtw_band(x, y, 0, 2).cpu().numpy().tolist() == pytest.approx([18 ** 0.5] * 2, rel=1e-6)
+    x = dev([[0, 1, 2]])
+    y = dev([[1, 2, 3]])
+    assert dtw_band(x, y, 1, 1).item() == pytest.approx(2.0)
+    assert dtw_band(x, y, 0, 1).item() == pytest.approx(3.0)
+
+
+def test_bounds_strict_fixture(cuda_ok):
+    """x=(4,0,3,2), y=(3,4,1,4), w=1: LB_Keogh^p 1, LB_Improved^p 2, DTW^p 5 (p=1) / 7 (p=2)."""
+    from paper_0811_3301_b200 import dtw_band, lb_improved, lb_keogh
+    x = np.array([[4, 0, 3, 2]], np.float32)
+    y = np.array([[3, 4, 1, 4]], np.float32)
+    env = _env_dev(y, 1)
+    for p, d in ((1, 5.0), (2, 7.0)):
+        assert lb_keogh(env, dev(x), p).item() ** p == pytest.approx(1.0)
+        assert lb_improved(dev(y), env, dev(x), 1, p).item() ** p == pytest.approx(2.0)
+        assert dtw_band(dev(x), dev(y), 1, p).item() ** p == pytest.approx(d)
+
+
+def test_error_model_on_gpu(cuda_ok):
+    from paper_0811_3301_b200 import DtwlbError, dtw_band, lb_keogh
+    with pytest.raises(DtwlbError) as e:
+        dtw_band(dev(np.zeros((2, 4))), dev(np.zeros((2, 4))), 1, 3)
+    assert e.value.name == "EUNSUPPORTED"
+    with pytest.raises(DtwlbError) as e:
+        dtw_band(dev(np.zeros((2, 4))), dev(np.zeros((2, 4))), -1, 1)
+    assert e.value.name == "EINVAL"

@@ -1,0 +1,139 @@
+"""nn_search parity against the fp64 oracle (GPU only).
+
+Ground truth is the oracle's brute-force k-NN (or its Algorithm-3 scan, which
+tests/test_oracle_search.py pins to brute force).  Comparison: tests/knn_compare.py
+(tie classes at relative 1e-4, distances within relative 1e-4).
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import oracle
+from knn_compare import assert_knn_match
+
+pytestmark = pytest.mark.gpu
+THREADS = max(1, os.cpu_count() or 1)
+EXTRA = 8
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def run(qs, db, w, p, k, **kw):
+    from paper_0811_3301_b200 import nn_search
+    idx, dist = nn_search(dev(qs), dev(db), w, p, k, **kw)
+    torch.cuda.synchronize()
+    return idx.cpu().numpy(), dist.cpu().numpy()
+
+
+def check(qs, db, w, p, k, brute=True, **kw):
+    g_idx, g_dist = run(qs, db, w, p, k, **kw)
+    ke = min(len(db), k + EXTRA)
+    if brute:
+        o_idx, o_dist = oracle.nn_brute(qs, db, w, p, ke, threads=THREADS)
+    else:
+        o_idx, o_dist, _ = oracle.nn_twopass(qs, db, w, p, ke, threads=THREADS)
+    base = kw.get("index_base", 0)
+    assert_knn_match(g_idx - base, g_dist, o_idx, o_dist, k)
+    return g_idx, g_dist
+
+
+def test_C1_full(cuda_ok):
+    c = datagen.CONFIGS["C1"]
+    qs, db = datagen.make(c)
+    check(qs, db, c.w, c.p, c.k)
+
+
+@pytest.mark.parametrize("name", ["C2p1", "C2p2"])
+def test_C2_full(cuda_ok, name):
+    c = datagen.CONFIGS[name]
+    qs, db = datagen.make(c)
+    check(qs, db, c.w, c.p, c.k, brute=False)
+
+
+@pytest.mark.parametrize("name,Q,N", [("C3", 6, 20_000), ("C4", 8, 30_000), ("C5", 8, 60_000)])
+def test_reduced_large_configs(cuda_ok, name, Q, N):
+    c = datagen.CONFIGS[name]
+    qs, db = datagen.make(c, Q=Q, N=N)
+    check(qs, db, c.w, c.p, c.k, brute=False)
+
+
+@pytest.mark.parametrize("p", [1, 2])
+@pytest.mark.parametrize("k", [1, 3, 10])
+def test_duplicates_self_queries_ties(cuda_ok, p, k):
+    qs, db = datagen.make("C2p1", Q=20, N=3000)
+    db[100] = qs[0]          # exact self-match -> distance 0
+    db[2000] = qs[0]         # duplicate of the self-match: smaller index first
+    db[7] = db[8]            # duplicate rows
+    db[1500] = qs[5] + 1e-3  # near tie
+    g_idx, g_dist = check(qs, db, 25, p, k)
+    assert g_idx[0, 0] == 100 and g_dist[0, 0] == 0.0
+    if k > 1:
+        assert g_idx[0, 1] == 2000 and g_dist[0, 1] == 0.0
+
+
+@pytest.mark.parametrize("n,w", [(7, 3), (7, 0), (50, 60), (128, 100), (130, 5), (1, 0), (300, 64), (96, 33)])
+def test_odd_shapes_and_bands(cuda_ok, n, w):
+    qs = datagen.random_walks(9, n, seed=3, role=1)
+    db = datagen.random_walks(700, n, seed=4)
+    for p in (1, 2):
+        check(qs, db, w, p, 2)
+
+
+def test_k_equals_N_and_small_N(cuda_ok):
+    qs, db = datagen.make("C1", Q=3, N=40)
+    check(qs, db, 12, 1, 40)     # full sorted order
+    check(qs, db, 12, 2, 1)
+    check(qs, db[:1], 12, 1, 1)  # N = 1
+
+
+def test_keogh_only_index_base_eps0(cuda_ok):
+    qs, db = datagen.make("C2p2", Q=16, N=5000)
+    check(qs, db, 25, 2, 5, keogh_only=True)
+    check(qs, db, 25, 2, 5, index_base=1_000_000)
+    check(qs, db, 25, 2, 5, eps=0.0)
+    check(qs, db, 25, 2, 5, query_block=4)   # several query blocks
+
+
+def test_host_buffers(cuda_ok):
+    """e2e path: host (numpy) inputs and outputs through the same C-ABI call."""
+    from paper_0811_3301_b200 import nn_search
+    qs, db = datagen.make("C2p1", Q=10, N=4000)
+    h_idx, h_dist = nn_search(qs, db, 25, 1, 3)
+    assert not h_idx.is_cuda
+    d_idx, d_dist = run(qs, db, 25, 1, 3)
+    assert np.array_equal(h_idx.numpy(), d_idx) and np.array_equal(h_dist.numpy(), d_dist)
+
+
+def test_empty_query_set(cuda_ok):
+    from paper_0811_3301_b200 import nn_search
+    idx, dist = nn_search(dev(np.zeros((0, 16))), dev(np.zeros((5, 16))), 2, 1, 1)
+    assert idx.shape == (0, 1)
+
+
+def test_deterministic_repeat(cuda_ok):
+    qs, db = datagen.make("C2p2", Q=32, N=8000)
+    a = run(qs, db, 25, 2, 10)
+    b = run(qs, db, 25, 2, 10)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("name,sample", [("C5", 3), ("C3", 3), ("C4", 3)])
+def test_full_size_sampled(cuda_ok, name, sample):
+    """Full BASELINE size in bench.py's launch configuration; the oracle checks a
+    sample of queries one by one (its Algorithm-3 scan over the whole database)."""
+    from paper_0811_3301_b200 import nn_search
+    c = datagen.CONFIGS[name]
+    qs, db = datagen.make(c)
+    idx, dist = nn_search(dev(qs), dev(db), c.w, c.p, c.k)
+    idx, dist = idx.cpu().numpy(), dist.cpu().numpy()
+    rows = np.linspace(0, c.Q - 1, sample).astype(int)
+    o_idx, o_dist, _ = oracle.nn_twopass(qs[rows], db, c.w, c.p, c.k + EXTRA, threads=THREADS)
+    assert_knn_match(idx[rows], dist[rows], o_idx, o_dist, c.k)
+    # properties at any size: ascending, finite, distinct, in range
+    assert np.all(np.diff(dist, axis=1) >= 0) and np.all(np.isfinite(dist))
+    assert idx.min() >= 0 and idx.max() < c.N
