@@ -78,10 +78,24 @@ def test_duplicates_self_queries_ties(cuda_ok, p, k):
 
 @pytest.mark.parametrize("n,w", [(7, 3), (7, 0), (50, 60), (128, 100), (130, 5), (1, 0), (300, 64), (96, 33)])
 def test_odd_shapes_and_bands(cuda_ok, n, w):
-    qs = datagen.random_walks(9, n, seed=3, role=1)
-    db = datagen.random_walks(700, n, seed=4)
+    if n == 1:  # a length-1 random walk is the constant 0: use white noise instead
+        g = np.random.default_rng(5)
+        qs = g.standard_normal((9, 1)).astype(np.float32)
+        db = g.standard_normal((700, 1)).astype(np.float32)
+    else:
+        qs = datagen.random_walks(9, n, seed=3, role=1)
+        db = datagen.random_walks(700, n, seed=4)
     for p in (1, 2):
         check(qs, db, w, p, 2)
+
+
+def test_all_tied_database_returns_smallest_indices(cuda_ok):
+    """Every candidate at distance 0: ties break to the smallest index (reading c4)."""
+    qs = np.zeros((4, 16), np.float32)
+    db = np.zeros((500, 16), np.float32)
+    for p in (1, 2):
+        idx, dist = run(qs, db, 3, p, 7)
+        assert np.all(idx == np.arange(7)) and np.all(dist == 0)
 
 
 def test_k_equals_N_and_small_N(cuda_ok):
