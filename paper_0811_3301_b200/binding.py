@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdtwlb.so")
+LIB_PATH = os.environ.get("DTWLB_LIB") or os.path.join(_HERE, "libdtwlb.so")
 
 STATUS = {0: "OK", 1: "EINVAL", 2: "EUNSUPPORTED", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL"}
 KEOGH_ONLY = 1

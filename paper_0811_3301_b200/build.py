@@ -15,13 +15,14 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libdtwlb.so")
-OBJ = os.path.join(HERE, "_obj")
+CHECKED = os.environ.get("DTWLB_CHECKED") == "1"  # debug build with device bounds checks
+LIB = os.path.join(HERE, "libdtwlb_checked.so" if CHECKED else "libdtwlb.so")
+OBJ = os.path.join(HERE, "_obj_checked" if CHECKED else "_obj")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 SOURCES = ["abi.cu", "envelope.cu", "keogh.cu", "improved.cu", "dtw.cu", "search.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-I", INCLUDE]
+         "-Xcompiler", "-fPIC", "-I", INCLUDE] + (["-DDTWLB_CHECKED"] if CHECKED else [])
 
 
 def _deps_mtime() -> float:

@@ -176,6 +176,7 @@ int dtw_band(const float *x, const float *y, int32_t n, int32_t w, int32_t p, fl
     w = w > n - 1 ? n - 1 : w;
     DtwArgs a{};
     a.db = x;
+    a.Ndb = count;
     a.n = n;
     a.w = w;
     a.total = count;

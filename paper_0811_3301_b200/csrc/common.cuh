@@ -38,6 +38,23 @@ extern unsigned long long g_launches;
         if (s_ != DTWLB_OK) return s_; \
     } while (0)
 
+// Device-side bounds checks of the debug build (build.py --checked): printf + trap.
+#ifdef DTWLB_CHECKED
+#define DCHECK(cond, ...)                                                  \
+    do {                                                                   \
+        if (!(cond)) {                                                     \
+            printf("DCHECK %s:%d (%s): ", __FILE__, __LINE__, #cond);       \
+            printf(__VA_ARGS__);                                           \
+            printf("\n");                                                  \
+            __trap();                                                      \
+        }                                                                  \
+    } while (0)
+#else
+#define DCHECK(cond, ...) \
+    do {                  \
+    } while (0)
+#endif
+
 // One-time device check: an sm_100 device must be current.
 int require_device();
 

@@ -134,8 +134,12 @@ dtw_kernel(DtwArgs a, int ipw) {
                     }
                     const int q = lo;
                     const int64_t j = a.pos[q] + (item - a.item_off[q]);
+                    DCHECK(q >= 0 && q < a.Qb && item >= a.item_off[q] && item < a.item_off[q + 1] && j >= 0 && j < a.cap,
+                           "dtw item %lld q=%d j=%lld pos=%d off=%d,%d", (long long)item, q, (long long)j, a.pos[q],
+                           a.item_off[q], a.item_off[q + 1]);
                     const unsigned long long key = a.list[(int64_t)q * a.cap + j];
                     const uint32_t c = (uint32_t)(key & 0xffffffffu);
+                    DCHECK((int64_t)c < a.Ndb, "dtw key c=%u N=%lld q=%d j=%lld key=%llx", c, (long long)a.Ndb, q, (long long)j, key);
                     beta = __uint_as_float((uint32_t)(key >> 32));
                     thr = a.thr[q];
                     xr = a.db + (int64_t)c * n;
@@ -145,6 +149,7 @@ dtw_kernel(DtwArgs a, int ipw) {
                     xr = a.db + item * n;
                     yb = a.ysh + item * a.LP;
                 }
+                DCHECK(item < a.total, "dtw item %lld total %lld", (long long)item, (long long)a.total);
                 if (beta > thr) {
                     a.res[item] = kInf;  // pruned by the bound under the current threshold
                 } else {

@@ -73,8 +73,9 @@ improved_kernel(ImprovedArgs a, int Ct) {
         // survivor masks over the tile (Ct <= 64)
         float b1v0 = lane < ct ? b1row[lane] : kInf;
         float b1v1 = lane + 32 < ct ? b1row[lane + 32] : kInf;
-        unsigned m0 = __ballot_sync(0xffffffffu, DENSE ? lane < ct : (b1v0 > lo && b1v0 <= hi));
-        unsigned m1 = __ballot_sync(0xffffffffu, DENSE ? lane + 32 < ct : (b1v1 > lo && b1v1 <= hi));
+        // (the padding value +inf must not pass a range whose hi is +inf: test lane < ct)
+        unsigned m0 = __ballot_sync(0xffffffffu, lane < ct && (DENSE || (b1v0 > lo && b1v0 <= hi)));
+        unsigned m1 = __ballot_sync(0xffffffffu, lane + 32 < ct && (DENSE || (b1v1 > lo && b1v1 <= hi)));
         if ((m0 | m1) == 0) continue;
         evals += __popc(m0) + __popc(m1);
 
@@ -128,6 +129,7 @@ improved_kernel(ImprovedArgs a, int Ct) {
                         int base = 0;
                         if (lane == 0) base = atomicAdd(a.list_len + q, 32);
                         base = __shfl_sync(0xffffffffu, base, 0);
+                        DCHECK(base + 32 <= a.cap, "list flush q=%lld base=%d cap=%lld", (long long)q, base, (long long)a.cap);
                         a.list[q * a.cap + base + lane] = mykey;
                     }
                 }
@@ -139,6 +141,7 @@ improved_kernel(ImprovedArgs a, int Ct) {
                 int base = 0;
                 if (lane == 0) base = atomicAdd(a.list_len + q, rem);
                 base = __shfl_sync(0xffffffffu, base, 0);
+                DCHECK(base + rem <= a.cap, "list tail q=%lld base=%d rem=%d cap=%lld", (long long)q, base, rem, (long long)a.cap);
                 if (lane < rem) a.list[q * a.cap + base + lane] = mykey;
             }
         }

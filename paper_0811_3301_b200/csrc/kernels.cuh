@@ -46,6 +46,7 @@ struct DtwArgs {
     int64_t ysh_stride_s;  // elements between shifted copies
     int LP;                // padded row length
     const float *db;       // candidate rows [*][n]
+    int64_t Ndb;           // rows of db (bounds checks of the debug build)
     int n, w;
     // PAIRS mode: item t -> candidate row t, query row t, no pruning
     // WALK mode: item t -> per-query sorted list entry

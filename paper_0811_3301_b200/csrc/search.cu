@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(1024) sort_runs_kernel(unsigned long long *__r
     const int q = run_q[blockIdx.x], r = run_idx[blockIdx.x];
     const int64_t base = (int64_t)q * cap + (int64_t)r * kRun;
     const int m = min(kRun, len[q] - r * kRun);
+    DCHECK(m > 0 && (int64_t)r * kRun + m <= cap, "sort q=%d r=%d m=%d cap=%lld", q, r, m, (long long)cap);
     int P2 = 1;
     while (P2 < m) P2 <<= 1;
     for (int t = threadIdx.x; t < P2; t += blockDim.x) v[t] = t < m ? list[base + t] : ~0ull;
@@ -264,6 +265,7 @@ __global__ void merge_kernel(QState s, int Qb, int k, float eps, const unsigned 
         const int t = b + lane;
         unsigned long long key = ~0ull;
         if (t < o1) {
+            DCHECK(p0 + (t - o0) < s.len[q] && t < s.counters[0], "merge q=%d t=%d o0=%d p0=%d len=%d", q, t, o0, p0, s.len[q]);
             const float d = res[t];
             if (d < kInf) key = pack_key(d, (uint32_t)(lq[p0 + (t - o0)] & 0xffffffffu));
         }
@@ -570,6 +572,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 da.ysh_stride_s = (int64_t)Q * LP;
                 da.LP = LP;
                 da.db = db;
+                da.Ndb = N;
                 da.n = n;
                 da.w = w;
                 da.item_off = s.item_off;
