@@ -104,12 +104,6 @@ def _dist_env():
     return ws, rank, local
 
 
-def shard_rows(N, G, r):
-    lo = r * N // G
-    hi = (r + 1) * N // G
-    return lo, hi
-
-
 # ----------------------------------------------------------------------------- CPU oracle
 def oracle_sample(cfg, qs, db, budget_s=15.0, threads=None):
     """Time the fp64 oracle (Alg. 3 scan, as it stands) on a bounded query sample."""
@@ -169,6 +163,7 @@ def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
     from paper_0811_3301_b200 import binding as B
+    from paper_0811_3301_b200.sharded import shard_range
 
     ws, rank, local = _dist_env()
     if ws > 1:
@@ -177,26 +172,28 @@ def run_ours(args, cfg):
     dev = torch.device("cuda", local if ws > 1 else 0)
     torch.cuda.set_device(dev)
     st = torch.cuda.current_stream()
-    lo, hi = shard_rows(cfg.N, ws, rank)
+    lo, hi = shard_range(cfg.N, ws, rank)
     qs_h, _ = datagen.make(cfg, N=0)
     db_h = datagen.series(cfg.family, hi - lo, cfg.n, cfg.seed, datagen.ROLE_DB, cfg.znorm, start=lo)
     qs = torch.from_numpy(qs_h).to(dev)
     db = torch.from_numpy(db_h).to(dev)
-    Nl = hi - lo
     k = cfg.k
+    from paper_0811_3301_b200.sharded import sharded_nn_search
     idx = torch.empty((cfg.Q, k), dtype=torch.int64, device=dev)
     dst = torch.empty((cfg.Q, k), dtype=torch.float32, device=dev)
-    if ws > 1:
-        g_idx = torch.empty((ws, cfg.Q, k), dtype=torch.int64, device=dev)
-        g_dst = torch.empty((ws, cfg.Q, k), dtype=torch.float32, device=dev)
+    gbufs = (torch.empty((ws * cfg.Q, k), dtype=torch.int64, device=dev),
+             torch.empty((ws * cfg.Q, k), dtype=torch.float32, device=dev))
+    last = {}
+
+    def search(q_, d_, w_, p_, k_, index_base=0, out=None):
+        i_, d2, st_ = B.nn_search(q_, d_, w_, p_, k_, index_base=index_base, out=out, return_stats=True)
+        last["st"] = st_
+        return i_, d2
 
     def step(stats=False):
-        r = B.nn_search(qs, db, cfg.w, cfg.p, k, index_base=lo, out=(idx, dst), return_stats=stats)
-        if ws > 1:
-            dist.all_gather_into_tensor(g_idx, idx)
-            dist.all_gather_into_tensor(g_dst, dst)
-            B.nn_merge(g_idx, g_dst)
-        return r[2] if stats else None
+        sharded_nn_search(qs, db, lo, cfg.w, cfg.p, k, search=search, merge=B.nn_merge, out_local=(idx, dst),
+                          gather_bufs=gbufs)
+        return last["st"] if stats else None
 
     def barrier():
         if ws > 1:

@@ -1,0 +1,83 @@
+"""Database-sharded multi-GPU k-NN: one process per GPU.
+
+Rank r of G owns database rows [r*N//G, (r+1)*N//G); queries are replicated.
+Each rank runs the full cascade on its shard (``nn_search`` with
+``index_base`` = its first row), then the ranks exchange their [Q][k]
+(index, distance) lists with one NCCL all-gather and merge them (``nn_merge``:
+the k smallest by (distance, index) of the G*k entries).  A shard's local k-th
+best is >= the global k-th best, so every local prune is also globally safe,
+and the union of the shard lists contains the global k-NN.
+
+The search and merge callables are injectable so the protocol can be tested
+with ``gloo`` on CPU (tests/test_sharded_cpu.py); the product path uses the
+CUDA library (``binding.nn_search`` / ``binding.nn_merge``).
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(N: int, world: int, rank: int):
+    """Contiguous, balanced rows [lo, hi) of rank `rank` (sizes differ by at most 1)."""
+    return rank * N // world, (rank + 1) * N // world
+
+
+def sharded_nn_search(queries: torch.Tensor, db_shard: torch.Tensor, shard_lo: int, w: int, p: int, k: int,
+                      group: Optional[dist.ProcessGroup] = None,
+                      search: Optional[Callable] = None, merge: Optional[Callable] = None,
+                      out_local=None, gather_bufs=None):
+    """Global k-NN over the union of all ranks' shards; every rank gets the result.
+
+    Shards with fewer than k rows contribute their whole shard padded with
+    (index -1, distance +inf), which the merge ignores.
+    """
+    if search is None or merge is None:
+        from . import binding
+        search = search or binding.nn_search
+        merge = merge or binding.nn_merge
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    Q = queries.shape[0]
+    dev = queries.device
+    kk = min(k, db_shard.shape[0])
+    if kk > 0:
+        if out_local is not None and kk == k:
+            idx, dst = search(queries, db_shard, w, p, k, index_base=shard_lo, out=out_local)
+        else:
+            idx, dst = search(queries, db_shard, w, p, kk, index_base=shard_lo)
+    else:
+        idx = torch.empty((Q, 0), dtype=torch.int64, device=dev)
+        dst = torch.empty((Q, 0), dtype=torch.float32, device=dev)
+    if kk < k:  # pad to k
+        pad_i = torch.full((Q, k - kk), -1, dtype=torch.int64, device=dev)
+        pad_d = torch.full((Q, k - kk), float("inf"), dtype=torch.float32, device=dev)
+        idx = torch.cat([idx, pad_i], 1)
+        dst = torch.cat([dst, pad_d], 1)
+    if world == 1:
+        return idx, dst
+    if gather_bufs is None:
+        g_idx = torch.empty((world * Q, k), dtype=torch.int64, device=dev)
+        g_dst = torch.empty((world * Q, k), dtype=torch.float32, device=dev)
+    else:
+        g_idx, g_dst = gather_bufs
+    # concatenated along dim 0 (the layout both NCCL and gloo accept), viewed as [G][Q][k]
+    dist.all_gather_into_tensor(g_idx, idx.contiguous(), group=group)
+    dist.all_gather_into_tensor(g_dst, dst.contiguous(), group=group)
+    return merge(g_idx.view(world, Q, k), g_dst.view(world, Q, k))
+
+
+def merge_reference(g_idx: torch.Tensor, g_dst: torch.Tensor):
+    """Host reference of nn_merge (tests): k smallest by (dist, idx), ignoring idx < 0."""
+    G, Q, k = g_idx.shape
+    out_i = torch.full((Q, k), -1, dtype=torch.int64)
+    out_d = torch.full((Q, k), float("inf"), dtype=torch.float32)
+    for q in range(Q):
+        cand = [(float(g_dst[g, q, j]), int(g_idx[g, q, j])) for g in range(G) for j in range(k)
+                if int(g_idx[g, q, j]) >= 0]
+        cand.sort()
+        for r, (d, i) in enumerate(cand[:k]):
+            out_i[q, r] = i
+            out_d[q, r] = d
+    return out_i, out_d

@@ -1,0 +1,95 @@
+"""World-size-2 `gloo` tests of the database-sharded protocol on CPU.
+
+The per-shard search is the oracle's brute force (CPU stand-in for the CUDA
+`nn_search`, which needs a GPU); the exchange (all-gather of [Q][k] lists with
+global indices) and the merge are the product's `sharded.py` code.  The result
+must equal the oracle's k-NN over the whole database.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import datagen
+import oracle
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _oracle_search(queries, db, w, p, k, index_base=0, out=None):
+    idx, dst = oracle.nn_brute(queries.numpy(), db.numpy(), w, p, k)
+    return torch.from_numpy(idx + index_base), torch.from_numpy(dst.astype(np.float32))
+
+
+def _worker(rank, world, port, N, k, result_q):
+    try:
+        _worker_body(rank, world, port, N, k, result_q)
+    except Exception as e:  # report instead of hanging the parent
+        result_q.put((rank, None, repr(e), None))
+        raise
+
+
+def _worker_body(rank, world, port, N, k, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_0811_3301_b200.sharded import merge_reference, shard_range, sharded_nn_search
+    cfg = datagen.CONFIGS["C2p2"]
+    lo, hi = shard_range(N, world, rank)
+    qs, _ = datagen.make(cfg, Q=5, N=0)
+    shard = datagen.series(cfg.family, hi - lo, cfg.n, cfg.seed, datagen.ROLE_DB, cfg.znorm, start=lo)
+    if rank == 1:
+        shard[3] = qs[2]  # an exact match living on the second shard (global index lo+3)
+    idx, dst = sharded_nn_search(torch.from_numpy(qs), torch.from_numpy(shard), lo, cfg.w, cfg.p, k,
+                                 search=_oracle_search, merge=merge_reference)
+    result_q.put((rank, idx.numpy(), dst.numpy(), lo))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("N,k", [(301, 3), (7, 5), (40, 10)])
+def test_sharded_equals_global(N, k):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, N, k, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    res.sort(key=lambda r: r[0])
+    for r in res:
+        assert r[1] is not None, r[2]
+    cfg = datagen.CONFIGS["C2p2"]
+    qs, db = datagen.make(cfg, Q=5, N=N)
+    lo1 = res[1][3]
+    db[lo1 + 3] = qs[2]
+    o_idx, o_dst = oracle.nn_brute(qs, db, cfg.w, cfg.p, min(k, N))
+    for rank, idx, dst, _ in res:
+        assert np.array_equal(idx[:, :min(k, N)], o_idx)          # identical on every rank
+        assert np.allclose(dst[:, :min(k, N)], o_dst, rtol=1e-6)
+    assert res[0][1][2, 0] == lo1 + 3 and res[0][2][2, 0] == 0.0
+
+
+def test_shard_ranges_partition():
+    from paper_0811_3301_b200.sharded import shard_range
+    for N in (1, 7, 1000, 1_000_000):
+        for G in (1, 2, 3, 4, 8):
+            r = [shard_range(N, G, i) for i in range(G)]
+            assert r[0][0] == 0 and r[-1][1] == N
+            assert all(r[i][1] == r[i + 1][0] for i in range(G - 1))
+            sizes = [b - a for a, b in r]
+            assert max(sizes) - min(sizes) <= 1
