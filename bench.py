@@ -264,11 +264,15 @@ def run_ours(args, cfg):
         ops = 4.0 * (cfg.Q * (cfg.N // ws)) * cfg.n
         achieved = ops / (keogh_ms * 1e-3) / 1e12
         peak = n_sm * 128 * sm_clock * 1e6 / 1e12
-        traffic = None
+        traffic, traffic_note = None, None
         tpath = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tpath):
             try:
-                traffic = json.load(open(tpath)).get(cfg.name)
+                t = json.load(open(tpath)).get(cfg.name)
+                if t:
+                    traffic = t["bytes"]
+                    traffic_note = (f"dram read+write bytes of one keogh launch ({t['launch_queries']} queries x "
+                                    f"{cfg.N} series) from ncu --set full; algorithmic {t['algorithmic_bytes']}")
             except Exception:
                 traffic = None
         clocks = clk.summary()
@@ -290,6 +294,9 @@ def run_ours(args, cfg):
                        "l2": f"inputs larger than L2 ({cfg.N * cfg.n * 4 / 1e9:.2f} GB database)"},
             "dtw_cells_per_s": cells_cmp / (ms_max * 1e-3),
             "dtw_cells_nominal_per_s": cells_nom / (ms_max * 1e-3),
+            "walk": {k2: statistics.mean(s[k2] for s in stats_all)
+                     for k2 in ("range1_improved", "range1_dtw", "range1_cells", "walk_rounds", "dtw_evaluated",
+                                "dtw_cells_computed")},
             "prune": {"keogh_pruned_frac": 1 - improved / pairs,
                       "improved_evaluated_frac": improved / pairs,
                       "dtw_evaluated_frac": dtw_eval / pairs,
@@ -300,7 +307,7 @@ def run_ours(args, cfg):
                          "peak": peak, "unit": "Tlane-op/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_note": f"{n_sm} SMs x 128 FP32 lanes x {sm_clock:.0f} MHz (guide unit counts, "
                                       "MEASURED_PEAKS sm_max_mhz); 4 lane-ops per pair-element",
-                         "keogh_ms": keogh_ms},
+                         "keogh_ms": keogh_ms, "traffic_note": traffic_note},
             "e2e": {"value": pairs / (e2e_ms * 1e-3), "unit": "pairs/s",
                     "h2d_bytes_per_step": int(qs_h.nbytes + db_h.nbytes),
                     "d2h_bytes_per_step": int(cfg.Q * k * 12)},

@@ -106,6 +106,9 @@ typedef struct nn_stats {
     int64_t dtw_cells_computed; /* cells actually executed (early abandon)            */
     double ms_envelope, ms_keogh, ms_select, ms_improved, ms_dtw, ms_total;
     int64_t kernel_launches;    /* kernels this call launched                         */
+    int64_t range1_improved, range1_dtw, range1_cells; /* ... of the above, in the first
+                                   (best-first seed) range of candidates               */
+    int64_t walk_rounds;        /* DTW walk rounds (plan -> DTW -> merge)              */
 } nn_stats;
 
 /* Exact k-nearest-neighbour search under banded DTW_p: for each query y_q,

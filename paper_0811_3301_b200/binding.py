@@ -39,7 +39,8 @@ class NnStats(ctypes.Structure):
                 ("dtw_cells_computed", ctypes.c_int64), ("ms_envelope", ctypes.c_double),
                 ("ms_keogh", ctypes.c_double), ("ms_select", ctypes.c_double),
                 ("ms_improved", ctypes.c_double), ("ms_dtw", ctypes.c_double), ("ms_total", ctypes.c_double),
-                ("kernel_launches", ctypes.c_int64)]
+                ("kernel_launches", ctypes.c_int64), ("range1_improved", ctypes.c_int64),
+                ("range1_dtw", ctypes.c_int64), ("range1_cells", ctypes.c_int64), ("walk_rounds", ctypes.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -131,6 +131,8 @@ int lb_improved(const float *q, const float *q_env, const float *db, int64_t Q, 
     DTWLB_TRY(ws_get_bytes(1, sizeof(float) * 3 * Q * n, (void **)&env));
     DTWLB_TRY(ws_get_bytes(2, sizeof(float) * 3 * Q * npadE, (void **)&qpad));
     DTWLB_TRY(ws_get_bytes(3, sizeof(float) * 2 * N * n, (void **)&dbenv));
+    void *imp_scratch;
+    DTWLB_TRY(ws_get_bytes(6, improved_scratch_bytes(Q, N), &imp_scratch));
     const float *U = q_env, *L = q_env + Q * n;
     float *LU = env, *UL = env + Q * n, *scr = env + 2 * Q * n;
     DTWLB_TRY(launch_keogh(U, L, db, Q, N, n, p, false, beta1, ldb, st));
@@ -156,6 +158,7 @@ int lb_improved(const float *q, const float *q_env, const float *db, int64_t Q, 
     a.npadE = npadE;
     a.dense = out;
     a.ldd = N;
+    improved_scratch_bind(a, imp_scratch);
     DTWLB_TRY(launch_improved(a, p, false, true, st));
     DTWLB_CUDA(cudaStreamSynchronize(st));  // workspace reuse safety
     return DTWLB_OK;
@@ -190,9 +193,12 @@ int dtw_band(const float *x, const float *y, int32_t n, int32_t w, int32_t p, fl
         float *ysh;
         DTWLB_TRY(ws_get_bytes(5, sizeof(float) * 4 * count * LP, (void **)&ysh));
         DTWLB_TRY(launch_build_ysh(y, count, n, ysh, LP, st));
+        unsigned *queue;
+        DTWLB_TRY(ws_get_bytes(7, 64, (void **)&queue));
         a.ysh = ysh;
         a.ysh_stride_s = count * LP;
         a.LP = LP;
+        a.queue = queue;
         DTWLB_TRY(launch_dtw(a, p, false, st));
     }
     DTWLB_CUDA(cudaStreamSynchronize(st));

@@ -9,14 +9,18 @@
 // pair tile.  Chunks of 32 samples of the envelopes U, L and of the candidate
 // rows are staged in shared memory with cp.async (double-buffered), read back
 // as 128-bit vectors, and each loaded value is reused 8x (envelope) or 4x
-// (candidate) from registers.  Per pair-element: FADD, FADD, FMNMX3(.., 0),
-// FADD|FFMA -- the minimal SASS for the bound.  Per-chunk partial
+// (candidate) from registers.  Per pair-element: FMNMX, FMNMX (the clamp of x
+// into [L, U], ALU pipe), FADD, FFMA|FADD (FMA pipe): 4 ops split 2/2 over the
+// two pipes, which measured faster than the 3-FMA-pipe-op form
+// max(x-U, L-x, 0) ("LB_Keogh instruction mix").  Per-chunk partial
 // sums are folded into the total at each chunk end (two-level summation keeps
 // the fp32 error at ~(32 + n/32) ulp instead of n ulp).
 // CTAs are ordered query-tile-fastest so each database tile is fetched from
 // HBM once and served from L2 to every query tile; the envelopes of the whole
 // query block stay L2-resident.  The i-tail beyond n is zero-filled on both
 // sides, which contributes max(0-0, 0-0, 0) = 0.
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace dtwlb {
@@ -38,11 +42,17 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-struct Stage {
+struct Stage {  // chunk of the operands, written by cp.async (double-buffered)
     float X[TC][KP];
     float U[TQ][KP];
     float L[TQ][KP];
 };
+// acc + |d|^p for a signed deviation d (p=1: FADD with |.| operand; p=2: FFMA)
+template <int P>
+__device__ __forceinline__ float acc_dev(float acc, float d) {
+    if constexpr (P == 1) return acc + fabsf(d);
+    else return fmaf(d, d, acc);
+}
 
 // Stage chunk [k0, k0+KC) of rows r0.. of a [rows][n] matrix into S[R][KP].
 template <int R, bool VEC>
@@ -70,8 +80,8 @@ __device__ __forceinline__ void stage_rows(float (*S)[KP], const float *__restri
     }
 }
 
-template <int P, bool VEC, bool ROOTED>
-__global__ void __launch_bounds__(NT, 1)
+template <int P, bool VEC, bool ROOTED, int VAR, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
 keogh_tile_kernel(const float *__restrict__ U, const float *__restrict__ L, const float *__restrict__ db,
                   int64_t Q, int64_t N, int n, float *__restrict__ out, int64_t ldo, int nqt) {
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -107,7 +117,6 @@ keogh_tile_kernel(const float *__restrict__ U, const float *__restrict__ L, cons
         cp_wait<1>();
         __syncthreads();
         const Stage &s = st[ch & 1];
-
         float part[4][8];
 #pragma unroll
         for (int r = 0; r < 4; ++r)
@@ -124,17 +133,31 @@ keogh_tile_kernel(const float *__restrict__ U, const float *__restrict__ L, cons
                 uv[r] = *reinterpret_cast<const float4 *>(&s.U[4 * qg + r][k]);
                 lv[r] = *reinterpret_cast<const float4 *>(&s.L[4 * qg + r][k]);
             }
+            if constexpr (VAR == 1) {
+                // d = x - clamp(x, L, U) (= x - H(x,y)_i of Eq. (1)); acc += |d|^p:
+                // FMNMX, FMNMX (ALU pipe), FADD, FFMA|FADD (FMA pipe)
 #pragma unroll
-            for (int r = 0; r < 4; ++r)
+                for (int r = 0; r < 4; ++r)
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    // d(x, [L, U]) = max(x - U, L - x, 0); acc += d^p
-                    float d;
-                    d = max3f(xv[j].x - uv[r].x, lv[r].x - xv[j].x, 0.f); part[r][j] = accp<P>(part[r][j], d);
-                    d = max3f(xv[j].y - uv[r].y, lv[r].y - xv[j].y, 0.f); part[r][j] = accp<P>(part[r][j], d);
-                    d = max3f(xv[j].z - uv[r].z, lv[r].z - xv[j].z, 0.f); part[r][j] = accp<P>(part[r][j], d);
-                    d = max3f(xv[j].w - uv[r].w, lv[r].w - xv[j].w, 0.f); part[r][j] = accp<P>(part[r][j], d);
-                }
+                    for (int j = 0; j < 8; ++j) {
+                        part[r][j] = acc_dev<P>(part[r][j], xv[j].x - fminf(fmaxf(xv[j].x, lv[r].x), uv[r].x));
+                        part[r][j] = acc_dev<P>(part[r][j], xv[j].y - fminf(fmaxf(xv[j].y, lv[r].y), uv[r].y));
+                        part[r][j] = acc_dev<P>(part[r][j], xv[j].z - fminf(fmaxf(xv[j].z, lv[r].z), uv[r].z));
+                        part[r][j] = acc_dev<P>(part[r][j], xv[j].w - fminf(fmaxf(xv[j].w, lv[r].w), uv[r].w));
+                    }
+            } else {
+                // d = max(x - U, L - x, 0); acc += d^p: FADD, FADD, FMNMX3(.., 0), FFMA|FADD
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        float d;
+                        d = max3f(xv[j].x - uv[r].x, lv[r].x - xv[j].x, 0.f); part[r][j] = accp<P>(part[r][j], d);
+                        d = max3f(xv[j].y - uv[r].y, lv[r].y - xv[j].y, 0.f); part[r][j] = accp<P>(part[r][j], d);
+                        d = max3f(xv[j].z - uv[r].z, lv[r].z - xv[j].z, 0.f); part[r][j] = accp<P>(part[r][j], d);
+                        d = max3f(xv[j].w - uv[r].w, lv[r].w - xv[j].w, 0.f); part[r][j] = accp<P>(part[r][j], d);
+                    }
+            }
         }
 #pragma unroll
         for (int r = 0; r < 4; ++r)
@@ -155,11 +178,23 @@ keogh_tile_kernel(const float *__restrict__ U, const float *__restrict__ L, cons
     }
 }
 
-template <int P, bool VEC, bool ROOTED>
-int launch_keogh_t(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n,
+// DTWLB_KEOGH_VAR (experiments): 0 = max3 form, 1 CTA/SM; 1 = clamp form, 1 CTA/SM;
+// 2 = max3 form, 2 CTAs/SM; 3 = clamp form, 2 CTAs/SM.
+int keogh_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DTWLB_KEOGH_VAR");
+        v = e ? atoi(e) : 2;  // default: max3 form, 2 CTAs per SM (measured best)
+        if (v < 0 || v > 3) v = 2;
+    }
+    return v;
+}
+
+template <int P, bool VEC, bool ROOTED, int VAR, int MINB>
+int launch_keogh_v(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n,
                    float *out, int64_t ldo, cudaStream_t st) {
     const size_t smem = 2 * sizeof(Stage);
-    auto k = keogh_tile_kernel<P, VEC, ROOTED>;
+    auto k = keogh_tile_kernel<P, VEC, ROOTED, VAR, MINB>;
     DTWLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t nqt = ceil_div(Q, TQ), nct = ceil_div(N, TC);
     const int64_t tiles = nqt * nct;
@@ -170,6 +205,17 @@ int launch_keogh_t(const float *U, const float *L, const float *db, int64_t Q, i
     k<<<(unsigned)tiles, NT, smem, st>>>(U, L, db, Q, N, n, out, ldo, (int)nqt);
     DTWLB_LAUNCH_CHECK();
     return DTWLB_OK;
+}
+
+template <int P, bool VEC, bool ROOTED>
+int launch_keogh_t(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n,
+                   float *out, int64_t ldo, cudaStream_t st) {
+    switch (keogh_variant()) {
+        case 1: return launch_keogh_v<P, VEC, ROOTED, 1, 1>(U, L, db, Q, N, n, out, ldo, st);
+        case 2: return launch_keogh_v<P, VEC, ROOTED, 0, 2>(U, L, db, Q, N, n, out, ldo, st);
+        case 3: return launch_keogh_v<P, VEC, ROOTED, 1, 2>(U, L, db, Q, N, n, out, ldo, st);
+        default: return launch_keogh_v<P, VEC, ROOTED, 0, 1>(U, L, db, Q, N, n, out, ldo, st);
+    }
 }
 
 }  // namespace

@@ -35,7 +35,13 @@ struct ImprovedArgs {
     float *dense;                  // [Qb][ldd], rooted
     int64_t ldd;
     unsigned long long *n_eval;    // stats: survivors evaluated (may be NULL)
+    // scratch: per 64-candidate tile, the list of (query, survivor mask) entries
+    unsigned long long *tile_m;    // [ceil(N/64)][Qb]
+    int *tile_q;                   // [ceil(N/64)][Qb]
+    int *tile_cnt;                 // [ceil(N/64)]
 };
+size_t improved_scratch_bytes(int64_t Qb, int64_t N);
+void improved_scratch_bind(ImprovedArgs &a, void *p);
 int launch_improved(const ImprovedArgs &a, int p, bool keogh_only, bool dense, cudaStream_t st);
 int improved_epl(int n);  // elements per lane (4, 8, 16, 32); 0 if n > 1024 (unsupported fast path)
 
@@ -51,6 +57,8 @@ struct DtwArgs {
     // PAIRS mode: item t -> candidate row t, query row t, no pruning
     // WALK mode: item t -> per-query sorted list entry
     const int *item_off;   // [Qb+1] prefix offsets of this round's items per query
+    const int *chunk_off;  // [Qb+1] prefix offsets of this round's warp chunks per query
+    int64_t nchunks;       // WALK: number of warp chunks (kDtwIpw items of one query each)
     const int *pos;        // [Qb] list position of the query's first item this round
     const unsigned long long *list;  // [Qb][cap]
     int64_t cap;
@@ -61,8 +69,10 @@ struct DtwArgs {
     unsigned long long *cells;  // stats: computed cells (may be NULL)
     unsigned long long *abandoned;  // stats (may be NULL)
     unsigned long long *started;    // stats: pairs whose DTW started (may be NULL)
+    unsigned *queue;                 // work-queue counter (scratch, 4 bytes) for the w <= 32 kernel
 };
-constexpr int kYPadL = 64;  // left padding of query rows (>= largest register band)
+constexpr int kYPadL = 64;
+constexpr int kDtwIpw = 64;  // items per warp chunk of the DTW walk  // left padding of query rows (>= largest register band)
 int dtw_padded_len(int n);
 int launch_dtw(const DtwArgs &a, int p, bool walk, cudaStream_t st);
 // Build the 4 shifted, +inf-padded copies of `rows` query rows.

@@ -73,7 +73,7 @@ std::mutex &ws_mutex() {
 
 enum Slot {
     S_QSTAGE, S_DBSTAGE, S_ENV, S_QPAD, S_YSH, S_DBENV, S_BETA1, S_LIST, S_RES, S_STATE, S_TOPK,
-    S_OUTSTAGE, S_SCRATCH, S_TMP, S_COUNT
+    S_OUTSTAGE, S_SCRATCH, S_TMP, S_MASK, S_COUNT
 };
 
 template <typename T>
@@ -170,8 +170,9 @@ struct QState {
     float *lo, *hi;  // current range of beta1
     float *tS;
     int *len, *pos, *rnd, *active;
-    int *item_off;   // [Qb+1]
-    int *counters;   // [0] total items of the round, [1] active queries
+    int *item_off;   // [Qb+1] first result slot of each query this round
+    int *chunk_off;  // [Qb+1] first warp chunk of each query this round
+    int *counters;   // [0] total items of the round, [1] total warp chunks
     unsigned long long *topk;  // [Qb][k]
     int *topk_n;
     unsigned long long *stat;  // [0] improved evals, [1] dtw items started, [2] cells, [3] abandoned
@@ -201,13 +202,39 @@ __global__ void start_walk_kernel(QState s, int Qb) {
     }
 }
 
-// Per-round plan: items of each active query = min(D0 * 2^round, remaining); exclusive scan.
+// Per-round plan: items of each active query = min(D0 * 2^round, remaining), and
+// the warp chunks (kDtwIpw items each, never spanning two queries) that hold them.
+// Two exclusive scans: item_off (results layout) and chunk_off (warp -> query).
 constexpr int kD0 = 32, kDMax = 65536;
-__global__ void __launch_bounds__(1024) plan_kernel(QState s, int Qb) {
-    __shared__ int warp_sums[32];
-    __shared__ int carry;
-    if (threadIdx.x == 0) carry = 0;
+__device__ __forceinline__ int2 block_scan2(int2 v, int2 *warp_sums, int2 &total) {
+    // inclusive block-wide scan of two ints; returns the inclusive value, sets total
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int tx = __shfl_up_sync(0xffffffffu, v.x, o), ty = __shfl_up_sync(0xffffffffu, v.y, o);
+        if (lane >= o) { v.x += tx; v.y += ty; }
+    }
+    if (lane == 31) warp_sums[wid] = v;
     __syncthreads();
+    if (wid == 0) {
+        int2 w = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : make_int2(0, 0);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int tx = __shfl_up_sync(0xffffffffu, w.x, o), ty = __shfl_up_sync(0xffffffffu, w.y, o);
+            if (lane >= o) { w.x += tx; w.y += ty; }
+        }
+        warp_sums[lane] = w;
+    }
+    __syncthreads();
+    if (wid) { v.x += warp_sums[wid - 1].x; v.y += warp_sums[wid - 1].y; }
+    total = warp_sums[(blockDim.x >> 5) - 1];
+    __syncthreads();
+    return v;
+}
+
+__global__ void __launch_bounds__(1024) plan_kernel(QState s, int Qb) {
+    __shared__ int2 warp_sums[32];
+    int2 carry = make_int2(0, 0);
     for (int base = 0; base < Qb; base += blockDim.x) {
         const int q = base + threadIdx.x;
         int cnt = 0;
@@ -216,39 +243,27 @@ __global__ void __launch_bounds__(1024) plan_kernel(QState s, int Qb) {
             d = min(d, kDMax);
             cnt = min(d, s.len[q] - s.pos[q]);
         }
-        // block-wide inclusive scan
-        int v = cnt;
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int t = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o) v += t;
+        const int2 mine = make_int2(cnt, (cnt + kDtwIpw - 1) / kDtwIpw);
+        int2 tot;
+        const int2 inc = block_scan2(mine, warp_sums, tot);
+        if (q < Qb) {
+            s.item_off[q] = carry.x + inc.x - mine.x;
+            s.chunk_off[q] = carry.y + inc.y - mine.y;
         }
-        if (lane == 31) warp_sums[wid] = v;
-        __syncthreads();
-        if (wid == 0) {
-            int ws_ = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int t = __shfl_up_sync(0xffffffffu, ws_, o);
-                if (lane >= o) ws_ += t;
-            }
-            warp_sums[lane] = ws_;
-        }
-        __syncthreads();
-        const int excl = carry + v - cnt + (wid ? warp_sums[wid - 1] : 0);
-        if (q < Qb) s.item_off[q] = excl;
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) carry = excl + cnt;
-        __syncthreads();
+        carry.x += tot.x;
+        carry.y += tot.y;
     }
     if (threadIdx.x == 0) {
-        s.item_off[Qb] = carry;
-        s.counters[0] = carry;
+        s.item_off[Qb] = carry.x;
+        s.chunk_off[Qb] = carry.y;
+        s.counters[0] = carry.x;
+        s.counters[1] = carry.y;
     }
 }
 
-// Merge a round's DTW results into each query's top-k; advance its walk.
+// Merge a round's DTW results into each query's top-k (keys (DTW^p bits, index),
+// ascending); advance its walk.  One warp per query; for k <= 32 the list lives in
+// registers (lane r = rank r) and an insertion is one ballot + one shuffle.
 __global__ void merge_kernel(QState s, int Qb, int k, float eps, const unsigned long long *__restrict__ list,
                              int64_t cap, const float *__restrict__ res) {
     const int lane = threadIdx.x & 31;
@@ -259,31 +274,62 @@ __global__ void merge_kernel(QState s, int Qb, int k, float eps, const unsigned 
     unsigned long long *tk = s.topk + (int64_t)q * k;
     const unsigned long long *lq = list + (int64_t)q * cap;
     const int p0 = s.pos[q];
-    int cnt = s.topk_n[q];
-    unsigned long long kth = tk[k - 1];
-    for (int b = o0; b < o1; b += 32) {
-        const int t = b + lane;
-        unsigned long long key = ~0ull;
-        if (t < o1) {
-            DCHECK(p0 + (t - o0) < s.len[q] && t < s.counters[0], "merge q=%d t=%d o0=%d p0=%d len=%d", q, t, o0, p0, s.len[q]);
-            const float d = res[t];
-            if (d < kInf) key = pack_key(d, (uint32_t)(lq[p0 + (t - o0)] & 0xffffffffu));
-        }
-        unsigned m = __ballot_sync(0xffffffffu, key < kth);
-        while (m) {
-            const int src = __ffs(m) - 1;
-            m &= m - 1;
-            const unsigned long long kk = __shfl_sync(0xffffffffu, key, src);
-            if (kk >= kth) continue;  // kth may have tightened
-            if (lane == 0) {  // sorted insertion of kk, dropping the current k-th
-                int j = min(cnt, k - 1);
-                while (j > 0 && tk[j - 1] > kk) { tk[j] = tk[j - 1]; --j; }
-                tk[j] = kk;
-                cnt = min(cnt + 1, k);
+    int cnt;
+    unsigned long long kth;
+    if (k <= 32) {
+        unsigned long long mykey = lane < k ? tk[lane] : ~0ull;
+        kth = __shfl_sync(0xffffffffu, mykey, k - 1);
+        for (int b = o0; b < o1; b += 32) {
+            const int t = b + lane;
+            unsigned long long key = ~0ull;
+            if (t < o1) {
+                DCHECK(p0 + (t - o0) < s.len[q], "merge q=%d t=%d o0=%d p0=%d len=%d", q, t, o0, p0, s.len[q]);
+                const float d = res[t];
+                if (d < kInf) key = pack_key(d, (uint32_t)(lq[p0 + (t - o0)] & 0xffffffffu));
             }
-            cnt = __shfl_sync(0xffffffffu, cnt, 0);
-            __syncwarp();
-            kth = tk[k - 1];
+            unsigned m = __ballot_sync(0xffffffffu, key < kth);
+            while (m) {
+                const int src = __ffs(m) - 1;
+                m &= m - 1;
+                const unsigned long long kk = __shfl_sync(0xffffffffu, key, src);
+                if (kk >= kth) continue;
+                const int at = __popc(__ballot_sync(0xffffffffu, lane < k && mykey < kk));
+                const unsigned long long up = __shfl_up_sync(0xffffffffu, mykey, 1);
+                if (lane < k) {
+                    if (lane > at) mykey = up;
+                    else if (lane == at) mykey = kk;
+                }
+                kth = __shfl_sync(0xffffffffu, mykey, k - 1);
+            }
+        }
+        if (lane < k) tk[lane] = mykey;
+        cnt = __popc(__ballot_sync(0xffffffffu, lane < k && mykey != ~0ull));
+    } else {
+        cnt = s.topk_n[q];
+        kth = tk[k - 1];
+        for (int b = o0; b < o1; b += 32) {
+            const int t = b + lane;
+            unsigned long long key = ~0ull;
+            if (t < o1) {
+                const float d = res[t];
+                if (d < kInf) key = pack_key(d, (uint32_t)(lq[p0 + (t - o0)] & 0xffffffffu));
+            }
+            unsigned m = __ballot_sync(0xffffffffu, key < kth);
+            while (m) {
+                const int src = __ffs(m) - 1;
+                m &= m - 1;
+                const unsigned long long kk = __shfl_sync(0xffffffffu, key, src);
+                if (kk >= kth) continue;  // kth may have tightened
+                if (lane == 0) {          // sorted insertion of kk, dropping the current k-th
+                    int j = min(cnt, k - 1);
+                    while (j > 0 && tk[j - 1] > kk) { tk[j] = tk[j - 1]; --j; }
+                    tk[j] = kk;
+                    cnt = min(cnt + 1, k);
+                }
+                cnt = __shfl_sync(0xffffffffu, cnt, 0);
+                __syncwarp();
+                kth = tk[k - 1];
+            }
         }
     }
     if (lane == 0) {
@@ -455,8 +501,10 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     DTWLB_TRY(wsget(S_LIST, (size_t)Qb * cap, &list));
     const int64_t res_cap = std::min<int64_t>(Qb * cap, Qb * (int64_t)kDMax);
     DTWLB_TRY(wsget(S_RES, (size_t)res_cap, &res));
+    char *imp_scratch;
+    DTWLB_TRY(wsget(S_MASK, improved_scratch_bytes(Qb, N), &imp_scratch));
     char *stb;
-    const size_t st_bytes = 16 * ((size_t)Qb * 4 * 8 + (Qb + 1) * 4 + 64 + 64 + 16 * 16) / 16;
+    const size_t st_bytes = (size_t)Qb * 4 * 8 + (Qb + 1) * 8 + 64 + 64 + 16 * 16;
     DTWLB_TRY(wsget(S_STATE, st_bytes, &stb));
     QState s;
     {
@@ -473,6 +521,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         s.rnd = reinterpret_cast<int *>(take(Qb * 4));
         s.active = reinterpret_cast<int *>(take(Qb * 4));
         s.item_off = reinterpret_cast<int *>(take((Qb + 1) * 4));
+        s.chunk_off = reinterpret_cast<int *>(take((Qb + 1) * 4));
     }
     DTWLB_TRY(wsget(S_TOPK, (size_t)Qb * k, &s.topk));
     int *topk_n;
@@ -488,6 +537,8 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     std::vector<int> h_len(Qb), run_q, run_idx;
     int *d_runs;
     double ms_keogh = 0, ms_select = 0, ms_improved = 0, ms_dtw = 0;
+    unsigned long long r1[3] = {0, 0, 0}, r1_base[4] = {0, 0, 0, 0};
+    int64_t walk_rounds = 0;
     cudaEvent_t ev[4];
     if (stats) for (auto &e : ev) cudaEventCreate(&e);
 
@@ -536,6 +587,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 ia.cap = cap;
                 ia.list_len = s.len;
                 ia.n_eval = s.stat + 0;
+                improved_scratch_bind(ia, imp_scratch);
                 DTWLB_TRY(launch_improved(ia, p, keogh_only, false, st));
             } else {
                 set_error(DTWLB_EUNSUPPORTED, "nn_search: n = %d > 1024 not supported", n);
@@ -561,11 +613,13 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
             start_walk_kernel<<<(unsigned)ceil_div(qn, 256), 256, 0, st>>>(s, (int)qn);
             DTWLB_LAUNCH_CHECK();
             for (int round = 0;; ++round) {
+                ++walk_rounds;
                 plan_kernel<<<1, 1024, 0, st>>>(s, (int)qn);
                 DTWLB_LAUNCH_CHECK();
-                int total = 0;
-                DTWLB_CUDA(cudaMemcpyAsync(&total, s.counters, sizeof(int), cudaMemcpyDeviceToHost, st));
+                int tot2[2] = {0, 0};
+                DTWLB_CUDA(cudaMemcpyAsync(tot2, s.counters, sizeof(tot2), cudaMemcpyDeviceToHost, st));
                 DTWLB_CUDA(cudaStreamSynchronize(st));
+                const int total = tot2[0];
                 if (total == 0) break;
                 DtwArgs da{};
                 da.ysh = ysh;
@@ -576,6 +630,8 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 da.n = n;
                 da.w = w;
                 da.item_off = s.item_off;
+                da.chunk_off = s.chunk_off;
+                da.nchunks = tot2[1];
                 da.pos = s.pos;
                 da.list = list;
                 da.cap = cap;
@@ -586,6 +642,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 da.cells = s.stat + 2;
                 da.abandoned = s.stat + 3;
                 da.started = s.stat + 1;
+                da.queue = reinterpret_cast<unsigned *>(s.counters + 4);
                 if (generic_dtw) DTWLB_TRY(launch_dtw_generic(da, queries + qb0 * n, scratch, p, true, st));
                 else {
                     da.ysh = ysh + qb0 * LP;
@@ -602,6 +659,15 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 cudaEventElapsedTime(&b, ev[1], ev[2]);
                 ms_improved += a;
                 ms_dtw += b;
+                if (macro == 0) {  // cumulative counters after range 1 (diagnostics)
+                    unsigned long long h[4];
+                    cudaMemcpy(h, s.stat, sizeof(h), cudaMemcpyDeviceToHost);
+                    r1[0] += h[0] - r1_base[0];
+                    r1[1] += h[1] - r1_base[1];
+                    r1[2] += h[2] - r1_base[2];
+                } else {
+                    cudaMemcpy(r1_base, s.stat, sizeof(r1_base), cudaMemcpyDeviceToHost);
+                }
             }
         }
         finalize_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(qn * k, 256), 4096)), 256, 0, st>>>(
@@ -632,6 +698,10 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         stats->ms_dtw = ms_dtw;
         stats->ms_total = tm.ms(0, 2);
         stats->kernel_launches = (int64_t)(__atomic_load_n(&g_launches, __ATOMIC_RELAXED) - launches0);
+        stats->range1_improved = (int64_t)r1[0];
+        stats->range1_dtw = (int64_t)r1[1];
+        stats->range1_cells = (int64_t)r1[2];
+        stats->walk_rounds = walk_rounds;
     }
     return DTWLB_OK;
 }
