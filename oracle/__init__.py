@@ -59,6 +59,8 @@ def _load():
             lib.oracle_projection.restype = None
             lib.oracle_lb_keogh.argtypes = [_dp, _dp, i, i, i]
             lib.oracle_lb_keogh.restype = d
+            lib.oracle_lb_piecewise.argtypes = [_dp, _dp, i, i, i, i]
+            lib.oracle_lb_piecewise.restype = d
             lib.oracle_lb_improved.argtypes = [_dp, _dp, i, i, i]
             lib.oracle_lb_improved.restype = d
             lib.oracle_dtw.argtypes = [_dp, _dp, i, i, i]
@@ -123,6 +125,13 @@ def lb_keogh(x, y, w, p):
     x, xp = _d(x)
     y, yp = _d(y)
     return _load().oracle_lb_keogh(xp, yp, x.shape[-1], int(w), int(p))
+
+
+def lb_piecewise(x, y, w, p, s=8):
+    """Piecewise-sum bound (p = 2 per reading c18), rooted; segment length s."""
+    x, xp = _d(x)
+    y, yp = _d(y)
+    return _load().oracle_lb_piecewise(xp, yp, x.shape[-1], int(w), int(s), int(p))
 
 
 def lb_improved(x, y, w, p):

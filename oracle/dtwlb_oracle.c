@@ -10,7 +10,7 @@
  *
  * Citations "P:n" are lines of the paper's LaTeX source, with the
  * section / equation / algorithm named alongside.  Readings of ambiguous
- * passages are numbered c1..c17 as in DESIGN.md ("Readings of the paper").
+ * passages are numbered c1..c18 as in DESIGN.md ("Readings of the paper").
  *
  * Conventions (section "Conventions"): series have length n; the
  * paper indexes 1..n, this file indexes 0..n-1 (index k here = k+1 there).
@@ -165,6 +165,44 @@ double oracle_lb_keogh(const double *x, const double *y, int n, int w, int p)
     free(U);
     free(L);
     return root_p(s, p);
+}
+
+/* Piecewise-sum lower bound (section "Using a multidimensional
+ * indexing structure"): with the cover C_j = [j*s, min((j+1)*s, n)) (the
+ * paper's equal-length cover P:662-665, last interval shorter) and
+ * P(v)_j = sum_{i in C_j} v_i,
+ *   p = 1:  sum_j d(P(x)_j, [P(L)_j, P(U)_j])          (the paper)
+ *   p = 2:  sum_j d(P(x)_j, [P(L)_j, P(U)_j])^2 / s    (reading c18: Cauchy-Schwarz
+ *           per interval, sum_{C_j} d_i^2 >= (sum_{C_j} d_i)^2 / |C_j|, |C_j| <= s)
+ * U, L: the query envelope.  Returns the p-th-power (unrooted) value. */
+double oracle_lb_piecewise_pow(const double *x, const double *U, const double *L, int n, int s, int p)
+{
+    double total = 0.0;
+    for (int j0 = 0; j0 < n; j0 += s) {
+        int j1 = j0 + s < n ? j0 + s : n;
+        double px = 0.0, pu = 0.0, pl = 0.0;
+        for (int i = j0; i < j1; ++i) {
+            px += x[i];
+            pu += U[i];
+            pl += L[i];
+        }
+        double d = 0.0; /* d(P(x)_j, [P(L)_j, P(U)_j]), P:123 point-to-set distance */
+        if (px > pu) d = px - pu;
+        else if (px < pl) d = pl - px;
+        total += p == 1 ? d : d * d / (double)s;
+    }
+    return total;
+}
+
+double oracle_lb_piecewise(const double *x, const double *y, int n, int w, int s, int p)
+{
+    double *U = (double *)malloc(sizeof(double) * (size_t)n);
+    double *L = (double *)malloc(sizeof(double) * (size_t)n);
+    oracle_envelope_naive(y, n, w, U, L);
+    double v = oracle_lb_piecewise_pow(x, U, L, n, s, p);
+    free(U);
+    free(L);
+    return root_p(v, p);
 }
 
 /* LB_Improved_p(x,y)^p = LB_Keogh_p(x,y)^p + LB_Keogh_p(y, H(x,y))^p

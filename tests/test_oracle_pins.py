@@ -276,3 +276,43 @@ def test_value_separated_error_is_exact():
 
 def test_lb_improved_rejects_infinity():
     assert math.isnan(oracle.lb_improved([1, 2], [2, 1], 1, 0))
+
+
+# ---------------------------------------------------------------- piecewise-sum pre-filter
+@pytest.mark.parametrize("case", GOLDEN["piecewise"], ids=lambda c: c["cite"][:30])
+def test_piecewise_golden(case):
+    """Hand-derived values of the piecewise-sum bound (p = 2 reading c18)."""
+    v = oracle.lb_piecewise(case["x"], case["y"], case["w"], case["p"], case["s"]) ** case["p"]
+    assert v == pytest.approx(case["value_pow"], abs=1e-12)
+
+
+def test_piecewise_chain_and_special_cases():
+    """piecewise <= LB_Keogh <= DTW (P:656-660 chain; p = 2 by Cauchy-Schwarz per interval);
+    s = 1 reduces to LB_Keogh; one interval (s >= n) is d(sum x, [sum L, sum U]) with the
+    envelope from numpy's sliding window (library routine); larger s never tightens when s
+    divides evenly (coarser cover of a refinement)."""
+    from numpy.lib.stride_tricks import sliding_window_view as swv
+    for _ in range(1500):
+        n = int(RNG.integers(1, 14))
+        integer = RNG.random() < 0.5
+        x = rand_int_series(n) if integer else RNG.standard_normal(n)
+        y = rand_int_series(n) if integer else RNG.standard_normal(n)
+        w = int(RNG.integers(0, n + 1))
+        for p in (1, 2):
+            kb = oracle.lb_keogh(x, y, w, p)
+            d = oracle.dtw(x, y, w, p)
+            tol = 1e-12 * (1 + d)
+            assert oracle.lb_piecewise(x, y, w, p, 1) == pytest.approx(kb, rel=1e-12, abs=1e-12)
+            for s in (2, 3, 4, 8):
+                pw = oracle.lb_piecewise(x, y, w, p, s)
+                assert pw <= kb + tol and pw <= d + tol
+            if n % 4 == 0:
+                assert oracle.lb_piecewise(x, y, w, p, 4) <= oracle.lb_piecewise(x, y, w, p, 2) + tol
+            we = min(w, n - 1)
+            yp = np.pad(np.asarray(y, float), (we, we), mode="edge")
+            U = swv(yp, 2 * we + 1).max(axis=1)
+            L = swv(yp, 2 * we + 1).min(axis=1)
+            sx, su, sl = float(np.sum(x)), float(U.sum()), float(L.sum())
+            one = max(sx - su, sl - sx, 0.0)
+            expect = one if p == 1 else one * one / n
+            assert oracle.lb_piecewise(x, y, w, p, n) ** p == pytest.approx(expect, rel=1e-9, abs=1e-9)
