@@ -186,7 +186,8 @@ def run_ours(args, cfg):
     last = {}
 
     def search(q_, d_, w_, p_, k_, index_base=0, out=None):
-        i_, d2, st_ = B.nn_search(q_, d_, w_, p_, k_, index_base=index_base, out=out, return_stats=True)
+        i_, d2, st_ = B.nn_search(q_, d_, w_, p_, k_, index_base=index_base, out=out, return_stats=True,
+                                  prefilter=not args.no_prefilter)
         last["st"] = st_
         return i_, d2
 
@@ -224,11 +225,12 @@ def run_ours(args, cfg):
     h_idx = torch.empty((cfg.Q, k), dtype=torch.int64).pin_memory()
     h_dst = torch.empty((cfg.Q, k), dtype=torch.float32).pin_memory()
     e2e_steps = max(1, min(args.steps, 3))
-    B.nn_search(qs_pin, db_pin, cfg.w, cfg.p, k, index_base=lo, out=(h_idx, h_dst))
+    B.nn_search(qs_pin, db_pin, cfg.w, cfg.p, k, index_base=lo, out=(h_idx, h_dst), prefilter=not args.no_prefilter)
     barrier()
     ev0.record(st)
     for _ in range(e2e_steps):
-        B.nn_search(qs_pin, db_pin, cfg.w, cfg.p, k, index_base=lo, out=(h_idx, h_dst))
+        B.nn_search(qs_pin, db_pin, cfg.w, cfg.p, k, index_base=lo, out=(h_idx, h_dst),
+                    prefilter=not args.no_prefilter)
     ev1.record(st)
     barrier()
     e2e_ms = torch.tensor([ev0.elapsed_time(ev1) / e2e_steps], device=dev)
@@ -250,6 +252,7 @@ def run_ours(args, cfg):
     keogh_ms = float(keogh_ms.item())
     pairs = cfg.Q * cfg.N
     improved = tot("improved_evaluated")
+    keogh_eval = tot("keogh_evaluated")
     dtw_eval = tot("dtw_evaluated")
     dtw_ab = tot("dtw_abandoned")
     cells_nom = tot("dtw_cells_nominal")
@@ -259,9 +262,11 @@ def run_ours(args, cfg):
         pk = _peaks()
         sm_clock = 1965.0 if not pk else float(pk.get("sm_max_mhz", 1965.0))
         n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-        # ALU roofline of the dominant kernel (LB_Keogh pass): 4 SASS lane-ops per
-        # pair-element (FADD, FADD, FMNMX3, FADD|FFMA), peak = SMs x 128 FP32 lanes x clock
-        ops = 4.0 * (cfg.Q * (cfg.N // ws)) * cfg.n
+        # ALU roofline of the dense gate pass (piecewise-sum bound over Dp = round_up(n/8, 4)
+        # segment sums, or LB_Keogh over n samples): 4 SASS lane-ops per pair-element
+        # (FADD, FADD, FMNMX3, FADD|FFMA), peak = SMs x 128 FP32 lanes x clock
+        elems = ((cfg.n + 7) // 8 + 3) // 4 * 4 if not args.no_prefilter else cfg.n
+        ops = 4.0 * (cfg.Q * (cfg.N // ws)) * elems
         achieved = ops / (keogh_ms * 1e-3) / 1e12
         peak = n_sm * 128 * sm_clock * 1e6 / 1e12
         traffic, traffic_note = None, None
@@ -297,7 +302,9 @@ def run_ours(args, cfg):
             "walk": {k2: statistics.mean(s[k2] for s in stats_all)
                      for k2 in ("range1_improved", "range1_dtw", "range1_cells", "walk_rounds", "dtw_evaluated",
                                 "dtw_cells_computed")},
-            "prune": {"keogh_pruned_frac": 1 - improved / pairs,
+            "prune": {"prefilter": not args.no_prefilter,
+                      "keogh_evaluated_frac": keogh_eval / pairs,
+                      "keogh_pruned_frac": 1 - improved / pairs,
                       "improved_evaluated_frac": improved / pairs,
                       "dtw_evaluated_frac": dtw_eval / pairs,
                       "dtw_abandoned_frac_of_evaluated": dtw_ab / max(1.0, dtw_eval)},
@@ -332,6 +339,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-prefilter", action="store_true",
+                    help="LB_Keogh over every pair (Alg. 3 as printed) instead of the piecewise-sum pre-filter")
     args = ap.parse_args()
     cfg = datagen.CONFIGS[args.config]
     if args.impl == "reference":

@@ -66,6 +66,18 @@ int lb_envelope(const float *x, int32_t n, int32_t w, float *U, float *L, int64_
 int lb_keogh(const float *q_env, const float *db, int64_t Q, int64_t N, int32_t n, int32_t p,
              float *out, void *stream);
 
+/* Piecewise-sum lower bound (section "Using a multidimensional
+ * indexing structure"), the cascade's pre-filter:
+ *   out[q][c]^p = sum_j d(P(x_c)_j, [P(L_q)_j, P(U_q)_j])^p * (p == 2 ? 1/s : 1)
+ * with P(v)_j = sum_{i in C_j} v_i over the cover C_j = [j*s, min((j+1)*s, n)),
+ * s = 8.  p = 1 is the paper's bound (<= LB_Keogh_1); p = 2 adds
+ * the per-segment Cauchy-Schwarz step (sum_{C_j} d_i^2 >= (sum_{C_j} d_i)^2/|C_j|,
+ * |C_j| <= s; reading c18).  Evaluated with outward rounding, so the
+ * returned value never exceeds the exact bound (hence never exceeds LB_Keogh_p
+ * or DTW_p).  q_env, db, out and errors as lb_keogh. */
+int lb_piecewise(const float *q_env, const float *db, int64_t Q, int64_t N, int32_t n, int32_t p,
+                 float *out, void *stream);
+
 /* LB_Improved_p (section "LB_Improved"; Alg. 3 lines P:587-606):
  *   out[q][c]^p = LB_Keogh_p(x_c, y_q)^p + LB_Keogh_p(y_q, H(x_c, y_q))^p,
  * i.e. the first pass plus the distance of y to the envelope of the
@@ -89,16 +101,21 @@ typedef struct nn_opts {
                               (p-th-power space); default 1e-3 (reading c13) */
     int64_t index_base;    /* added to every returned index (database shards)        */
     int32_t query_block;   /* queries per pipeline block; 0 = automatic              */
-    int32_t flags;         /* DTWLB_KEOGH_ONLY: skip the LB_Improved pass (Alg. 2)   */
+    int32_t flags;         /* DTWLB_KEOGH_ONLY: skip the LB_Improved pass (Alg. 2);
+                              DTWLB_NO_PREFILTER: LB_Keogh over every pair (Alg. 3
+                              literally) instead of the piecewise-sum pre-filter;
+                              DTWLB_NO_CASCADE: see below                           */
     int32_t reserved[4];
 } nn_opts;
 
 #define DTWLB_KEOGH_ONLY 1
+#define DTWLB_NO_PREFILTER 2
+#define DTWLB_NO_CASCADE 4   /* DTW abandons on the row minimum alone (no LB_Keogh suffix) */
 
 /* Counters of one nn_search call (host struct, filled on return). */
 typedef struct nn_stats {
     int64_t pairs;            /* Q*N query-candidate pairs                            */
-    int64_t keogh_evaluated;  /* LB_Keogh evaluations (= pairs)                       */
+    int64_t keogh_evaluated;  /* LB_Keogh evaluations (= pairs without the pre-filter) */
     int64_t improved_evaluated; /* LB_Improved evaluations (LB_Keogh survivors seen)  */
     int64_t dtw_evaluated;    /* DTW evaluations started                              */
     int64_t dtw_abandoned;    /* ... of which early-abandoned                         */
@@ -109,15 +126,20 @@ typedef struct nn_stats {
     int64_t range1_improved, range1_dtw, range1_cells; /* ... of the above, in the first
                                    (best-first seed) range of candidates               */
     int64_t walk_rounds;        /* DTW walk rounds (plan -> DTW -> merge)              */
+    int64_t prefilter_evaluated; /* piecewise-sum bound evaluations (pairs, or 0)      */
+    int32_t prefilter_segment;   /* segment length s of the pre-filter (0 = off)       */
+    int32_t reserved_;
 } nn_stats;
 
 /* Exact k-nearest-neighbour search under banded DTW_p: for each query y_q,
  * the k database rows with the smallest (DTW_p(y_q, x_c), c) in lexicographic
  * order (ties to the smaller index), by the paper's cascade (Alg. 3,
  * P:578-620, generalised to p in {1,2}, k >= 1 and many queries): query
- * envelope -> LB_Keogh over the whole database -> LB_Improved on survivors ->
- * banded DTW on what remains, each gate pruning only when the bound exceeds
- * the current k-th best times (1+eps).
+ * envelope -> [piecewise-sum bound over the whole database ->]
+ * LB_Keogh -> LB_Improved on survivors -> banded DTW on what remains, each gate
+ * pruning only when the bound exceeds the current k-th best times (1+eps).
+ * Without the pre-filter (DTWLB_NO_PREFILTER) LB_Keogh runs over the whole
+ * database, as Alg. 3 is printed.
  *   queries: [Q][n] float32, db: [N][n] float32 -- device OR host pointers
  *            (host buffers are staged to the device inside the call);
  *   out_idx: [Q][k] int64 (index_base + row), out_dist: [Q][k] float32 rooted

@@ -17,6 +17,8 @@ LIB_PATH = os.environ.get("DTWLB_LIB") or os.path.join(_HERE, "libdtwlb.so")
 
 STATUS = {0: "OK", 1: "EINVAL", 2: "EUNSUPPORTED", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL"}
 KEOGH_ONLY = 1
+NO_PREFILTER = 2
+NO_CASCADE = 4
 MAX_K = 1024
 
 
@@ -40,13 +42,15 @@ class NnStats(ctypes.Structure):
                 ("ms_keogh", ctypes.c_double), ("ms_select", ctypes.c_double),
                 ("ms_improved", ctypes.c_double), ("ms_dtw", ctypes.c_double), ("ms_total", ctypes.c_double),
                 ("kernel_launches", ctypes.c_int64), ("range1_improved", ctypes.c_int64),
-                ("range1_dtw", ctypes.c_int64), ("range1_cells", ctypes.c_int64), ("walk_rounds", ctypes.c_int64)]
+                ("range1_dtw", ctypes.c_int64), ("range1_cells", ctypes.c_int64), ("walk_rounds", ctypes.c_int64),
+                ("prefilter_evaluated", ctypes.c_int64), ("prefilter_segment", ctypes.c_int32),
+                ("reserved_", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
-EXPORTS = ["lb_envelope", "lb_keogh", "lb_improved", "dtw_band", "nn_search", "nn_merge",
+EXPORTS = ["lb_envelope", "lb_keogh", "lb_piecewise", "lb_improved", "dtw_band", "nn_search", "nn_merge",
            "dtwlb_last_error", "dtwlb_release_workspace"]
 
 _lib = None
@@ -62,12 +66,13 @@ def load():
         vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
         lib.lb_envelope.argtypes = [vp, i32, i32, vp, vp, i64, vp]
         lib.lb_keogh.argtypes = [vp, vp, i64, i64, i32, i32, vp, vp]
+        lib.lb_piecewise.argtypes = [vp, vp, i64, i64, i32, i32, vp, vp]
         lib.lb_improved.argtypes = [vp, vp, vp, i64, i64, i32, i32, i32, vp, vp]
         lib.dtw_band.argtypes = [vp, vp, i32, i32, i32, vp, i64, vp]
         lib.nn_search.argtypes = [vp, i64, vp, i64, i32, i32, i32, i32, vp, vp,
                                   ctypes.POINTER(NnOpts), ctypes.POINTER(NnStats), vp]
         lib.nn_merge.argtypes = [vp, vp, i32, i64, i32, vp, vp, vp]
-        for f in ("lb_envelope", "lb_keogh", "lb_improved", "dtw_band", "nn_search", "nn_merge"):
+        for f in ("lb_envelope", "lb_keogh", "lb_piecewise", "lb_improved", "dtw_band", "nn_search", "nn_merge"):
             getattr(lib, f).restype = ctypes.c_int
         lib.dtwlb_last_error.restype = ctypes.c_char_p
         lib.dtwlb_last_error.argtypes = []
@@ -117,6 +122,17 @@ def lb_keogh(q_env: torch.Tensor, db: torch.Tensor, p: int) -> torch.Tensor:
     return out
 
 
+def lb_piecewise(q_env: torch.Tensor, db: torch.Tensor, p: int) -> torch.Tensor:
+    """[Q][N] piecewise-sum bound (rooted, outward-rounded); q_env as lb_keogh."""
+    q_env = _dev(q_env, "q_env")
+    db = _dev(db, "db")
+    Q, n = q_env.shape[1], q_env.shape[2]
+    N = db.shape[0]
+    out = torch.empty((Q, N), dtype=torch.float32, device=db.device)
+    _check(load().lb_piecewise(q_env.data_ptr(), db.data_ptr(), Q, N, n, p, out.data_ptr(), _stream()))
+    return out
+
+
 def lb_improved(q: torch.Tensor, q_env: torch.Tensor, db: torch.Tensor, w: int, p: int) -> torch.Tensor:
     """[Q][N] LB_Improved_p (rooted)."""
     q, q_env, db = _dev(q, "q"), _dev(q_env, "q_env"), _dev(db, "db")
@@ -137,17 +153,19 @@ def dtw_band(x: torch.Tensor, y: torch.Tensor, w: int, p: int) -> torch.Tensor:
     return out
 
 
-def _opts(eps, index_base, query_block, keogh_only):
+def _opts(eps, index_base, query_block, keogh_only, prefilter=True, cascade=True):
     o = NnOpts()
     o.eps = eps
     o.index_base = index_base
     o.query_block = query_block
-    o.flags = KEOGH_ONLY if keogh_only else 0
+    o.flags = (KEOGH_ONLY if keogh_only else 0) | (0 if prefilter else NO_PREFILTER) | (0 if cascade else NO_CASCADE)
     return o
 
 
 def nn_search(queries, db, w: int, p: int, k: int, *, eps: float = 1e-3, index_base: int = 0,
-              query_block: int = 0, keogh_only: bool = False, out=None, return_stats: bool = False):
+              query_block: int = 0, keogh_only: bool = False, prefilter: bool = True, cascade: bool = True,
+              out=None,
+              return_stats: bool = False):
     """Exact k-NN under banded DTW_p.  Returns (idx int64 [Q][k], dist float32 [Q][k]).
 
     queries/db may be CUDA tensors (device path) or host tensors / numpy arrays
@@ -170,7 +188,7 @@ def nn_search(queries, db, w: int, p: int, k: int, *, eps: float = 1e-3, index_b
         dist = torch.empty((Q, k), dtype=torch.float32, device=dev, pin_memory=host)
     else:
         idx, dist = out
-    o = _opts(eps, index_base, query_block, keogh_only)
+    o = _opts(eps, index_base, query_block, keogh_only, prefilter, cascade)
     st = NnStats()
     _check(load().nn_search(queries.data_ptr(), Q, db.data_ptr(), N, n, w, p, k, idx.data_ptr(),
                             dist.data_ptr(), ctypes.byref(o), ctypes.byref(st) if return_stats else None,

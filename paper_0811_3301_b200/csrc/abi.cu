@@ -107,6 +107,28 @@ int lb_keogh(const float *q_env, const float *db, int64_t Q, int64_t N, int32_t 
     return launch_keogh(q_env, q_env + Q * n, db, Q, N, n, p, true, out, N, as_stream(stream));
 }
 
+int lb_piecewise(const float *q_env, const float *db, int64_t Q, int64_t N, int32_t n, int32_t p, float *out,
+                 void *stream) {
+    g_err[0] = 0;
+    CHECK_ARG(n >= 1, "lb_piecewise: n = %d < 1", n);
+    CHECK_ARG(Q >= 0 && N >= 0, "lb_piecewise: negative size");
+    DTWLB_TRY(check_p(p));
+    if (Q == 0 || N == 0) return DTWLB_OK;
+    CHECK_ARG(q_env && db && out, "lb_piecewise: NULL pointer");
+    DTWLB_TRY(require_device());
+    std::lock_guard<std::mutex> lock(api_mutex());
+    cudaStream_t st = as_stream(stream);
+    const int Dp = paa_pitch(n);
+    float *xs, *qs;
+    DTWLB_TRY(ws_get_bytes(7, sizeof(float) * 2 * N * Dp, (void **)&xs));
+    DTWLB_TRY(ws_get_bytes(8, sizeof(float) * 2 * Q * Dp, (void **)&qs));
+    DTWLB_TRY(launch_paa_sums(db, N, n, xs, xs + N * Dp, st));
+    DTWLB_TRY(launch_paa_env_sums(q_env, q_env + Q * n, Q, n, qs, qs + Q * Dp, st));
+    DTWLB_TRY(launch_paa_bound(qs, qs + Q * Dp, xs, xs + N * Dp, Q, N, n, p, true, out, N, st));
+    DTWLB_CUDA(cudaStreamSynchronize(st));  // workspace reuse safety
+    return DTWLB_OK;
+}
+
 int lb_improved(const float *q, const float *q_env, const float *db, int64_t Q, int64_t N, int32_t n,
                 int32_t w, int32_t p, float *out, void *stream) {
     g_err[0] = 0;
@@ -150,7 +172,7 @@ int lb_improved(const float *q, const float *q_env, const float *db, int64_t Q, 
     a.ULq = qpad + 2 * Q * npadE;
     a.Ux = dbenv;
     a.Lx = dbenv + N * n;
-    a.beta1 = beta1;
+    a.gate = beta1;
     a.ldb = ldb;
     a.Qb = Q;
     a.N = N;

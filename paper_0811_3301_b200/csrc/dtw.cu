@@ -107,6 +107,16 @@ __device__ __forceinline__ void load_x8(float (&xv)[8], const float *__restrict_
     }
 }
 
+// LB_Keogh term of row i: d(x_i, [L(y)_i, U(y)_i])^p.  Every banded path visits row i
+// in some column j with |i-j| <= w, at cost |x_i - y_j|^p >= this term, so the sum of
+// the terms of the rows not yet computed bounds what the path still has to pay
+// (cascading abandon, reading c19).
+template <int P>
+__device__ __forceinline__ float row_lb(float x, float u, float l) {
+    const float d = max3f(x - u, l - x, 0.f);
+    return P == 1 ? d : d * d;
+}
+
 template <int WB>
 __device__ __forceinline__ float band_min(const float (&B)[2 * WB + 2]) {
     float m = B[0];
@@ -172,6 +182,10 @@ dtw_kernel(DtwArgs a, int ipw) {
     int i = 0;
     float B[NB + 1];
     float xv[8];  // x of the current 8-row block
+    // cascading abandon: rest = LB_Keogh^p terms of the rows not yet computed
+    const bool casc = WALK && a.b1 != nullptr;
+    float rest = 0.f;
+    const float *ur = nullptr, *lr = nullptr;
     unsigned long long rows_done = 0, n_abandon = 0, n_started = 0;
 
     while (true) {
@@ -194,6 +208,11 @@ dtw_kernel(DtwArgs a, int ipw) {
                     thr = thr_q;
                     xr = a.db + (int64_t)c * n;
                     yb = yq;
+                    if (casc) {
+                        rest = fabsf(__ldg(a.b1 + (int64_t)q * a.ldb + c));  // beta1 = sum of all row terms
+                        ur = a.Uq + (int64_t)q * n;
+                        lr = a.Lq + (int64_t)q * n;
+                    }
                 } else {
                     thr = kInf;
                     xr = a.db + item * n;
@@ -224,6 +243,11 @@ dtw_kernel(DtwArgs a, int ipw) {
             const int i0 = i, iend = min(n, i + 8);
             float xn[8];
             load_x8(xn, xr, iend, n);
+            if (casc) {
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                    if (i0 + t < iend) rest -= row_lb<P>(xv[t], __ldg(ur + i0 + t), __ldg(lr + i0 + t));
+            }
             while (i + 1 < iend) {
                 const int s0 = i - w + kYPadL;
                 const float *ys = yb + (int64_t)(s0 & 3) * ystride + (s0 & ~3);
@@ -250,8 +274,8 @@ dtw_kernel(DtwArgs a, int ipw) {
                 }
                 a.res[item] = WALK ? r : rootp<P>(r);
                 has = false;
-            } else if (band_min<WB>(B) > thr) {
-                a.res[item] = kInf;  // early abandon (reading c15)
+            } else if (band_min<WB>(B) + rest > thr) {
+                a.res[item] = kInf;  // early abandon (readings c15, c19)
                 ++n_abandon;
                 has = false;
             }
@@ -347,6 +371,10 @@ dtw4_kernel(DtwArgs a) {
     float thr = kInf;
     int i = 0;
     float B[NB + 1], Y[NY];
+    // cascading abandon: rest = LB_Keogh^p terms of the rows not yet computed
+    const bool casc = WALK && a.b1 != nullptr;
+    float rest = 0.f;
+    const float *ur = nullptr, *lr = nullptr;
     unsigned long long rows_done = 0, n_abandon = 0, n_started = 0;
 
     while (true) {
@@ -385,6 +413,11 @@ dtw4_kernel(DtwArgs a) {
                     beta = __uint_as_float((uint32_t)(key >> 32));
                     thr = a.thr[q];
                     xr = a.db + (int64_t)c * n;
+                    if (casc) {
+                        rest = fabsf(__ldg(a.b1 + (int64_t)q * a.ldb + c));  // beta1 = sum of all row terms
+                        ur = a.Uq + (int64_t)q * n;
+                        lr = a.Lq + (int64_t)q * n;
+                    }
                     yr = a.ysh + (int64_t)sh * a.ysh_stride_s + (int64_t)q * a.LP;
                 } else {
                     thr = kInf;
@@ -440,6 +473,17 @@ dtw4_kernel(DtwArgs a) {
 #pragma unroll
                     for (int t = 0; t < 4; ++t) xv[t] = __ldg(xr + i + t);
                 }
+                if (casc) {
+                    if ((n & 3) == 0) {
+                        const float4 u4 = __ldg(reinterpret_cast<const float4 *>(ur + i));
+                        const float4 l4 = __ldg(reinterpret_cast<const float4 *>(lr + i));
+                        rest -= row_lb<P>(xv[0], u4.x, l4.x) + row_lb<P>(xv[1], u4.y, l4.y) +
+                                row_lb<P>(xv[2], u4.z, l4.z) + row_lb<P>(xv[3], u4.w, l4.w);
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) rest -= row_lb<P>(xv[t], __ldg(ur + i + t), __ldg(lr + i + t));
+                    }
+                }
                 four_rows<WB, P, EXACT>(B, Y, xv, w2);
                 i += 4;
                 // shift the y window by four and append y[i + w + 1 .. i + w + 4] (next block)
@@ -452,6 +496,7 @@ dtw4_kernel(DtwArgs a) {
             }
             if (i + 4 > n && i < n) {  // tail rows (n % 4 != 0): one row at a time
                 while (i < n) {
+                    if (casc) rest -= row_lb<P>(__ldg(xr + i), __ldg(ur + i), __ldg(lr + i));
                     float prev = kInf;
 #pragma unroll
                     for (int d = 0; d < NB; ++d) {
@@ -476,8 +521,8 @@ dtw4_kernel(DtwArgs a) {
                 }
                 a.res[item] = WALK ? r : rootp<P>(r);
                 has = false;
-            } else if (band_min<WB>(B) > thr) {
-                a.res[item] = kInf;
+            } else if (band_min<WB>(B) + rest > thr) {
+                a.res[item] = kInf;  // early abandon (readings c15, c19)
                 ++n_abandon;
                 has = false;
             }

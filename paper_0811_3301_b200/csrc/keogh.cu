@@ -9,16 +9,17 @@
 // pair tile.  Chunks of 32 samples of the envelopes U, L and of the candidate
 // rows are staged in shared memory with cp.async (double-buffered), read back
 // as 128-bit vectors, and each loaded value is reused 8x (envelope) or 4x
-// (candidate) from registers.  Per pair-element: FMNMX, FMNMX (the clamp of x
-// into [L, U], ALU pipe), FADD, FFMA|FADD (FMA pipe): 4 ops split 2/2 over the
-// two pipes, which measured faster than the 3-FMA-pipe-op form
-// max(x-U, L-x, 0) ("LB_Keogh instruction mix").  Per-chunk partial
-// sums are folded into the total at each chunk end (two-level summation keeps
-// the fp32 error at ~(32 + n/32) ulp instead of n ulp).
+// (candidate) from registers.  Per pair-element: FADD, FADD, FMNMX3, FADD|FFMA
+// (d = max(x - U, L - x, 0); 3 FMA-pipe ops + 1 half-rate ALU op, issue-bound).
+// Per-chunk partial sums are folded into the total at each chunk end (two-level
+// summation keeps the fp32 error at ~(32 + n/32) ulp instead of n ulp).
 // CTAs are ordered query-tile-fastest so each database tile is fetched from
 // HBM once and served from L2 to every query tile; the envelopes of the whole
 // query block stay L2-resident.  The i-tail beyond n is zero-filled on both
 // sides, which contributes max(0-0, 0-0, 0) = 0.
+//
+// The same tile kernel evaluates the piecewise-sum pre-filter over
+// segment sums (PAA = true): D = n/8 "samples" per row, directed rounding.
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -42,18 +43,13 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+template <bool PAA>
 struct Stage {  // chunk of the operands, written by cp.async (double-buffered)
-    float X[TC][KP];
+    float X[TC][KP];           // candidate rows (LB_Keogh) or their lower sums (PAA)
+    float X2[PAA ? TC : 1][KP];  // PAA: upper sums of the candidate segments
     float U[TQ][KP];
     float L[TQ][KP];
 };
-// acc + |d|^p for a signed deviation d (p=1: FADD with |.| operand; p=2: FFMA)
-template <int P>
-__device__ __forceinline__ float acc_dev(float acc, float d) {
-    if constexpr (P == 1) return acc + fabsf(d);
-    else return fmaf(d, d, acc);
-}
-
 // Stage chunk [k0, k0+KC) of rows r0.. of a [rows][n] matrix into S[R][KP].
 template <int R, bool VEC>
 __device__ __forceinline__ void stage_rows(float (*S)[KP], const float *__restrict__ g, int64_t r0,
@@ -80,12 +76,28 @@ __device__ __forceinline__ void stage_rows(float (*S)[KP], const float *__restri
     }
 }
 
-template <int P, bool VEC, bool ROOTED, int VAR, int MINB>
-__global__ void __launch_bounds__(NT, MINB)
+// PAA = false: LB_Keogh^p, d = max(x - U, L - x, 0), FADD, FADD, FMNMX3, FADD|FFMA.
+// PAA = true:  piecewise-sum bound over segment sums with directed rounding:
+//   d = max(Xlo - Uhi, Llo - Xhi, 0) (rounded down), acc += d^p (rounded down), so the
+//   result never exceeds the exact sum_j d(X_j, [L_j, U_j])^p; same 4 ops per element.
+template <int P, bool PAA>
+__device__ __forceinline__ float lb_elem(float acc, float xl, float xh, float u, float l) {
+    if constexpr (PAA) {
+        const float d = max3f(__fsub_rd(xl, u), __fsub_rd(l, xh), 0.f);
+        if constexpr (P == 1) return __fadd_rd(acc, d);
+        else return __fmaf_rd(d, d, acc);
+    } else {
+        return accp<P>(acc, max3f(xl - u, l - xl, 0.f));
+    }
+}
+
+template <int P, bool VEC, bool ROOTED, bool PAA>
+__global__ void __launch_bounds__(NT, 2)
 keogh_tile_kernel(const float *__restrict__ U, const float *__restrict__ L, const float *__restrict__ db,
-                  int64_t Q, int64_t N, int n, float *__restrict__ out, int64_t ldo, int nqt) {
+                  const float *__restrict__ db2, int64_t Q, int64_t N, int n, float *__restrict__ out,
+                  int64_t ldo, int nqt) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    Stage *st = reinterpret_cast<Stage *>(smraw);
+    Stage<PAA> *st = reinterpret_cast<Stage<PAA> *>(smraw);
 
     const int64_t tile = blockIdx.x;
     const int64_t q0 = (tile % nqt) * TQ;
@@ -102,21 +114,23 @@ keogh_tile_kernel(const float *__restrict__ U, const float *__restrict__ L, cons
 
     const int nchunks = (n + KC - 1) / KC;
     stage_rows<TC, VEC>(st[0].X, db, c0, N, n, 0);
+    if constexpr (PAA) stage_rows<TC, VEC>(st[0].X2, db2, c0, N, n, 0);
     stage_rows<TQ, VEC>(st[0].U, U, q0, Q, n, 0);
     stage_rows<TQ, VEC>(st[0].L, L, q0, Q, n, 0);
     cp_commit();
 
     for (int ch = 0; ch < nchunks; ++ch) {
         if (ch + 1 < nchunks) {
-            Stage &nx = st[(ch + 1) & 1];
+            Stage<PAA> &nx = st[(ch + 1) & 1];
             stage_rows<TC, VEC>(nx.X, db, c0, N, n, (ch + 1) * KC);
+            if constexpr (PAA) stage_rows<TC, VEC>(nx.X2, db2, c0, N, n, (ch + 1) * KC);
             stage_rows<TQ, VEC>(nx.U, U, q0, Q, n, (ch + 1) * KC);
             stage_rows<TQ, VEC>(nx.L, L, q0, Q, n, (ch + 1) * KC);
         }
         cp_commit();
         cp_wait<1>();
         __syncthreads();
-        const Stage &s = st[ch & 1];
+        const Stage<PAA> &s = st[ch & 1];
         float part[4][8];
 #pragma unroll
         for (int r = 0; r < 4; ++r)
@@ -125,44 +139,32 @@ keogh_tile_kernel(const float *__restrict__ U, const float *__restrict__ L, cons
 
 #pragma unroll 2
         for (int k = 0; k < KC; k += 4) {
-            float4 xv[8], uv[4], lv[4];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) xv[j] = *reinterpret_cast<const float4 *>(&s.X[cg + 16 * j][k]);
+            float4 uv[4], lv[4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
                 uv[r] = *reinterpret_cast<const float4 *>(&s.U[4 * qg + r][k]);
                 lv[r] = *reinterpret_cast<const float4 *>(&s.L[4 * qg + r][k]);
             }
-            if constexpr (VAR == 1) {
-                // d = x - clamp(x, L, U) (= x - H(x,y)_i of Eq. (1)); acc += |d|^p:
-                // FMNMX, FMNMX (ALU pipe), FADD, FFMA|FADD (FMA pipe)
 #pragma unroll
-                for (int r = 0; r < 4; ++r)
+            for (int j = 0; j < 8; ++j) {
+                const float4 xv = *reinterpret_cast<const float4 *>(&s.X[cg + 16 * j][k]);
+                float4 xw = xv;
+                if constexpr (PAA) xw = *reinterpret_cast<const float4 *>(&s.X2[cg + 16 * j][k]);
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        part[r][j] = acc_dev<P>(part[r][j], xv[j].x - fminf(fmaxf(xv[j].x, lv[r].x), uv[r].x));
-                        part[r][j] = acc_dev<P>(part[r][j], xv[j].y - fminf(fmaxf(xv[j].y, lv[r].y), uv[r].y));
-                        part[r][j] = acc_dev<P>(part[r][j], xv[j].z - fminf(fmaxf(xv[j].z, lv[r].z), uv[r].z));
-                        part[r][j] = acc_dev<P>(part[r][j], xv[j].w - fminf(fmaxf(xv[j].w, lv[r].w), uv[r].w));
-                    }
-            } else {
-                // d = max(x - U, L - x, 0); acc += d^p: FADD, FADD, FMNMX3(.., 0), FFMA|FADD
-#pragma unroll
-                for (int r = 0; r < 4; ++r)
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        float d;
-                        d = max3f(xv[j].x - uv[r].x, lv[r].x - xv[j].x, 0.f); part[r][j] = accp<P>(part[r][j], d);
-                        d = max3f(xv[j].y - uv[r].y, lv[r].y - xv[j].y, 0.f); part[r][j] = accp<P>(part[r][j], d);
-                        d = max3f(xv[j].z - uv[r].z, lv[r].z - xv[j].z, 0.f); part[r][j] = accp<P>(part[r][j], d);
-                        d = max3f(xv[j].w - uv[r].w, lv[r].w - xv[j].w, 0.f); part[r][j] = accp<P>(part[r][j], d);
-                    }
+                for (int r = 0; r < 4; ++r) {
+                    float t = part[r][j];
+                    t = lb_elem<P, PAA>(t, xv.x, xw.x, uv[r].x, lv[r].x);
+                    t = lb_elem<P, PAA>(t, xv.y, xw.y, uv[r].y, lv[r].y);
+                    t = lb_elem<P, PAA>(t, xv.z, xw.z, uv[r].z, lv[r].z);
+                    t = lb_elem<P, PAA>(t, xv.w, xw.w, uv[r].w, lv[r].w);
+                    part[r][j] = t;
+                }
             }
         }
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[r][j] += part[r][j];
+            for (int j = 0; j < 8; ++j) acc[r][j] = PAA ? __fadd_rd(acc[r][j], part[r][j]) : acc[r][j] + part[r][j];
         __syncthreads();
     }
 
@@ -173,59 +175,45 @@ keogh_tile_kernel(const float *__restrict__ U, const float *__restrict__ L, cons
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             int64_t c = c0 + cg + 16 * j;
-            if (c < N) out[q * ldo + c] = ROOTED ? rootp<P>(acc[r][j]) : acc[r][j];
+            if (c >= N) continue;
+            float v = acc[r][j];
+            if constexpr (PAA) {
+                // Cauchy-Schwarz per segment: sum_{i in C_j} d_i^2 >= (sum d_i)^2 / |C_j| >= D_j^2 / s
+                if constexpr (P == 2) v = __fmul_rd(v, 1.0f / kSeg);
+                if constexpr (ROOTED) v = P == 1 ? v : __fsqrt_rd(v);
+            } else if constexpr (ROOTED) {
+                v = rootp<P>(v);
+            }
+            out[q * ldo + c] = v;
         }
     }
 }
 
-// DTWLB_KEOGH_VAR (experiments): 0 = max3 form, 1 CTA/SM; 1 = clamp form, 1 CTA/SM;
-// 2 = max3 form, 2 CTAs/SM; 3 = clamp form, 2 CTAs/SM.
-int keogh_variant() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("DTWLB_KEOGH_VAR");
-        v = e ? atoi(e) : 2;  // default: max3 form, 2 CTAs per SM (measured best)
-        if (v < 0 || v > 3) v = 2;
-    }
-    return v;
-}
-
-template <int P, bool VEC, bool ROOTED, int VAR, int MINB>
-int launch_keogh_v(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n,
-                   float *out, int64_t ldo, cudaStream_t st) {
-    const size_t smem = 2 * sizeof(Stage);
-    auto k = keogh_tile_kernel<P, VEC, ROOTED, VAR, MINB>;
+template <int P, bool VEC, bool ROOTED, bool PAA>
+int launch_tile_t(const float *U, const float *L, const float *db, const float *db2, int64_t Q, int64_t N,
+                  int n, float *out, int64_t ldo, cudaStream_t st) {
+    const size_t smem = 2 * sizeof(Stage<PAA>);
+    auto k = keogh_tile_kernel<P, VEC, ROOTED, PAA>;
     DTWLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t nqt = ceil_div(Q, TQ), nct = ceil_div(N, TC);
     const int64_t tiles = nqt * nct;
     if (tiles > 0x7fffffffLL) {
-        set_error(DTWLB_EINVAL, "lb_keogh: problem too large (%lld tiles)", (long long)tiles);
+        set_error(DTWLB_EINVAL, "bound pass: problem too large (%lld tiles)", (long long)tiles);
         return DTWLB_EINVAL;
     }
-    k<<<(unsigned)tiles, NT, smem, st>>>(U, L, db, Q, N, n, out, ldo, (int)nqt);
+    k<<<(unsigned)tiles, NT, smem, st>>>(U, L, db, db2, Q, N, n, out, ldo, (int)nqt);
     DTWLB_LAUNCH_CHECK();
     return DTWLB_OK;
 }
 
-template <int P, bool VEC, bool ROOTED>
-int launch_keogh_t(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n,
-                   float *out, int64_t ldo, cudaStream_t st) {
-    switch (keogh_variant()) {
-        case 1: return launch_keogh_v<P, VEC, ROOTED, 1, 1>(U, L, db, Q, N, n, out, ldo, st);
-        case 2: return launch_keogh_v<P, VEC, ROOTED, 0, 2>(U, L, db, Q, N, n, out, ldo, st);
-        case 3: return launch_keogh_v<P, VEC, ROOTED, 1, 2>(U, L, db, Q, N, n, out, ldo, st);
-        default: return launch_keogh_v<P, VEC, ROOTED, 0, 1>(U, L, db, Q, N, n, out, ldo, st);
-    }
-}
-
-}  // namespace
-
-int launch_keogh(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n, int p,
-                 bool rooted, float *out, int64_t ldo, cudaStream_t st) {
+template <bool PAA>
+int launch_tile(const float *U, const float *L, const float *db, const float *db2, int64_t Q, int64_t N, int n,
+                int p, bool rooted, float *out, int64_t ldo, cudaStream_t st) {
     if (Q == 0 || N == 0) return DTWLB_OK;
     const bool vec = (n % 4 == 0) && ((reinterpret_cast<uintptr_t>(U) | reinterpret_cast<uintptr_t>(L) |
-                                       reinterpret_cast<uintptr_t>(db)) % 16 == 0);
-#define DTWLB_K(P_, V_, R_) return launch_keogh_t<P_, V_, R_>(U, L, db, Q, N, n, out, ldo, st)
+                                       reinterpret_cast<uintptr_t>(db) | reinterpret_cast<uintptr_t>(db2)) %
+                                      16 == 0);
+#define DTWLB_K(P_, V_, R_) return launch_tile_t<P_, V_, R_, PAA>(U, L, db, db2, Q, N, n, out, ldo, st)
     if (p == 1) {
         if (vec) { if (rooted) DTWLB_K(1, true, true); else DTWLB_K(1, true, false); }
         else { if (rooted) DTWLB_K(1, false, true); else DTWLB_K(1, false, false); }
@@ -234,6 +222,69 @@ int launch_keogh(const float *U, const float *L, const float *db, int64_t Q, int
         else { if (rooted) DTWLB_K(2, false, true); else DTWLB_K(2, false, false); }
     }
 #undef DTWLB_K
+}
+
+// ---------------------------------------------------------------- piecewise sums
+// One thread per (row, segment): directed fp64 sums of the s samples, then a directed
+// conversion to fp32 (the interval [lo, hi] contains the exact sum).
+__global__ void paa_sums_kernel(const float *__restrict__ x, int64_t count, int n, float *__restrict__ lo,
+                                float *__restrict__ hi, float pad_lo, float pad_hi, bool lo_only_down) {
+    const int D = paa_dims(n), Dp = paa_pitch(n);
+    const int64_t total = count * Dp;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = t / Dp;
+        const int j = (int)(t - r * Dp);
+        if (j >= D) {
+            if (lo) lo[t] = pad_lo;
+            if (hi) hi[t] = pad_hi;
+            continue;
+        }
+        const float *xr = x + r * n;
+        const int i1 = min(n, (j + 1) * kSeg);
+        double sd = 0.0, su = 0.0;
+        for (int i = j * kSeg; i < i1; ++i) {
+            const double v = (double)__ldg(xr + i);
+            sd = __dadd_rd(sd, v);
+            su = __dadd_ru(su, v);
+        }
+        if (lo) lo[t] = __double2float_rd(sd);
+        if (hi) hi[t] = __double2float_ru(su);
+    }
+    (void)lo_only_down;
+}
+
+}  // namespace
+
+int launch_paa_sums(const float *x, int64_t count, int n, float *lo, float *hi, cudaStream_t st) {
+    if (count == 0) return DTWLB_OK;
+    const int64_t total = count * paa_pitch(n);
+    const int grid = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
+    paa_sums_kernel<<<grid, 256, 0, st>>>(x, count, n, lo, hi, 0.f, 0.f, false);
+    DTWLB_LAUNCH_CHECK();
+    return DTWLB_OK;
+}
+
+int launch_paa_env_sums(const float *U, const float *L, int64_t count, int n, float *Uhi, float *Llo,
+                        cudaStream_t st) {
+    if (count == 0) return DTWLB_OK;
+    const int64_t total = count * paa_pitch(n);
+    const int grid = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
+    paa_sums_kernel<<<grid, 256, 0, st>>>(U, count, n, nullptr, Uhi, 0.f, kInf, false);
+    DTWLB_LAUNCH_CHECK();
+    paa_sums_kernel<<<grid, 256, 0, st>>>(L, count, n, Llo, nullptr, -kInf, 0.f, false);
+    DTWLB_LAUNCH_CHECK();
+    return DTWLB_OK;
+}
+
+int launch_paa_bound(const float *Uhi, const float *Llo, const float *Xlo, const float *Xhi, int64_t Q,
+                     int64_t N, int n, int p, bool rooted, float *out, int64_t ldo, cudaStream_t st) {
+    return launch_tile<true>(Uhi, Llo, Xlo, Xhi, Q, N, paa_pitch(n), p, rooted, out, ldo, st);
+}
+
+int launch_keogh(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n, int p,
+                 bool rooted, float *out, int64_t ldo, cudaStream_t st) {
+    return launch_tile<false>(U, L, db, db, Q, N, n, p, rooted, out, ldo, st);
 }
 
 }  // namespace dtwlb

@@ -15,17 +15,41 @@ int launch_envelope(const float *x, int n, int w, float *U, float *L, int64_t co
 int launch_keogh(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n, int p,
                  bool rooted, float *out, int64_t ldo, cudaStream_t st);
 
-// Padded per-query arrays used by the LB_Improved survivor kernel:
-//   yq, LUq, ULq: [Q][npadE] (npadE = 32 * epl), zero padded.
-// Candidate envelopes of the database: Ux, Lx: [N][n].
+// Piecewise-sum pre-filter (section "Using a multidimensional indexing
+// structure"): segment sums over C_j = [j*s, min((j+1)*s, n)), s = kSeg, D = ceil(n/s)
+// segments padded to Dp = round_up(D, 4) columns.  Outward-rounded (fp64 directed
+// sums, then directed conversion), so the fp32 bound is provably <= the exact one.
+constexpr int kSeg = 8;
+__host__ __device__ inline int paa_dims(int n) { return (n + kSeg - 1) / kSeg; }
+__host__ __device__ inline int paa_pitch(int n) { return (paa_dims(n) + 3) / 4 * 4; }
+// rows [count][n] -> lo/hi sums [count][Dp] (pad columns 0) (database side)
+int launch_paa_sums(const float *x, int64_t count, int n, float *lo, float *hi, cudaStream_t st);
+// query envelope U, L [count][n] -> Uhi (sums rounded up, pad +inf), Llo (rounded down, pad -inf)
+int launch_paa_env_sums(const float *U, const float *L, int64_t count, int n, float *Uhi, float *Llo,
+                        cudaStream_t st);
+// beta0[q][c] = sum_j d(X_c,j, [Llo_q,j, Uhi_q,j])^p * (p == 2 ? 1/s : 1), directed rounding
+// (a lower bound of LB_Keogh^p, hence of DTW_p^p); rooted if `rooted`.
+int launch_paa_bound(const float *Uhi, const float *Llo, const float *Xlo, const float *Xhi, int64_t Q,
+                     int64_t N, int n, int p, bool rooted, float *out, int64_t ldo, cudaStream_t st);
+
+// Arguments of the survivor passes (improved.cu).  Padded per-query arrays:
+//   yq, LUq, ULq: [Q][npadE] (npadE = 32 * epl), zero padded;
+//   Uq, Lq: [Q][npadE] query envelope padded with +inf / -inf (phase 1 only).
+// Candidate side: Ux, Lx: [N][n] envelopes of the database rows; xdb: the rows.
 struct ImprovedArgs {
     const float *yq, *LUq, *ULq;  // [Qb][npadE]
+    const float *Uq, *Lq;         // [Qb][npadE] (xdb != NULL)
     const float *Ux, *Lx;         // [N][n]
-    const float *beta1;           // [Qb][ldb] LB_Keogh^p
+    const float *xdb;             // [N][n]: if set, beta1 (LB_Keogh^p) is computed in-kernel
+                                  // from x (pre-filtered cascade); else read from `gate`
+    const float *gate;            // [Qb][ldb] dense gate bound (beta0 = piecewise-sum bound,
+                                  // or beta1 = LB_Keogh^p when xdb == NULL)
+    float *gate_w;                // = gate (LIST mode with xdb): slots of the pairs whose beta1
+                                  // passed are overwritten with -beta1 (for the DTW walk)
     int64_t ldb;
     int64_t Qb, N;
     int n, npadE;
-    const float *lo, *hi;          // per query: survivors satisfy lo < beta1 <= min(hi, thr)
+    const float *lo, *hi;          // per query: gate survivors satisfy lo < gate <= min(hi, thr)
     const float *thr;              // per query: tau^p (1+eps)  (may be NULL = +inf)
     // LIST mode outputs
     unsigned long long *list;      // [Qb][cap] keys (beta_lb bits << 32 | c)
@@ -34,7 +58,8 @@ struct ImprovedArgs {
     // DENSE mode output
     float *dense;                  // [Qb][ldd], rooted
     int64_t ldd;
-    unsigned long long *n_eval;    // stats: survivors evaluated (may be NULL)
+    unsigned long long *n_eval;        // stats: LB_Improved (phase-2) evaluations (may be NULL)
+    unsigned long long *n_eval_keogh;  // stats: in-kernel LB_Keogh evaluations (may be NULL)
     // scratch: per 64-candidate tile, the list of (query, survivor mask) entries
     unsigned long long *tile_m;    // [ceil(N/64)][Qb]
     int *tile_q;                   // [ceil(N/64)][Qb]
@@ -70,6 +95,11 @@ struct DtwArgs {
     unsigned long long *abandoned;  // stats (may be NULL)
     unsigned long long *started;    // stats: pairs whose DTW started (may be NULL)
     unsigned *queue;                 // work-queue counter (scratch, 4 bytes) for the w <= 32 kernel
+    // WALK, cascading abandon (may be NULL = off): |b1[q*ldb + c]| = LB_Keogh^p of the pair,
+    // Uq/Lq [Qb][n] the query envelopes; abandon once rowmin + (terms of rows left) > thr
+    const float *b1;
+    int64_t ldb;
+    const float *Uq, *Lq;
 };
 constexpr int kYPadL = 64;
 constexpr int kDtwIpw = 64;  // items per warp chunk of the DTW walk  // left padding of query rows (>= largest register band)

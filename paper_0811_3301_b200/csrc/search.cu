@@ -73,7 +73,7 @@ std::mutex &ws_mutex() {
 
 enum Slot {
     S_QSTAGE, S_DBSTAGE, S_ENV, S_QPAD, S_YSH, S_DBENV, S_BETA1, S_LIST, S_RES, S_STATE, S_TOPK,
-    S_OUTSTAGE, S_SCRATCH, S_TMP, S_MASK, S_COUNT
+    S_OUTSTAGE, S_SCRATCH, S_TMP, S_MASK, S_PAA, S_QPAA, S_COUNT
 };
 
 template <typename T>
@@ -87,13 +87,13 @@ int wsget(int slot, size_t count, T **out) {
 // ------------------------------------------------------------------ kernels
 // Padded copies of the query-side LB_Improved arrays: [Q][npadE], zero padded.
 __global__ void pad_rows_kernel(const float *__restrict__ src, int64_t rows, int n, float *__restrict__ dst,
-                                int npad) {
+                                int npad, float padv) {
     const int64_t total = rows * (int64_t)npad;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
         int64_t r = t / npad;
         int i = (int)(t - r * npad);
-        dst[t] = i < n ? src[r * n + i] : 0.f;
+        dst[t] = i < n ? src[r * n + i] : padv;
     }
 }
 
@@ -421,6 +421,10 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     const float eps = opts ? opts->eps : 1e-3f;
     const int64_t index_base = opts ? opts->index_base : 0;
     const bool keogh_only = opts && (opts->flags & DTWLB_KEOGH_ONLY);
+    // piecewise-sum pre-filter as the dense gate pass, LB_Keogh on its survivors
+    const bool prefilter = !(opts && (opts->flags & DTWLB_NO_PREFILTER));
+    // DTW early abandon on rowmin + LB_Keogh terms of the remaining rows (reading c19)
+    const bool cascade = !(opts && (opts->flags & DTWLB_NO_CASCADE));
     w = std::min(w, n - 1);
     Timer tm(stats != nullptr, st);
     tm.mark();  // 0
@@ -461,16 +465,25 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     DTWLB_TRY(launch_envelope(queries, n, w, U, L, Q, st));
     DTWLB_TRY(launch_envelope(L, n, w, LU, scr, Q, st));   // LU = U(L(y))
     DTWLB_TRY(launch_envelope(U, n, w, scr, UL, Q, st));   // UL = L(U(y))
-    float *qpad;  // y, LU, UL padded: [3][Q][npadE]
-    DTWLB_TRY(wsget(S_QPAD, (size_t)3 * Q * npadE, &qpad));
+    float *qpad;  // y, LU, UL (zero padded), U (+inf padded), L (-inf padded): [5][Q][npadE]
+    DTWLB_TRY(wsget(S_QPAD, (size_t)5 * Q * npadE, &qpad));
     {
         const int grid = (int)std::min<int64_t>(ceil_div(Q * npadE, 256), 148 * 8);
-        pad_rows_kernel<<<grid, 256, 0, st>>>(queries, Q, n, qpad, npadE);
-        DTWLB_LAUNCH_CHECK();
-        pad_rows_kernel<<<grid, 256, 0, st>>>(LU, Q, n, qpad + (size_t)Q * npadE, npadE);
-        DTWLB_LAUNCH_CHECK();
-        pad_rows_kernel<<<grid, 256, 0, st>>>(UL, Q, n, qpad + 2 * (size_t)Q * npadE, npadE);
-        DTWLB_LAUNCH_CHECK();
+        const float *src[5] = {queries, LU, UL, U, L};
+        const float padv[5] = {0.f, 0.f, 0.f, kInf, -kInf};
+        for (int a = 0; a < (prefilter ? 5 : 3); ++a) {
+            pad_rows_kernel<<<grid, 256, 0, st>>>(src[a], Q, n, qpad + (size_t)a * Q * npadE, npadE, padv[a]);
+            DTWLB_LAUNCH_CHECK();
+        }
+    }
+    // piecewise sums: database [2][N][Dp] (lo, hi), query envelope [2][Q][Dp] (Uhi, Llo)
+    const int Dp = paa_pitch(n);
+    float *xpaa = nullptr, *qpaa = nullptr;
+    if (prefilter) {
+        DTWLB_TRY(wsget(S_PAA, (size_t)2 * N * Dp, &xpaa));
+        DTWLB_TRY(wsget(S_QPAA, (size_t)2 * Q * Dp, &qpaa));
+        DTWLB_TRY(launch_paa_sums(db, N, n, xpaa, xpaa + (size_t)N * Dp, st));
+        DTWLB_TRY(launch_paa_env_sums(U, L, Q, n, qpaa, qpaa + (size_t)Q * Dp, st));
     }
     const bool generic_dtw = w > 64;
     const int LP = dtw_padded_len(n);
@@ -544,9 +557,14 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
 
     for (int64_t qb0 = 0; qb0 < Q; qb0 += Qb) {
         const int64_t qn = std::min<int64_t>(Qb, Q - qb0);
-        // ---- a2: LB_Keogh for the block ----
+        // ---- dense gate pass for the block: the piecewise-sum bound beta0 (pre-filter,
+        //      LB_Keogh then runs on its survivors inside the survivor pass), or a2 itself ----
         if (stats) cudaEventRecord(ev[0], st);
-        DTWLB_TRY(launch_keogh(U + qb0 * n, L + qb0 * n, db, qn, N, n, p, false, beta1, ldb, st));
+        if (prefilter)
+            DTWLB_TRY(launch_paa_bound(qpaa + qb0 * Dp, qpaa + (size_t)Q * Dp + qb0 * Dp, xpaa,
+                                       xpaa + (size_t)N * Dp, qn, N, n, p, false, beta1, ldb, st));
+        else
+            DTWLB_TRY(launch_keogh(U + qb0 * n, L + qb0 * n, db, qn, N, n, p, false, beta1, ldb, st));
         if (stats) cudaEventRecord(ev[1], st);
         init_state_kernel<<<(unsigned)ceil_div(qn, 256), 256, 0, st>>>(s, (int)qn, k);
         DTWLB_LAUNCH_CHECK();
@@ -572,9 +590,16 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 ia.yq = qpad + qb0 * npadE;
                 ia.LUq = qpad + (size_t)Q * npadE + qb0 * npadE;
                 ia.ULq = qpad + 2 * (size_t)Q * npadE + qb0 * npadE;
+                if (prefilter) {
+                    ia.Uq = qpad + 3 * (size_t)Q * npadE + qb0 * npadE;
+                    ia.Lq = qpad + 4 * (size_t)Q * npadE + qb0 * npadE;
+                    ia.xdb = db;
+                    ia.gate_w = beta1;
+                    ia.n_eval_keogh = s.stat + 4;
+                }
                 ia.Ux = dbenv;
                 ia.Lx = dbenv + (size_t)N * n;
-                ia.beta1 = beta1;
+                ia.gate = beta1;
                 ia.ldb = ldb;
                 ia.Qb = qn;
                 ia.N = N;
@@ -643,6 +668,12 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 da.abandoned = s.stat + 3;
                 da.started = s.stat + 1;
                 da.queue = reinterpret_cast<unsigned *>(s.counters + 4);
+                if (cascade) {  // cascading abandon with the pair's LB_Keogh row terms
+                    da.b1 = beta1;
+                    da.ldb = ldb;
+                    da.Uq = U + qb0 * n;
+                    da.Lq = L + qb0 * n;
+                }
                 if (generic_dtw) DTWLB_TRY(launch_dtw_generic(da, queries + qb0 * n, scratch, p, true, st));
                 else {
                     da.ysh = ysh + qb0 * LP;
@@ -685,7 +716,9 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         unsigned long long h[8];
         DTWLB_CUDA(cudaMemcpy(h, s.stat, sizeof(h), cudaMemcpyDeviceToHost));
         stats->pairs = Q * N;
-        stats->keogh_evaluated = Q * N;
+        stats->keogh_evaluated = prefilter ? (int64_t)h[4] : Q * N;
+        stats->prefilter_evaluated = prefilter ? Q * N : 0;
+        stats->prefilter_segment = prefilter ? kSeg : 0;
         stats->improved_evaluated = (int64_t)h[0];
         stats->dtw_cells_computed = (int64_t)h[2];
         stats->dtw_abandoned = (int64_t)h[3];

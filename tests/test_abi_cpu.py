@@ -25,7 +25,7 @@ def lib():
 
 def test_header_declares_the_boundary():
     fns = _header_functions()
-    for f in ["lb_envelope", "lb_keogh", "lb_improved", "dtw_band", "nn_search", "nn_merge",
+    for f in ["lb_envelope", "lb_keogh", "lb_piecewise", "lb_improved", "dtw_band", "nn_search", "nn_merge",
               "dtwlb_last_error", "dtwlb_release_workspace"]:
         assert f in fns, fns
 
@@ -43,6 +43,8 @@ def test_argument_validation_precedes_device(lib):
     assert b"n = 0" in lib.dtwlb_last_error()
     assert lib.lb_envelope(null, 8, -1, null, null, 1, null) == 1         # w < 0
     assert lib.lb_keogh(null, null, 1, 1, 8, 3, null, null) == 2          # p = 3 unsupported
+    assert lib.lb_piecewise(null, null, 1, 1, 8, 3, null, null) == 2      # p = 3 unsupported
+    assert lib.lb_piecewise(null, null, 1, 1, 0, 1, null, null) == 1      # n < 1
     assert lib.dtw_band(null, null, 8, 2, 0, null, 1, null) == 2          # p = 0 (inf) unsupported on GPU
     assert lib.nn_search(null, 1, null, 0, 8, 1, 1, 1, null, null, None, None, null) == 1   # N = 0
     assert lib.nn_search(null, 1, null, 4, 8, 1, 1, 5, null, null, None, None, null) == 1   # k > N

@@ -92,6 +92,37 @@ def test_lb_keogh_and_improved(cuda_ok, n, w, p):
     assert np.all(ib >= kb * (1 - 1e-6))
 
 
+@pytest.mark.parametrize("n,w", BOUND_CASES + [(1, 0), (9, 2), (1001, 50)])
+@pytest.mark.parametrize("p", [1, 2])
+def test_lb_piecewise(cuda_ok, n, w, p):
+    """Pre-filter bound (s = 8): outward rounding keeps the GPU value at or
+    below the exact (fp64) bound, within relative 1e-5 of it; never above LB_Keogh."""
+    from paper_0811_3301_b200 import lb_keogh, lb_piecewise
+    Q, N = 67, 300
+    if n >= 512:
+        Q, N = 9, 140
+    kind = "raw" if n == 128 else "rw"
+    qs, db = series(Q, n, kind), series(N, n, kind)
+    db[5] = qs[3]
+    q_env = _env_dev(qs, w)
+    pw = lb_piecewise(q_env, dev(db), p).cpu().numpy().astype(np.float64)
+    kb = lb_keogh(q_env, dev(db), p).cpu().numpy().astype(np.float64)
+    op = np.array([[oracle.lb_piecewise(db[c], qs[q], w, p, 8) for c in range(N)] for q in range(Q)])
+    assert np.all(pw <= op * (1 + 1e-7) + 1e-30), "outward rounding violated"
+    close(pw, op, 1e-5, 1e-5)
+    assert np.all(pw <= kb * (1 + 1e-5) + 1e-6)
+    assert pw[3, 5] == 0.0
+
+
+def test_lb_piecewise_golden(cuda_ok):
+    from paper_0811_3301_b200 import lb_piecewise
+    x = np.array([[2, 3, 0, 0, 5, 0, 0, 0, 0]], np.float32)
+    y = np.array([[3, 2, 3, 4, 1, 1, 1, 1, 1]], np.float32)
+    for p in (1, 2):
+        got = lb_piecewise(_env_dev(y, 1), dev(x), p).item() ** p
+        assert got == pytest.approx(oracle.lb_piecewise(x[0], y[0], 1, p, 8) ** p, rel=1e-6)
+
+
 @pytest.mark.parametrize("n,w", [(1, 0), (2, 1), (3, 2), (4, 1), (7, 3), (128, 12), (256, 25), (257, 25),
                                  (256, 8), (256, 17), (200, 40), (512, 51), (1000, 50), (300, 64), (128, 100),
                                  (64, 200), (33, 0)])

@@ -55,22 +55,24 @@ def test_C2_full(cuda_ok, name):
     check(qs, db, c.w, c.p, c.k, brute=False)
 
 
+@pytest.mark.parametrize("prefilter", [True, False])
 @pytest.mark.parametrize("name,Q,N", [("C3", 6, 20_000), ("C4", 8, 30_000), ("C5", 8, 60_000)])
-def test_reduced_large_configs(cuda_ok, name, Q, N):
+def test_reduced_large_configs(cuda_ok, name, Q, N, prefilter):
     c = datagen.CONFIGS[name]
     qs, db = datagen.make(c, Q=Q, N=N)
-    check(qs, db, c.w, c.p, c.k, brute=False)
+    check(qs, db, c.w, c.p, c.k, brute=False, prefilter=prefilter)
 
 
+@pytest.mark.parametrize("prefilter", [True, False])
 @pytest.mark.parametrize("p", [1, 2])
 @pytest.mark.parametrize("k", [1, 3, 10])
-def test_duplicates_self_queries_ties(cuda_ok, p, k):
+def test_duplicates_self_queries_ties(cuda_ok, p, k, prefilter):
     qs, db = datagen.make("C2p1", Q=20, N=3000)
     db[100] = qs[0]          # exact self-match -> distance 0
     db[2000] = qs[0]         # duplicate of the self-match: smaller index first
     db[7] = db[8]            # duplicate rows
     db[1500] = qs[5] + 1e-3  # near tie
-    g_idx, g_dist = check(qs, db, 25, p, k)
+    g_idx, g_dist = check(qs, db, 25, p, k, prefilter=prefilter)
     assert g_idx[0, 0] == 100 and g_dist[0, 0] == 0.0
     if k > 1:
         assert g_idx[0, 1] == 2000 and g_dist[0, 1] == 0.0
@@ -87,6 +89,7 @@ def test_odd_shapes_and_bands(cuda_ok, n, w):
         db = datagen.random_walks(700, n, seed=4)
     for p in (1, 2):
         check(qs, db, w, p, 2)
+        check(qs, db, w, p, 2, prefilter=False)
 
 
 def test_all_tied_database_returns_smallest_indices(cuda_ok):
@@ -94,8 +97,9 @@ def test_all_tied_database_returns_smallest_indices(cuda_ok):
     qs = np.zeros((4, 16), np.float32)
     db = np.zeros((500, 16), np.float32)
     for p in (1, 2):
-        idx, dist = run(qs, db, 3, p, 7)
-        assert np.all(idx == np.arange(7)) and np.all(dist == 0)
+        for pf in (True, False):
+            idx, dist = run(qs, db, 3, p, 7, prefilter=pf)
+            assert np.all(idx == np.arange(7)) and np.all(dist == 0)
 
 
 def test_k_equals_N_and_small_N(cuda_ok):
@@ -108,6 +112,8 @@ def test_k_equals_N_and_small_N(cuda_ok):
 def test_keogh_only_index_base_eps0(cuda_ok):
     qs, db = datagen.make("C2p2", Q=16, N=5000)
     check(qs, db, 25, 2, 5, keogh_only=True)
+    check(qs, db, 25, 2, 5, keogh_only=True, prefilter=False)
+    check(qs, db, 25, 1, 3, prefilter=False, query_block=5)
     check(qs, db, 25, 2, 5, index_base=1_000_000)
     check(qs, db, 25, 2, 5, eps=0.0)
     check(qs, db, 25, 2, 5, query_block=4)   # several query blocks
