@@ -129,6 +129,8 @@ typedef struct nn_stats {
     int64_t prefilter_evaluated; /* piecewise-sum bound evaluations (pairs, or 0)      */
     int32_t prefilter_segment;   /* segment length s of the pre-filter (0 = off)       */
     int32_t reserved_;
+    double ms_survivor_kernel;   /* device time of the survivor-pass kernels (LB_Keogh /
+                                    LB_Improved on sparse pairs), part of ms_improved   */
 } nn_stats;
 
 /* Exact k-nearest-neighbour search under banded DTW_p: for each query y_q,

@@ -48,33 +48,38 @@ __device__ __forceinline__ float f4get(const float4 &v, int k) {
 
 // B holds row i-1; computes rows i (x = xa) and i+1 (x = xb); B <- row i+1.
 // ys: aligned pointer with ys[d] = y[i + d - w] (padded), d = 0..2WB+1.
+// Skewed by two cells: at step d row i computes band cell d and row i+1 band cell
+// d-2, whose up (row i, cell d-1) and diagonal (row i, cell d-2) neighbours were
+// produced one and two steps earlier -- the two cells of a step are independent
+// (two dependency chains per thread); row i+1 uses the previous step's y value.
 template <int WB, int P, bool EXACT, bool SMEM>
 __device__ __forceinline__ void two_rows(float (&B)[2 * WB + 2], float xa, float xb,
                                          const float *__restrict__ ys, int w2) {
     constexpr int NB = 2 * WB + 1;
-    float a_prev = kInf, rb_prev = kInf;
+    float a1 = kInf, a2 = kInf, bl = kInf, yp = 0.f;
     float4 yv4;
 #pragma unroll
-    for (int d = 0; d < NB; ++d) {
-        if ((d & 3) == 0) yv4 = ld4<SMEM>(ys + d);
-        const float yv = f4get(yv4, d & 3);
-        float a = cell<P>(min3f(B[d], B[d + 1], a_prev), xa - yv);
-        if (!EXACT && d > w2) a = kInf;
-        if (d >= 1) {
-            float b = cell<P>(min3f(a_prev, a, rb_prev), xb - yv);
-            if (!EXACT && d - 1 > w2) b = kInf;
-            B[d - 1] = b;
-            rb_prev = b;
+    for (int d = 0; d <= NB + 1; ++d) {
+        float yv = 0.f;
+        if (d <= NB) {
+            if ((d & 3) == 0) yv4 = ld4<SMEM>(ys + d);
+            yv = f4get(yv4, d & 3);
         }
-        a_prev = a;
-    }
-    {
-        constexpr int d = NB;  // row i+1, cell 2WB uses y[i+1+2WB-w]
-        if ((d & 3) == 0) yv4 = ld4<SMEM>(ys + d);
-        const float yv = f4get(yv4, d & 3);
-        float b = cell<P>(fminf(a_prev, rb_prev), xb - yv);
-        if (!EXACT && d - 1 > w2) b = kInf;
-        B[NB - 1] = b;
+        float a = kInf;
+        if (d < NB) {
+            a = cell<P>(min3f(B[d], B[d + 1], a1), xa - yv);
+            if (!EXACT && d > w2) a = kInf;
+        }
+        if (d >= 2) {
+            const int e = d - 2;  // row i+1: up = row i cell e+1 (a1), diag = row i cell e (a2)
+            float b = cell<P>(min3f(a2, a1, bl), xb - yp);
+            if (!EXACT && e > w2) b = kInf;
+            B[e] = b;
+            bl = b;
+        }
+        a2 = a1;
+        a1 = a;
+        yp = yv;
     }
 }
 
@@ -115,6 +120,19 @@ template <int P>
 __device__ __forceinline__ float row_lb(float x, float u, float l) {
     const float d = max3f(x - u, l - x, 0.f);
     return P == 1 ? d : d * d;
+}
+
+// 8 values v[i0 .. i0+7] of a row of length n (fill beyond n); vector loads when aligned
+__device__ __forceinline__ void load8(float (&v)[8], const float *__restrict__ r, int i0, int n, float fill) {
+    if (((n & 3) == 0) && i0 + 8 <= n) {
+        const float4 a = __ldg(reinterpret_cast<const float4 *>(r + i0));
+        const float4 b = __ldg(reinterpret_cast<const float4 *>(r + i0 + 4));
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+        v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) v[t] = i0 + t < n ? __ldg(r + i0 + t) : fill;
+    }
 }
 
 template <int WB>
@@ -316,69 +334,115 @@ template <int WB, int P, bool EXACT>
 __device__ __forceinline__ void four_rows(float (&B)[2 * WB + 2], const float (&Y)[(2 * WB + 4 + 3) / 4 * 4],
                                           const float (&x)[4], int w2) {
     constexpr int NB = 2 * WB + 1;
-    float p0 = kInf, p1 = kInf, p2 = kInf, p3 = kInf;   // left neighbours (same row)
-    float a0 = kInf, a1 = kInf, a2 = kInf;              // row r cell (d-r-1): diag of row r+1
+    // skew 2: at step d, row r computes band cell e = d - 2r.  Its up (row r-1, cell e+1)
+    // and diagonal (row r-1, cell e) neighbours came out of row r-1 one and two steps
+    // earlier (h1, h2), its left neighbour is its own previous cell (pl); y index e + r.
+    float pl0 = kInf, pl1 = kInf, pl2 = kInf, pl3 = kInf;
+    float h1_0 = kInf, h2_0 = kInf, h1_1 = kInf, h2_1 = kInf, h1_2 = kInf, h2_2 = kInf;
 #pragma unroll
-    for (int d = 0; d < NB + 3; ++d) {
-        const float yv = Y[d];
+    for (int d = 0; d < NB + 6; ++d) {
         float c0 = kInf, c1 = kInf, c2 = kInf;
         if (d < NB) {  // row 0, cell d: up = B[d+1], diag = B[d]
-            c0 = cell<P>(min3f(B[d], B[d + 1], p0), x[0] - yv);
+            c0 = cell<P>(min3f(B[d], B[d + 1], pl0), x[0] - Y[d]);
             if (!EXACT && d > w2) c0 = kInf;
-            p0 = c0;
+            pl0 = c0;
         }
-        if (d >= 1 && d - 1 < NB) {  // row 1, cell d-1: up = row0 cell d, diag = row0 cell d-1
-            const float up = d < NB ? c0 : kInf;
-            c1 = cell<P>(min3f(a0, up, p1), x[1] - yv);
-            if (!EXACT && d - 1 > w2) c1 = kInf;
-            p1 = c1;
+        if (d >= 2 && d - 2 < NB) {  // row 1, cell d-2
+            c1 = cell<P>(min3f(h2_0, h1_0, pl1), x[1] - Y[d - 1]);
+            if (!EXACT && d - 2 > w2) c1 = kInf;
+            pl1 = c1;
         }
-        if (d >= 2 && d - 2 < NB) {  // row 2, cell d-2
-            const float up = (d - 1 < NB) ? c1 : kInf;
-            c2 = cell<P>(min3f(a1, up, p2), x[2] - yv);
-            if (!EXACT && d - 2 > w2) c2 = kInf;
-            p2 = c2;
+        if (d >= 4 && d - 4 < NB) {  // row 2, cell d-4
+            c2 = cell<P>(min3f(h2_1, h1_1, pl2), x[2] - Y[d - 2]);
+            if (!EXACT && d - 4 > w2) c2 = kInf;
+            pl2 = c2;
         }
-        if (d >= 3) {  // row 3, cell d-3 (stored: B becomes row i+3)
-            const float up = (d - 2 < NB) ? c2 : kInf;
-            float c3 = cell<P>(min3f(a2, up, p3), x[3] - yv);
-            if (!EXACT && d - 3 > w2) c3 = kInf;
-            p3 = c3;
-            B[d - 3] = c3;
+        if (d >= 6) {  // row 3, cell d-6 (stored: B becomes row i+3)
+            float c3 = cell<P>(min3f(h2_2, h1_2, pl3), x[3] - Y[d - 3]);
+            if (!EXACT && d - 6 > w2) c3 = kInf;
+            pl3 = c3;
+            B[d - 6] = c3;
         }
-        a0 = c0;
-        a1 = c1;
-        a2 = c2;
+        h2_0 = h1_0; h1_0 = c0;
+        h2_1 = h1_1; h1_1 = c1;
+        h2_2 = h1_2; h1_2 = c2;
     }
 }
 
+// Per-lane staging slot of the pipelined refill: the y window (NY floats) and x[0..7]
+// of the lane's next pair, written by cp.async while the lane still waits one step;
+// +4 floats of padding rotate the banks between lanes.
+template <int WB>
+struct Dtw4Cfg {
+    static constexpr int NY = (2 * WB + 4 + 3) / 4 * 4;
+    static constexpr int SL = NY + 12;
+    static constexpr size_t smem = (size_t)NT * SL * sizeof(float) +
+                                   (size_t)(NT / 32) * kChunk4 * (sizeof(unsigned long long) + sizeof(int));
+};
+
+// Lane states of dtw4_kernel
+constexpr int kFree = 0, kPending = 1, kActive = 2;
+
 template <int WB, int P, bool EXACT, bool WALK>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, (WB <= 25 ? 3 : 2))
 dtw4_kernel(DtwArgs a) {
     constexpr int NB = 2 * WB + 1;
-    constexpr int NY = (2 * WB + 4 + 3) / 4 * 4;  // window length, a multiple of 4 (aligned refills)
-    const int lane = threadIdx.x & 31;
+    constexpr int NY = Dtw4Cfg<WB>::NY;  // window length, a multiple of 4 (aligned refills)
+    constexpr int SL = Dtw4Cfg<WB>::SL;
+    extern __shared__ __align__(16) float dsm[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    float *slot = dsm + (size_t)threadIdx.x * SL;  // this lane's staging slot
+    unsigned long long *ckey = reinterpret_cast<unsigned long long *>(dsm + (size_t)NT * SL) + wid * kChunk4;
+    int *cq = reinterpret_cast<int *>(reinterpret_cast<unsigned long long *>(dsm + (size_t)NT * SL) +
+                                      (NT / 32) * kChunk4) + wid * kChunk4;
     const int n = a.n, w = EXACT ? WB : a.w, w2 = 2 * w;
     const int sh = (kYPadL - w) & 3;  // alignment class of (i - w) for i % 4 == 0
     const int64_t total = a.total;
     const int64_t nchunks = (total + kChunk4 - 1) / kChunk4;
+    const unsigned lt = (1u << lane) - 1u;
 
     int64_t cbeg = 0, cend = 0, cursor = 0;
-    bool has = false;
+    int st = kFree;
     int64_t item = 0;
-    int q = 0;  // WALK: query of the lane's last item (items are in query order)
     const float *xr = nullptr, *yr = nullptr;
-    float thr = kInf;
+    float thr = kInf, thr_n = kInf, beta_n = 0.f;
     int i = 0;
     float B[NB + 1], Y[NY];
+    float xv[8];  // x of rows i .. i+7 (loaded one 8-row step ahead)
     // cascading abandon: rest = LB_Keogh^p terms of the rows not yet computed
     const bool casc = WALK && a.b1 != nullptr;
-    float rest = 0.f;
+    float rest = 0.f, rest_n = 0.f;
     const float *ur = nullptr, *lr = nullptr;
     unsigned long long rows_done = 0, n_abandon = 0, n_started = 0;
 
     while (true) {
-        unsigned need = __ballot_sync(0xffffffffu, !has);
+        // ---- (a) activate the lanes whose refill copies were issued one step ago ----
+        if (__any_sync(0xffffffffu, st == kPending)) {
+            cp_wait<0>();
+            if (st == kPending) {
+                if (beta_n > thr_n) {
+                    a.res[item] = kInf;  // pruned by its bound under the current threshold
+                    st = kFree;
+                } else {
+#pragma unroll
+                    for (int d = 0; d < NY; d += 4) {
+                        const float4 v = *reinterpret_cast<const float4 *>(slot + d);
+                        Y[d] = v.x; Y[d + 1] = v.y; Y[d + 2] = v.z; Y[d + 3] = v.w;
+                    }
+                    const float4 x0 = *reinterpret_cast<const float4 *>(slot + NY);
+                    const float4 x1 = *reinterpret_cast<const float4 *>(slot + NY + 4);
+                    xv[0] = x0.x; xv[1] = x0.y; xv[2] = x0.z; xv[3] = x0.w;
+                    xv[4] = x1.x; xv[5] = x1.y; xv[6] = x1.z; xv[7] = x1.w;
+                    thr = thr_n;
+                    rest = rest_n;
+                    st = kActive;
+                    ++n_started;
+                }
+            }
+        }
+        // ---- (b) refill free lanes: claim the next items of the warp's chunk and issue
+        //      their copies (y window, x[0..7]) into the lane's slot; active next step ----
+        const unsigned need = __ballot_sync(0xffffffffu, st == kFree);
         if (need && cursor >= cend) {  // the warp's chunk is exhausted: grab the next one
             int64_t c = 0;
             if (lane == 0) c = atomicAdd(a.queue, 1u);
@@ -388,67 +452,75 @@ dtw4_kernel(DtwArgs a) {
                 cend = cbeg + kChunk4 < total ? cbeg + kChunk4 : total;
                 cursor = cbeg;
                 if constexpr (WALK) {
+                    // stage the chunk's keys and queries: items are in query order, each
+                    // lane walks its 8 items (cbeg + lane + 32 t) forward from the chunk's first query
                     int lo = 0, hi = a.Qb;  // item_off[lo] <= cbeg < item_off[hi]
                     while (hi - lo > 1) {
                         const int mid = (lo + hi) >> 1;
                         if (a.item_off[mid] <= cbeg) lo = mid; else hi = mid;
                     }
-                    q = lo;  // only read when a lane starts its next item (from this chunk on)
+                    int q = lo;
+                    for (int t = 0; t < kChunk4 / 32; ++t) {
+                        const int64_t it = cbeg + lane + 32 * t;
+                        if (it < cend) {
+                            while (it >= a.item_off[q + 1]) ++q;
+                            const int64_t j = a.pos[q] + (it - a.item_off[q]);
+                            DCHECK(j >= 0 && j < a.cap, "dtw4 item %lld q=%d j=%lld", (long long)it, q, (long long)j);
+                            ckey[lane + 32 * t] = a.list[(int64_t)q * a.cap + j];
+                            cq[lane + 32 * t] = q;
+                        }
+                    }
                 }
+                __syncwarp();
             }
         }
         if (need && cursor < cend) {
-            const int64_t mine = cursor + __popc(need & ((1u << lane) - 1));
+            const int64_t mine = cursor + __popc(need & lt);
             cursor += __popc(need);
-            if (!has && mine < cend) {
+            if (st == kFree && mine < cend) {
                 item = mine;
-                float beta = 0.f;
+                int64_t c, qy;
                 if constexpr (WALK) {
-                    while (item >= a.item_off[q + 1]) ++q;
-                    const int64_t j = a.pos[q] + (item - a.item_off[q]);
-                    DCHECK(j >= 0 && j < a.cap, "dtw4 item %lld q=%d j=%lld", (long long)item, q, (long long)j);
-                    const unsigned long long key = a.list[(int64_t)q * a.cap + j];
-                    const uint32_t c = (uint32_t)(key & 0xffffffffu);
-                    DCHECK((int64_t)c < a.Ndb, "dtw4 key c=%u q=%d", c, q);
-                    beta = __uint_as_float((uint32_t)(key >> 32));
-                    thr = a.thr[q];
-                    xr = a.db + (int64_t)c * n;
+                    const unsigned long long key = ckey[item - cbeg];
+                    qy = cq[item - cbeg];
+                    c = (int64_t)(key & 0xffffffffu);
+                    DCHECK(c < a.Ndb, "dtw4 key c=%lld q=%lld", (long long)c, (long long)qy);
+                    beta_n = __uint_as_float((uint32_t)(key >> 32));
+                    thr_n = a.thr[qy];
                     if (casc) {
-                        rest = fabsf(__ldg(a.b1 + (int64_t)q * a.ldb + c));  // beta1 = sum of all row terms
-                        ur = a.Uq + (int64_t)q * n;
-                        lr = a.Lq + (int64_t)q * n;
+                        rest_n = fabsf(__ldg(a.b1 + qy * a.ldb + c));  // beta1 = sum of all row terms
+                        ur = a.Uq + qy * n;
+                        lr = a.Lq + qy * n;
                     }
-                    yr = a.ysh + (int64_t)sh * a.ysh_stride_s + (int64_t)q * a.LP;
                 } else {
-                    thr = kInf;
-                    xr = a.db + item * n;
-                    yr = a.ysh + (int64_t)sh * a.ysh_stride_s + item * a.LP;
+                    c = qy = item;
+                    beta_n = 0.f;
+                    thr_n = kInf;
                 }
-                if (beta > thr) {
-                    a.res[item] = kInf;
+                xr = a.db + c * n;
+                yr = a.ysh + (int64_t)sh * a.ysh_stride_s + qy * a.LP;
+                // Y[d] = ypad[-w + kYPadL + d]; the copy `sh` makes base (kYPadL - w - sh) aligned
+                const float *ys = yr + (kYPadL - w - sh);
+#pragma unroll
+                for (int d = 0; d < NY; d += 4) cp_async16(slot + d, ys + d, 16);
+                if (((n & 3) == 0) && n >= 8) {
+                    cp_async16(slot + NY, xr, 16);
+                    cp_async16(slot + NY + 4, xr + 4, 16);
                 } else {
-                    has = true;
-                    ++n_started;
-                    i = 0;
 #pragma unroll
-                    for (int d = 0; d <= NB; ++d) B[d] = kInf;
-#pragma unroll
-                    for (int d = 0; d < NB; ++d)
-                        if (d == w) B[d] = 0.f;
-                    // Y[d] = ypad[-w + kYPadL + d]; the copy `sh` makes base (kYPadL - w - sh) aligned
-                    const float *ys = yr + (kYPadL - w - sh);
-#pragma unroll
-                    for (int d = 0; d < NY; d += 4) {
-                        const float4 v = __ldg(reinterpret_cast<const float4 *>(ys + d));
-                        Y[d] = v.x;
-                        Y[d + 1] = v.y;
-                        Y[d + 2] = v.z;
-                        Y[d + 3] = v.w;
-                    }
+                    for (int t = 0; t < 8; ++t) cp_async4(slot + NY + t, t < n ? xr + t : xr, t < n ? 4 : 0);
                 }
+                cp_commit();
+#pragma unroll
+                for (int d = 0; d <= NB; ++d) B[d] = kInf;
+#pragma unroll
+                for (int d = 0; d < NB; ++d)
+                    if (d == w) B[d] = 0.f;  // virtual D(-1,-1) = 0 sits on the diagonal
+                i = 0;
+                st = kPending;
             }
         }
-        if (!__any_sync(0xffffffffu, has)) {
+        if (!__any_sync(0xffffffffu, st != kFree)) {
             // no lane has work: done when the queue is exhausted
             bool more = cursor < cend;
             if (!more) {
@@ -460,32 +532,36 @@ dtw4_kernel(DtwArgs a) {
             if (!more) break;
             continue;
         }
-        if (has) {
+        // ---- (c) advance the active lanes by up to 8 rows ----
+        if (st == kActive) {
             const int i0 = i;
+            // prefetch x of the next 8-row step: the loads of a candidate row miss L1 and
+            // their latency hides behind this step's cells
+            float xn[8];
+            load8(xn, xr, i0 + 8, n, 0.f);
             // up to two blocks of four rows, then the abandon test
 #pragma unroll 1
-            for (int blk = 0; blk < 2 && i + 4 <= n; ++blk) {
-                float xv[4];
-                if ((n & 3) == 0) {
-                    const float4 v = __ldg(reinterpret_cast<const float4 *>(xr + i));
-                    xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
-                } else {
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) xv[t] = __ldg(xr + i + t);
-                }
-                if (casc) {
+            for (int blk = 0; blk < 2; ++blk) {
+                if (i + 4 > n) break;
+                const float x4[4] = {xv[0], xv[1], xv[2], xv[3]};
+                if (casc) {  // query envelope rows: L1-resident (the warp's items share queries)
+                    float u4[4], l4[4];
                     if ((n & 3) == 0) {
-                        const float4 u4 = __ldg(reinterpret_cast<const float4 *>(ur + i));
-                        const float4 l4 = __ldg(reinterpret_cast<const float4 *>(lr + i));
-                        rest -= row_lb<P>(xv[0], u4.x, l4.x) + row_lb<P>(xv[1], u4.y, l4.y) +
-                                row_lb<P>(xv[2], u4.z, l4.z) + row_lb<P>(xv[3], u4.w, l4.w);
+                        const float4 uu = __ldg(reinterpret_cast<const float4 *>(ur + i));
+                        const float4 ll = __ldg(reinterpret_cast<const float4 *>(lr + i));
+                        u4[0] = uu.x; u4[1] = uu.y; u4[2] = uu.z; u4[3] = uu.w;
+                        l4[0] = ll.x; l4[1] = ll.y; l4[2] = ll.z; l4[3] = ll.w;
                     } else {
 #pragma unroll
-                        for (int t = 0; t < 4; ++t) rest -= row_lb<P>(xv[t], __ldg(ur + i + t), __ldg(lr + i + t));
+                        for (int t = 0; t < 4; ++t) { u4[t] = __ldg(ur + i + t); l4[t] = __ldg(lr + i + t); }
                     }
+                    rest -= row_lb<P>(x4[0], u4[0], l4[0]) + row_lb<P>(x4[1], u4[1], l4[1]) +
+                            row_lb<P>(x4[2], u4[2], l4[2]) + row_lb<P>(x4[3], u4[3], l4[3]);
                 }
-                four_rows<WB, P, EXACT>(B, Y, xv, w2);
+                four_rows<WB, P, EXACT>(B, Y, x4, w2);
                 i += 4;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) xv[t] = xv[t + 4];
                 // shift the y window by four and append y[i + w + 1 .. i + w + 4] (next block)
 #pragma unroll
                 for (int d = 0; d + 4 < NY; ++d) Y[d] = Y[d + 4];
@@ -494,7 +570,7 @@ dtw4_kernel(DtwArgs a) {
                     Y[NY - 4] = v.x; Y[NY - 3] = v.y; Y[NY - 2] = v.z; Y[NY - 1] = v.w;
                 }
             }
-            if (i + 4 > n && i < n) {  // tail rows (n % 4 != 0): one row at a time
+            if (i + 4 > n && i < n && i - i0 < 8) {  // tail rows (n % 4 != 0): one row at a time
                 while (i < n) {
                     if (casc) rest -= row_lb<P>(__ldg(xr + i), __ldg(ur + i), __ldg(lr + i));
                     float prev = kInf;
@@ -511,7 +587,10 @@ dtw4_kernel(DtwArgs a) {
                     Y[NY - 1] = __ldg(yr + (kYPadL - w - sh) + i + NY - 1);
                 }
             }
+#pragma unroll
+            for (int t = 0; t < 8; ++t) xv[t] = xn[t];
             rows_done += (unsigned long long)(i - i0);
+            // ---- (d) finished or abandoned lanes become free ----
             if (i >= n) {
                 float r = B[WB];
                 if constexpr (!EXACT) {
@@ -520,11 +599,11 @@ dtw4_kernel(DtwArgs a) {
                         if (d == w) r = B[d];
                 }
                 a.res[item] = WALK ? r : rootp<P>(r);
-                has = false;
+                st = kFree;
             } else if (band_min<WB>(B) + rest > thr) {
                 a.res[item] = kInf;  // early abandon (readings c15, c19)
                 ++n_abandon;
-                has = false;
+                st = kFree;
             }
         }
     }
@@ -593,7 +672,10 @@ int launch_dtw4_t(const DtwArgs &a, cudaStream_t st) {
     const int64_t chunks = ceil_div(a.total, kChunk4);
     int64_t warps = std::min<int64_t>(chunks, (int64_t)148 * 48);  // persistent-ish: <= 48 warps per SM
     const int64_t grid = ceil_div(warps * 32, NT);
-    dtw4_kernel<WB, P, EXACT, WALK><<<(unsigned)grid, NT, 0, st>>>(a);
+    constexpr size_t smem = Dtw4Cfg<WB>::smem;
+    auto k = dtw4_kernel<WB, P, EXACT, WALK>;
+    DTWLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<(unsigned)grid, NT, smem, st>>>(a);
     DTWLB_LAUNCH_CHECK();
     return DTWLB_OK;
 }

@@ -35,6 +35,8 @@
 //    (beta1 + beta2, c) of each pair with LB_Improved^p <= thr, appended to the
 //    query's list with one warp-aggregated atomic per group.  DENSE mode (the
 //    lb_improved C-ABI call) writes the rooted bound of every pair instead.
+#include <type_traits>
+
 #include "kernels.cuh"
 
 namespace dtwlb {
@@ -145,19 +147,18 @@ __device__ __forceinline__ void load_p2(QRegs<EPL / 4, B1X, KO> &r, const Improv
     }
 }
 
-// Up to four set bits of m (lowest first), removed from m; missing slots repeat
-// the first bit (evaluated redundantly, results discarded).  Returns the count.
-__device__ __forceinline__ int take4(unsigned long long &m, int (&bits)[4]) {
-    int nb = 0;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int bt = __ffsll(m) - 1;  // -1 if m == 0
-        bits[u] = bt;
-        if (bt >= 0) { m &= m - 1; ++nb; }
-    }
-#pragma unroll
-    for (int u = 1; u < 4; ++u) bits[u] = bits[u] >= 0 ? bits[u] : bits[0];
-    return nb;
+// Compact the set bits of the warp-uniform 64-bit mask m into lst[0..cnt) (ascending),
+// padded with zeros to a multiple of 4 (padding slots are evaluated redundantly on
+// local row 0 and discarded).  Returns cnt.  Caller syncs the warp before reading.
+__device__ __forceinline__ int compact_mask(unsigned long long m, int *lst, int lane) {
+    const unsigned lo = (unsigned)m, hi = (unsigned)(m >> 32);
+    const unsigned lt = (1u << lane) - 1u;
+    const int nlo = __popc(lo);
+    if ((lo >> lane) & 1u) lst[__popc(lo & lt)] = lane;
+    if ((hi >> lane) & 1u) lst[nlo + __popc(hi & lt)] = lane + 32;
+    const int cnt = nlo + __popc(hi);
+    if (lane < ((4 - (cnt & 3)) & 3)) lst[cnt + lane] = 0;
+    return cnt;
 }
 
 // Transposed butterfly: four per-lane partial sums -> lane l holds the warp
@@ -177,8 +178,92 @@ __device__ __forceinline__ float reduce4(float s0, float s1, float s2, float s3,
     return v;
 }
 
-__device__ __forceinline__ int pick4(const int (&b)[4], int u) {
-    return u == 0 ? b[0] : (u == 1 ? b[1] : (u == 2 ? b[2] : b[3]));
+__device__ __forceinline__ int pick4(const int4 &b, int u) {
+    return u == 0 ? b.x : (u == 1 ? b.y : (u == 2 ? b.z : b.w));
+}
+
+// W-wide butterfly (W in {1, 2, 4}): lane l ends with the warp total of slot l >> (5 - log2 W).
+template <int W>
+__device__ __forceinline__ float reduceW(const float (&s)[4], int lane) {
+    if constexpr (W == 4) {
+        return reduce4(s[0], s[1], s[2], s[3], lane);
+    } else if constexpr (W == 2) {
+        const bool hi16 = lane & 16;
+        float v = hi16 ? s[1] : s[0];
+        v += __shfl_xor_sync(0xffffffffu, hi16 ? s[0] : s[1], 16);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        return v;
+    } else {
+        float v = s[0];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        return v;
+    }
+}
+
+// Phase-1 partial sums of W survivors (local rows li[0..W)): lane covers samples
+// 4*lane + 128*v .. +3 of beta1 = sum_i d(x_i, [L_i, U_i])^p.
+template <int W, int P, int NV, int NPAD>
+__device__ __forceinline__ float p1_group(const float *sX, const int (&li)[4], const float4 (&uq)[NV],
+                                          const float4 (&lq)[NV], int lane) {
+    float s[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        const float4 uu = uq[v], ll = lq[v];
+#pragma unroll
+        for (int u = 0; u < W; ++u) {
+            const float4 x = *reinterpret_cast<const float4 *>(sX + li[u] * NPAD + 4 * lane + 128 * v);
+            float t = s[u];
+            t = accp<P>(t, max3f(x.x - uu.x, ll.x - x.x, 0.f));
+            t = accp<P>(t, max3f(x.y - uu.y, ll.y - x.y, 0.f));
+            t = accp<P>(t, max3f(x.z - uu.z, ll.z - x.z, 0.f));
+            t = accp<P>(t, max3f(x.w - uu.w, ll.w - x.w, 0.f));
+            s[u] = t;
+        }
+    }
+    return reduceW<W>(s, lane);
+}
+
+// Phase-2 partial sums: beta2 = sum_i max(y_i - max(U(x)_i, LU_i), min(L(x)_i, UL_i) - y_i, 0)^p.
+template <int W, int P, int NV, int NPAD>
+__device__ __forceinline__ float p2_group(const float *sU, const float *sL, const int (&li)[4],
+                                          const float4 (&yq)[NV], const float4 (&luq)[NV],
+                                          const float4 (&ulq)[NV], int lane) {
+    float s[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        const float4 y = yq[v], lu = luq[v], ul = ulq[v];
+#pragma unroll
+        for (int u = 0; u < W; ++u) {
+            const int off = li[u] * NPAD + 4 * lane + 128 * v;
+            const float4 ux = *reinterpret_cast<const float4 *>(sU + off);
+            const float4 lx = *reinterpret_cast<const float4 *>(sL + off);
+            float t = s[u];
+            t = accp<P>(t, max3f(y.x - fmaxf(ux.x, lu.x), fminf(lx.x, ul.x) - y.x, 0.f));
+            t = accp<P>(t, max3f(y.y - fmaxf(ux.y, lu.y), fminf(lx.y, ul.y) - y.y, 0.f));
+            t = accp<P>(t, max3f(y.z - fmaxf(ux.z, lu.z), fminf(lx.z, ul.z) - y.z, 0.f));
+            t = accp<P>(t, max3f(y.w - fmaxf(ux.w, lu.w), fminf(lx.w, ul.w) - y.w, 0.f));
+            s[u] = t;
+        }
+    }
+    return reduceW<W>(s, lane);
+}
+
+// Read the W list entries at g (g % 4 == 0 for W = 4, 2; any for W = 1).
+template <int W>
+__device__ __forceinline__ void read_group(const int *lst, int g, int (&li)[4]) {
+    if constexpr (W == 4) {
+        const int4 v = *reinterpret_cast<const int4 *>(lst + g);
+        li[0] = v.x; li[1] = v.y; li[2] = v.z; li[3] = v.w;
+    } else if constexpr (W == 2) {
+        const int2 v = *reinterpret_cast<const int2 *>(lst + g);
+        li[0] = v.x; li[1] = v.y; li[2] = v.x; li[3] = v.y;
+    } else {
+        li[0] = li[1] = li[2] = li[3] = lst[g];
+    }
 }
 
 // Append the keys of the lanes with `pass` (one lane per survivor) to query q's list.
@@ -205,11 +290,12 @@ improved_kernel(ImprovedArgs a, int Ct) {
     constexpr int NV = EPL / 4;
     constexpr int NPAD = 32 * EPL;
     extern __shared__ __align__(16) float sm[];
-    // [Ct][NPAD] blocks: x (B1X), U(x), L(x) (!KO); then per-warp beta1 slots [NW][64]
+    // [Ct][NPAD] blocks: x (B1X), U(x), L(x) (!KO); then per warp: the survivor list of
+    // the current phase (local rows, 68 ints), the phase-2 list (68 ints) and its beta1 (64)
     float *sX = sm;
     float *sU = sm + (B1X ? (size_t)Ct * NPAD : 0);
     float *sL = sU + (KO ? 0 : (size_t)Ct * NPAD);
-    float *sB1 = sL + (KO ? 0 : (size_t)Ct * NPAD);
+    int *sW = reinterpret_cast<int *>(sL + (KO ? 0 : (size_t)Ct * NPAD));
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int subs = 64 / Ct;
@@ -222,7 +308,7 @@ improved_kernel(ImprovedArgs a, int Ct) {
     if (cnt == 0) return;
     const int ct = (int)((a.N - c0) < Ct ? (a.N - c0) : Ct);
     const int n = a.n;
-    const unsigned long long submask = (Ct == 64 ? ~0ull : ((1ull << Ct) - 1)) << (sub * Ct);
+    const unsigned long long ctmask = Ct == 64 ? ~0ull : ((1ull << Ct) - 1);
 
     // stage the tile: x padded with 0 (the query's padded U = +inf, L = -inf give d = 0);
     // U(x) = +inf, L(x) = -inf padding gives d = 0 in phase 2
@@ -238,16 +324,20 @@ improved_kernel(ImprovedArgs a, int Ct) {
     }
     __syncthreads();
 
-    float *myB1 = sB1 + warp * 64;
+    int *lst1 = sW + warp * 200;   // 68 ints
+    int *lst2 = lst1 + 68;         // 68 ints
+    float *b1v = reinterpret_cast<float *>(lst2 + 68);  // 64 floats
     unsigned long long evals1 = 0, evals2 = 0;
     const int *eq = a.tile_q + tile * a.Qb;
     const unsigned long long *em = a.tile_m + tile * a.Qb;
     const int u_me = lane >> 3;  // survivor slot this lane ends up holding after reduce4
+    const bool lead8 = (lane & 7) == 0;
+    const unsigned lt = (1u << lane) - 1u;
     int e = warp;
     if (e >= cnt) return;
     QRegs<NV, B1X, KO> cur, nxt;
     int64_t qe = eq[e];
-    unsigned long long mcur = em[e] & submask;
+    unsigned long long mcur = (em[e] >> (sub * Ct)) & ctmask;
     load_p1<EPL, B1X, KO>(cur, a, qe, c0t, lane);
     if (PREFETCH) load_p2<EPL, B1X, KO>(cur, a, qe, lane);
     while (true) {
@@ -257,126 +347,117 @@ improved_kernel(ImprovedArgs a, int Ct) {
         unsigned long long mn = 0;
         if (more) {
             qn = eq[en];
-            mn = em[en] & submask;
+            mn = (em[en] >> (sub * Ct)) & ctmask;
             if constexpr (PREFETCH) {
                 load_p1<EPL, B1X, KO>(nxt, a, qn, c0t, lane);
                 load_p2<EPL, B1X, KO>(nxt, a, qn, lane);
             }
         }
         const int64_t q = qe;
-        unsigned long long m = mcur;
-        // ---------------- phase 1: beta1 (B1X) -> phase-2 mask
-        unsigned long long m2 = 0;
+        float *gq = a.gate_w ? a.gate_w + q * a.ldb + c0 : nullptr;
+        // ---------------- phase 1: beta1 (B1X) of the gate survivors -> phase-2 list
+        // groups of 4 survivors; a tail of 1 or 2 runs as a 1- or 2-wide group (lane l then
+        // holds slot l >> 5-log2(W)), so few slots are spent on padding
+        int n2 = 0;
         if constexpr (B1X) {
-            while (m) {
-                int bits[4];
-                const int nb = take4(m, bits);
-                evals1 += nb;
-                float s[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    const float4 uu = cur.u[v], ll = cur.l[v];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const float4 x = *reinterpret_cast<const float4 *>(
-                            sX + (bits[u] - sub * Ct) * NPAD + 4 * lane + 128 * v);
-                        float t = s[u];
-                        t = accp<P>(t, max3f(x.x - uu.x, ll.x - x.x, 0.f));
-                        t = accp<P>(t, max3f(x.y - uu.y, ll.y - x.y, 0.f));
-                        t = accp<P>(t, max3f(x.z - uu.z, ll.z - x.z, 0.f));
-                        t = accp<P>(t, max3f(x.w - uu.w, ll.w - x.w, 0.f));
-                        s[u] = t;
-                    }
-                }
-                const float b1 = reduce4(s[0], s[1], s[2], s[3], lane);
-                const int myb = pick4(bits, u_me);
-                const bool lead = (lane & 7) == 0 && u_me < nb;
+            const int n1 = compact_mask(mcur, lst1, lane);
+            __syncwarp();
+            evals1 += n1;
+            auto phase1 = [&](auto wc, int g) {
+                constexpr int W = decltype(wc)::value;
+                constexpr int SH = W == 4 ? 3 : (W == 2 ? 4 : 5);
+                int li[4];
+                read_group<W>(lst1, g, li);
+                const float b1 = p1_group<W, P, NV, NPAD>(sX, li, cur.u, cur.l, lane);
+                const int us = lane >> SH;
+                const int myl = W == 1 ? li[0] : pick4(make_int4(li[0], li[1], li[2], li[3]), us);
+                const bool pass = (lane & ((1 << SH) - 1)) == 0 && g + us < n1 && (DENSE || b1 <= cur.thr);
                 if constexpr (!DENSE) {
                     // keep beta1 for the DTW walk's cascading abandon: the gate slot (beta0,
                     // already consumed by this range's mask) takes -beta1 (<= 0, so no later
                     // range re-selects it; the walk reads |.|)
-                    if (lead && b1 <= cur.thr) a.gate_w[q * a.ldb + c0t + myb] = -b1;
+                    if (pass) gq[myl] = -b1;
                 }
                 if constexpr (KO) {
                     if constexpr (DENSE) {
-                        if (lead) a.dense[q * a.ldd + c0t + myb] = rootp<P>(b1);
+                        if (pass) a.dense[q * a.ldd + c0 + myl] = rootp<P>(b1);
                     } else {
-                        append_keys(a, q, lead && b1 <= cur.thr, b1, c0t + myb, lane);
+                        append_keys(a, q, pass, b1, c0 + myl, lane);
                     }
                 } else {
-                    const bool pass = lead && (DENSE || b1 <= cur.thr);
-                    if (pass) myB1[myb] = b1;
                     const unsigned bal = __ballot_sync(0xffffffffu, pass);
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        if ((bal >> (8 * u)) & 1u) m2 |= 1ull << bits[u];
+                    if (pass) {
+                        const int pos = n2 + __popc(bal & lt);
+                        lst2[pos] = myl;
+                        b1v[pos] = b1;
+                    }
+                    n2 += __popc(bal);
                 }
+            };
+            int g = 0;
+            for (; n1 - g >= 3; g += 4) phase1(std::integral_constant<int, 4>{}, g);
+            if (n1 - g == 2) phase1(std::integral_constant<int, 2>{}, g);
+            else if (n1 - g == 1) phase1(std::integral_constant<int, 1>{}, g);
+            if constexpr (!KO) {
+                if (lane < ((4 - (n2 & 3)) & 3)) lst2[n2 + lane] = 0;
             }
             __syncwarp();
         } else {
-            m2 = m;
+            n2 = compact_mask(mcur, lst2, lane);
+            __syncwarp();
         }
         // ---------------- phase 2: beta2, LB_Improved^p = beta1 + beta2
         if constexpr (!KO) {
-            if (!PREFETCH && m2) load_p2<EPL, B1X, KO>(cur, a, q, lane);
-            while (m2) {
-                int bits[4];
-                const int nb = take4(m2, bits);
-                evals2 += nb;
-                float s[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    const float4 y = cur.y[v], lu = cur.lu[v], ul = cur.ul[v];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int off = (bits[u] - sub * Ct) * NPAD + 4 * lane + 128 * v;
-                        const float4 ux = *reinterpret_cast<const float4 *>(sU + off);
-                        const float4 lx = *reinterpret_cast<const float4 *>(sL + off);
-                        // d = max(y - max(Ux, LU), min(Lx, UL) - y, 0)
-                        float t = s[u];
-                        t = accp<P>(t, max3f(y.x - fmaxf(ux.x, lu.x), fminf(lx.x, ul.x) - y.x, 0.f));
-                        t = accp<P>(t, max3f(y.y - fmaxf(ux.y, lu.y), fminf(lx.y, ul.y) - y.y, 0.f));
-                        t = accp<P>(t, max3f(y.z - fmaxf(ux.z, lu.z), fminf(lx.z, ul.z) - y.z, 0.f));
-                        t = accp<P>(t, max3f(y.w - fmaxf(ux.w, lu.w), fminf(lx.w, ul.w) - y.w, 0.f));
-                        s[u] = t;
-                    }
-                }
-                const float b2 = reduce4(s[0], s[1], s[2], s[3], lane);
-                const int myb = pick4(bits, u_me);
+            if (!PREFETCH && n2) load_p2<EPL, B1X, KO>(cur, a, q, lane);
+            evals2 += n2;
+            auto phase2 = [&](auto wc, int g) {
+                constexpr int W = decltype(wc)::value;
+                constexpr int SH = W == 4 ? 3 : (W == 2 ? 4 : 5);
+                int li[4];
+                read_group<W>(lst2, g, li);
+                const float b2 = p2_group<W, P, NV, NPAD>(sU, sL, li, cur.y, cur.lu, cur.ul, lane);
+                const int us = lane >> SH;
+                const int myl = W == 1 ? li[0] : pick4(make_int4(li[0], li[1], li[2], li[3]), us);
                 float b1;
                 if constexpr (B1X) {
-                    b1 = myB1[myb];
+                    b1 = b1v[min(g + us, n2 - 1)];
                 } else {
-                    const float va = __shfl_sync(0xffffffffu, cur.b1a, myb & 31);
-                    const float vb = __shfl_sync(0xffffffffu, cur.b1b, myb & 31);
-                    b1 = myb < 32 ? va : vb;
+                    const int t64 = sub * Ct + myl;  // slot in the 64-tile
+                    const float va = __shfl_sync(0xffffffffu, cur.b1a, t64 & 31);
+                    const float vb = __shfl_sync(0xffffffffu, cur.b1b, t64 & 31);
+                    b1 = t64 < 32 ? va : vb;
                 }
                 const float beta = b1 + b2;
-                const bool lead = (lane & 7) == 0 && u_me < nb;
+                const bool lead = (lane & ((1 << SH) - 1)) == 0 && g + us < n2;
                 if constexpr (DENSE) {
-                    if (lead) a.dense[q * a.ldd + c0t + myb] = rootp<P>(beta);
+                    if (lead) a.dense[q * a.ldd + c0 + myl] = rootp<P>(beta);
                 } else {
-                    append_keys(a, q, lead && beta <= cur.thr, beta, c0t + myb, lane);
+                    append_keys(a, q, lead && beta <= cur.thr, beta, c0 + myl, lane);
                 }
-            }
-            if constexpr (B1X) __syncwarp();
+            };
+            int g = 0;
+            for (; n2 - g >= 3; g += 4) phase2(std::integral_constant<int, 4>{}, g);
+            if (n2 - g == 2) phase2(std::integral_constant<int, 2>{}, g);
+            else if (n2 - g == 1) phase2(std::integral_constant<int, 1>{}, g);
         } else if constexpr (!B1X) {
             // Alg. 2 (keogh-only) over the dense beta1 block: the gate survivors are the keys
-            while (m2) {
-                int bits[4];
-                const int nb = take4(m2, bits);
-                const int myb = pick4(bits, u_me);
-                const float va = __shfl_sync(0xffffffffu, cur.b1a, myb & 31);
-                const float vb = __shfl_sync(0xffffffffu, cur.b1b, myb & 31);
-                const float b1 = myb < 32 ? va : vb;
-                const bool lead = (lane & 7) == 0 && u_me < nb;
+            for (int g = 0; g < n2; g += 4) {
+                const int4 li = *reinterpret_cast<const int4 *>(lst2 + g);
+                const int nb = min(4, n2 - g);
+                const int myl = pick4(li, u_me);
+                const int t64 = sub * Ct + myl;
+                const float va = __shfl_sync(0xffffffffu, cur.b1a, t64 & 31);
+                const float vb = __shfl_sync(0xffffffffu, cur.b1b, t64 & 31);
+                const float b1 = t64 < 32 ? va : vb;
+                const bool lead = lead8 && u_me < nb;
                 if constexpr (DENSE) {
-                    if (lead) a.dense[q * a.ldd + c0t + myb] = rootp<P>(b1);
+                    if (lead) a.dense[q * a.ldd + c0 + myl] = rootp<P>(b1);
                 } else {
-                    append_keys(a, q, lead && b1 <= cur.thr, b1, c0t + myb, lane);
+                    append_keys(a, q, lead && b1 <= cur.thr, b1, c0 + myl, lane);
                 }
             }
         }
+        __syncwarp();
         if (!more) break;
         if constexpr (PREFETCH) {
             cur = nxt;
@@ -400,7 +481,7 @@ int launch_imp_t(const ImprovedArgs &a, int64_t ntiles, cudaStream_t st) {
     const int arrays = (B1X ? 1 : 0) + (KO ? 0 : 2);
     // staged rows: at most 64 candidates and 192 KB (3 arrays) / 128 KB (2 arrays)
     const int Ct = std::min(64, 16384 / NPAD);
-    const size_t smem = (size_t)arrays * Ct * NPAD * sizeof(float) + (size_t)(NT / 32) * 64 * sizeof(float);
+    const size_t smem = (size_t)arrays * Ct * NPAD * sizeof(float) + (size_t)(NT / 32) * 200 * sizeof(int);
     auto k = improved_kernel<P, EPL, B1X, KO, DENSE>;
     DTWLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t grid = ntiles * (64 / Ct);
@@ -459,8 +540,11 @@ int launch_improved(const ImprovedArgs &a, int p, bool keogh_only, bool dense, c
         DTWLB_LAUNCH_CHECK();
     }
     const int epl = a.npadE / 32;
-    return p == 1 ? launch_imp_p<1>(a, epl, keogh_only, dense, ntiles, st)
-                  : launch_imp_p<2>(a, epl, keogh_only, dense, ntiles, st);
+    if (a.ev0) DTWLB_CUDA(cudaEventRecord(a.ev0, st));
+    const int rc = p == 1 ? launch_imp_p<1>(a, epl, keogh_only, dense, ntiles, st)
+                          : launch_imp_p<2>(a, epl, keogh_only, dense, ntiles, st);
+    if (a.ev1) DTWLB_CUDA(cudaEventRecord(a.ev1, st));
+    return rc;
 }
 
 }  // namespace dtwlb

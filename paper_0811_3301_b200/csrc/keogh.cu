@@ -31,18 +31,6 @@ namespace {
 constexpr int TQ = 64, TC = 128, KC = 32, KP = KC + 4;  // KP: padded pitch (floats)
 constexpr int NT = 256;
 
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src_bytes) {
-    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async4(void *smem, const void *gmem, int src_bytes) {
-    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
 template <bool PAA>
 struct Stage {  // chunk of the operands, written by cp.async (double-buffered)
     float X[TC][KP];           // candidate rows (LB_Keogh) or their lower sums (PAA)

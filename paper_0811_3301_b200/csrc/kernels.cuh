@@ -64,6 +64,7 @@ struct ImprovedArgs {
     unsigned long long *tile_m;    // [ceil(N/64)][Qb]
     int *tile_q;                   // [ceil(N/64)][Qb]
     int *tile_cnt;                 // [ceil(N/64)]
+    cudaEvent_t ev0, ev1;          // optional: recorded around the survivor kernel (timing)
 };
 size_t improved_scratch_bytes(int64_t Qb, int64_t N);
 void improved_scratch_bind(ImprovedArgs &a, void *p);

@@ -20,6 +20,7 @@
 //   a6  finalize: k smallest by (DTW^p, index), rooted.
 // Pruning rule (reading c3/c13): a bound prunes only if bound > tau^p (1 + eps).
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -97,11 +98,14 @@ __global__ void pad_rows_kernel(const float *__restrict__ src, int64_t rows, int
     }
 }
 
-// Sampled quantile of each query's beta1 row: t_S such that ~S candidates have
-// beta1 <= t_S (selection threshold only -- correctness does not depend on it).
+// Sampled quantiles of each query's gate-bound row: t_r (r = 0..R-2) such that ~S*G^r
+// candidates have gate <= t_r.  They split the candidates into R ranges processed in
+// ascending order (selection thresholds only -- correctness does not depend on them).
 constexpr int kSample = 2048;
+constexpr int kMaxRanges = 8;
 __global__ void __launch_bounds__(512) sample_threshold_kernel(const float *__restrict__ beta1, int64_t ldb,
-                                                               int64_t N, int64_t S, float *__restrict__ tS) {
+                                                               int64_t N, int64_t S, int R, int G,
+                                                               float *__restrict__ tS, int Qb) {
     __shared__ float v[kSample];
     const int64_t q = blockIdx.x;
     const int M = N < kSample ? (int)N : kSample;
@@ -123,15 +127,17 @@ __global__ void __launch_bounds__(512) sample_threshold_kernel(const float *__re
             }
             __syncthreads();
         }
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < R - 1) {
+        int64_t Sr = S;
+        for (int i = 0; i < (int)threadIdx.x; ++i) Sr *= G;
         float t;
-        if (S >= N) t = kInf;
+        if (Sr >= N) t = kInf;
         else {
-            int64_t r = (S * M + N - 1) / N;  // rank in the sample
+            int64_t r = (Sr * M + N - 1) / N;  // rank in the sample
             r = r < 1 ? 1 : (r > M ? M : r);
             t = v[r - 1];
         }
-        tS[q] = t;
+        tS[(int64_t)threadIdx.x * Qb + q] = t;
     }
 }
 
@@ -186,10 +192,10 @@ __global__ void init_state_kernel(QState s, int Qb, int k) {
     }
 }
 
-__global__ void set_range_kernel(QState s, int Qb, int macro) {
+__global__ void set_range_kernel(QState s, int Qb, int macro, int R) {
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < Qb; q += gridDim.x * blockDim.x) {
-        s.lo[q] = macro == 0 ? -kInf : s.tS[q];
-        s.hi[q] = macro == 0 ? s.tS[q] : kInf;
+        s.lo[q] = macro == 0 ? -kInf : s.tS[(int64_t)(macro - 1) * Qb + q];
+        s.hi[q] = macro == R - 1 ? kInf : s.tS[(int64_t)macro * Qb + q];
         s.len[q] = 0;
     }
 }
@@ -517,7 +523,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     char *imp_scratch;
     DTWLB_TRY(wsget(S_MASK, improved_scratch_bytes(Qb, N), &imp_scratch));
     char *stb;
-    const size_t st_bytes = (size_t)Qb * 4 * 8 + (Qb + 1) * 8 + 64 + 64 + 16 * 16;
+    const size_t st_bytes = (size_t)Qb * 4 * (8 + kMaxRanges) + (Qb + 1) * 8 + 64 + 64 + 16 * 16;
     DTWLB_TRY(wsget(S_STATE, st_bytes, &stb));
     QState s;
     {
@@ -528,7 +534,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         s.thr = reinterpret_cast<float *>(take(Qb * 4));
         s.lo = reinterpret_cast<float *>(take(Qb * 4));
         s.hi = reinterpret_cast<float *>(take(Qb * 4));
-        s.tS = reinterpret_cast<float *>(take(Qb * 4));
+        s.tS = reinterpret_cast<float *>(take(Qb * 4 * (kMaxRanges - 1)));
         s.len = reinterpret_cast<int *>(take(Qb * 4));
         s.pos = reinterpret_cast<int *>(take(Qb * 4));
         s.rnd = reinterpret_cast<int *>(take(Qb * 4));
@@ -546,13 +552,19 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
 
     // target size of the first (best-first) range
     const int64_t S = std::max<int64_t>(std::max<int64_t>(256, 4LL * k), std::min<int64_t>(8192, N / 64));
+    // number of ranges R and the growth G of their sampled sizes (S, S*G, S*G^2, ..., rest)
+    static const int env_R = [] { const char *e = getenv("DTWLB_RANGES"); return e ? atoi(e) : 0; }();
+    static const int env_G = [] { const char *e = getenv("DTWLB_RANGE_GROWTH"); return e ? atoi(e) : 0; }();
+    const int R = std::min(kMaxRanges, std::max(2, env_R > 0 ? env_R : 2));
+    const int G = std::max(2, env_G > 0 ? env_G : 8);
 
     std::vector<int> h_len(Qb), run_q, run_idx;
     int *d_runs;
     double ms_keogh = 0, ms_select = 0, ms_improved = 0, ms_dtw = 0;
     unsigned long long r1[3] = {0, 0, 0}, r1_base[4] = {0, 0, 0, 0};
     int64_t walk_rounds = 0;
-    cudaEvent_t ev[4];
+    cudaEvent_t ev[6];
+    double ms_survivor = 0;
     if (stats) for (auto &e : ev) cudaEventCreate(&e);
 
     for (int64_t qb0 = 0; qb0 < Q; qb0 += Qb) {
@@ -568,7 +580,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         if (stats) cudaEventRecord(ev[1], st);
         init_state_kernel<<<(unsigned)ceil_div(qn, 256), 256, 0, st>>>(s, (int)qn, k);
         DTWLB_LAUNCH_CHECK();
-        sample_threshold_kernel<<<(unsigned)qn, 512, 0, st>>>(beta1, ldb, N, S, s.tS);
+        sample_threshold_kernel<<<(unsigned)qn, 512, 0, st>>>(beta1, ldb, N, S, R, G, s.tS, (int)qn);
         DTWLB_LAUNCH_CHECK();
         if (stats) {
             cudaEventRecord(ev[2], st);
@@ -580,8 +592,8 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
             ms_select += b;
         }
 
-        for (int macro = 0; macro < 2; ++macro) {
-            set_range_kernel<<<(unsigned)ceil_div(qn, 256), 256, 0, st>>>(s, (int)qn, macro);
+        for (int macro = 0; macro < R; ++macro) {
+            set_range_kernel<<<(unsigned)ceil_div(qn, 256), 256, 0, st>>>(s, (int)qn, macro, R);
             DTWLB_LAUNCH_CHECK();
             if (stats) cudaEventRecord(ev[0], st);
             // ---- a4: LB_Improved on the range's LB_Keogh survivors ----
@@ -612,6 +624,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 ia.cap = cap;
                 ia.list_len = s.len;
                 ia.n_eval = s.stat + 0;
+                if (stats) { ia.ev0 = ev[4]; ia.ev1 = ev[5]; }
                 improved_scratch_bind(ia, imp_scratch);
                 DTWLB_TRY(launch_improved(ia, p, keogh_only, false, st));
             } else {
@@ -621,6 +634,11 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
             // ---- a3: sort each query's list in runs ----
             DTWLB_CUDA(cudaMemcpyAsync(h_len.data(), s.len, sizeof(int) * qn, cudaMemcpyDeviceToHost, st));
             DTWLB_CUDA(cudaStreamSynchronize(st));
+            if (stats) {
+                float t = 0;
+                cudaEventElapsedTime(&t, ev[4], ev[5]);
+                ms_survivor += t;
+            }
             run_q.clear();
             run_idx.clear();
             for (int q = 0; q < qn; ++q)
@@ -728,6 +746,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         stats->ms_keogh = ms_keogh;
         stats->ms_select = ms_select;
         stats->ms_improved = ms_improved;
+        stats->ms_survivor_kernel = ms_survivor;
         stats->ms_dtw = ms_dtw;
         stats->ms_total = tm.ms(0, 2);
         stats->kernel_launches = (int64_t)(__atomic_load_n(&g_launches, __ATOMIC_RELAXED) - launches0);
