@@ -369,13 +369,13 @@ __device__ __forceinline__ void four_rows(float (&B)[2 * WB + 2], const float (&
     }
 }
 
-// Per-lane staging slot of the pipelined refill: the y window (NY floats) and x[0..7]
-// of the lane's next pair, written by cp.async while the lane still waits one step;
-// +4 floats of padding rotate the banks between lanes.
+// Per-lane staging slot of the pipelined refill: the y window (NY floats), x[0..7] and
+// the query envelope U[0..3], L[0..3] of the lane's next pair, written by cp.async while
+// the lane still waits one step; +4 floats of padding rotate the banks between lanes.
 template <int WB>
 struct Dtw4Cfg {
     static constexpr int NY = (2 * WB + 4 + 3) / 4 * 4;
-    static constexpr int SL = NY + 12;
+    static constexpr int SL = NY + 20;
     static constexpr size_t smem = (size_t)NT * SL * sizeof(float) +
                                    (size_t)(NT / 32) * kChunk4 * (sizeof(unsigned long long) + sizeof(int));
 };
@@ -413,6 +413,7 @@ dtw4_kernel(DtwArgs a) {
     const bool casc = WALK && a.b1 != nullptr;
     float rest = 0.f, rest_n = 0.f;
     const float *ur = nullptr, *lr = nullptr;
+    float uc[4], lc[4];  // U(y), L(y) of the current 4-row block (loaded one block ahead)
     unsigned long long rows_done = 0, n_abandon = 0, n_started = 0;
 
     while (true) {
@@ -433,8 +434,14 @@ dtw4_kernel(DtwArgs a) {
                     const float4 x1 = *reinterpret_cast<const float4 *>(slot + NY + 4);
                     xv[0] = x0.x; xv[1] = x0.y; xv[2] = x0.z; xv[3] = x0.w;
                     xv[4] = x1.x; xv[5] = x1.y; xv[6] = x1.z; xv[7] = x1.w;
+                    if (casc) {
+                        const float4 u0 = *reinterpret_cast<const float4 *>(slot + NY + 8);
+                        const float4 l0 = *reinterpret_cast<const float4 *>(slot + NY + 12);
+                        uc[0] = u0.x; uc[1] = u0.y; uc[2] = u0.z; uc[3] = u0.w;
+                        lc[0] = l0.x; lc[1] = l0.y; lc[2] = l0.z; lc[3] = l0.w;
+                    }
                     thr = thr_n;
-                    rest = rest_n;
+                    rest = fabsf(rest_n);
                     st = kActive;
                     ++n_started;
                 }
@@ -488,7 +495,7 @@ dtw4_kernel(DtwArgs a) {
                     beta_n = __uint_as_float((uint32_t)(key >> 32));
                     thr_n = a.thr[qy];
                     if (casc) {
-                        rest_n = fabsf(__ldg(a.b1 + qy * a.ldb + c));  // beta1 = sum of all row terms
+                        rest_n = __ldg(a.b1 + qy * a.ldb + c);  // +-beta1 = sum of all row terms (|.| later)
                         ur = a.Uq + qy * n;
                         lr = a.Lq + qy * n;
                     }
@@ -509,6 +516,18 @@ dtw4_kernel(DtwArgs a) {
                 } else {
 #pragma unroll
                     for (int t = 0; t < 8; ++t) cp_async4(slot + NY + t, t < n ? xr + t : xr, t < n ? 4 : 0);
+                }
+                if (casc) {
+                    if (((n & 3) == 0) && n >= 4) {
+                        cp_async16(slot + NY + 8, ur, 16);
+                        cp_async16(slot + NY + 12, lr, 16);
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            cp_async4(slot + NY + 8 + t, t < n ? ur + t : ur, t < n ? 4 : 0);
+                            cp_async4(slot + NY + 12 + t, t < n ? lr + t : lr, t < n ? 4 : 0);
+                        }
+                    }
                 }
                 cp_commit();
 #pragma unroll
@@ -544,19 +563,24 @@ dtw4_kernel(DtwArgs a) {
             for (int blk = 0; blk < 2; ++blk) {
                 if (i + 4 > n) break;
                 const float x4[4] = {xv[0], xv[1], xv[2], xv[3]};
-                if (casc) {  // query envelope rows: L1-resident (the warp's items share queries)
-                    float u4[4], l4[4];
+                if (casc) {  // LB_Keogh terms of these 4 rows; envelope of the next block in flight
+                    rest -= row_lb<P>(x4[0], uc[0], lc[0]) + row_lb<P>(x4[1], uc[1], lc[1]) +
+                            row_lb<P>(x4[2], uc[2], lc[2]) + row_lb<P>(x4[3], uc[3], lc[3]);
+                    const int inx = i + 4;
                     if ((n & 3) == 0) {
-                        const float4 uu = __ldg(reinterpret_cast<const float4 *>(ur + i));
-                        const float4 ll = __ldg(reinterpret_cast<const float4 *>(lr + i));
-                        u4[0] = uu.x; u4[1] = uu.y; u4[2] = uu.z; u4[3] = uu.w;
-                        l4[0] = ll.x; l4[1] = ll.y; l4[2] = ll.z; l4[3] = ll.w;
+                        if (inx < n) {
+                            const float4 uu = __ldg(reinterpret_cast<const float4 *>(ur + inx));
+                            const float4 ll = __ldg(reinterpret_cast<const float4 *>(lr + inx));
+                            uc[0] = uu.x; uc[1] = uu.y; uc[2] = uu.z; uc[3] = uu.w;
+                            lc[0] = ll.x; lc[1] = ll.y; lc[2] = ll.z; lc[3] = ll.w;
+                        }
                     } else {
 #pragma unroll
-                        for (int t = 0; t < 4; ++t) { u4[t] = __ldg(ur + i + t); l4[t] = __ldg(lr + i + t); }
+                        for (int t = 0; t < 4; ++t) {
+                            uc[t] = inx + t < n ? __ldg(ur + inx + t) : 0.f;
+                            lc[t] = inx + t < n ? __ldg(lr + inx + t) : 0.f;
+                        }
                     }
-                    rest -= row_lb<P>(x4[0], u4[0], l4[0]) + row_lb<P>(x4[1], u4[1], l4[1]) +
-                            row_lb<P>(x4[2], u4[2], l4[2]) + row_lb<P>(x4[3], u4[3], l4[3]);
                 }
                 four_rows<WB, P, EXACT>(B, Y, x4, w2);
                 i += 4;

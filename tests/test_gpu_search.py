@@ -119,6 +119,26 @@ def test_keogh_only_index_base_eps0(cuda_ok):
     check(qs, db, 25, 2, 5, query_block=4)   # several query blocks
 
 
+@pytest.mark.parametrize("name", ["C2p1", "C2p2"])
+def test_cascade_and_prefilter_switches(cuda_ok, name):
+    """Every combination of the pre-filter and the DTW cascading abandon
+    (reading c19) returns the same exact k-NN; only the work done differs."""
+    from paper_0811_3301_b200 import nn_search
+    c = datagen.CONFIGS[name]
+    qs, db = datagen.make(c, Q=24, N=6000)
+    ref = None
+    for pf in (True, False):
+        for cas in (True, False):
+            g_idx, g_dist = check(qs, db, c.w, c.p, 4, brute=False, prefilter=pf, cascade=cas)
+            if ref is None:
+                ref = (g_idx, g_dist)
+            else:  # bit-identical across modes: DTW values do not depend on the pruning path
+                assert np.array_equal(ref[0], g_idx) and np.array_equal(ref[1], g_dist)
+    _, _, st = nn_search(dev(qs), dev(db), c.w, c.p, 4, return_stats=True)
+    assert st["prefilter_evaluated"] == 24 * 6000 and st["prefilter_segment"] == 8
+    assert st["dtw_evaluated"] <= st["improved_evaluated"] <= st["keogh_evaluated"] <= 24 * 6000
+
+
 def test_host_buffers(cuda_ok):
     """e2e path: host (numpy) inputs and outputs through the same C-ABI call."""
     from paper_0811_3301_b200 import nn_search
