@@ -96,8 +96,9 @@ select_mask_kernel(const float *__restrict__ gate, int64_t ldb, int64_t Qb, int6
 template <int EPL, bool B1X>
 struct ImpCfg {
     static constexpr int NT = EPL <= 8 ? 512 : 256;
-    // prefetch the next entry's query registers while the current one is evaluated
-    // (n <= 256; beyond that the doubled query registers would spill)
+    // prefetch the next entry's phase-1 query registers (U, L) while the current one is
+    // evaluated, and issue the current entry's phase-2 loads (y, LU, UL) before its phase 1
+    // (n <= 256; beyond that the extra query registers would spill)
     static constexpr bool PREFETCH = EPL <= 8;
 };
 
@@ -148,7 +149,7 @@ __device__ __forceinline__ void load_p2(QRegs<EPL / 4, B1X, KO> &r, const Improv
 }
 
 // Compact the set bits of the warp-uniform 64-bit mask m into lst[0..cnt) (ascending),
-// padded with zeros to a multiple of 4 (padding slots are evaluated redundantly on
+// padded with zeros to a multiple of 8 (padding slots are evaluated redundantly on
 // local row 0 and discarded).  Returns cnt.  Caller syncs the warp before reading.
 __device__ __forceinline__ int compact_mask(unsigned long long m, int *lst, int lane) {
     const unsigned lo = (unsigned)m, hi = (unsigned)(m >> 32);
@@ -157,7 +158,7 @@ __device__ __forceinline__ int compact_mask(unsigned long long m, int *lst, int 
     if ((lo >> lane) & 1u) lst[__popc(lo & lt)] = lane;
     if ((hi >> lane) & 1u) lst[nlo + __popc(hi & lt)] = lane + 32;
     const int cnt = nlo + __popc(hi);
-    if (lane < ((4 - (cnt & 3)) & 3)) lst[cnt + lane] = 0;
+    if (lane < ((8 - (cnt & 7)) & 7)) lst[cnt + lane] = 0;
     return cnt;
 }
 
@@ -182,10 +183,27 @@ __device__ __forceinline__ int pick4(const int4 &b, int u) {
     return u == 0 ? b.x : (u == 1 ? b.y : (u == 2 ? b.z : b.w));
 }
 
-// W-wide butterfly (W in {1, 2, 4}): lane l ends with the warp total of slot l >> (5 - log2 W).
+// W-wide butterfly (W in {1, 2, 4, 8}): lane l ends with the warp total of slot l >> (5 - log2 W).
 template <int W>
-__device__ __forceinline__ float reduceW(const float (&s)[4], int lane) {
-    if constexpr (W == 4) {
+__device__ __forceinline__ float reduceW(const float (&s)[8], int lane) {
+    if constexpr (W == 8) {
+        // transposed: keep the half of the slots this lane's half-warp owns at each level
+        const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+        float k[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            k[j] = h16 ? s[4 + j] : s[j];
+            k[j] += __shfl_xor_sync(0xffffffffu, h16 ? s[j] : s[4 + j], 16);
+        }
+        float m0 = h8 ? k[2] : k[0], m1 = h8 ? k[3] : k[1];
+        m0 += __shfl_xor_sync(0xffffffffu, h8 ? k[0] : k[2], 8);
+        m1 += __shfl_xor_sync(0xffffffffu, h8 ? k[1] : k[3], 8);
+        float v = h4 ? m1 : m0;
+        v += __shfl_xor_sync(0xffffffffu, h4 ? m0 : m1, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        return v;
+    } else if constexpr (W == 4) {
         return reduce4(s[0], s[1], s[2], s[3], lane);
     } else if constexpr (W == 2) {
         const bool hi16 = lane & 16;
@@ -207,9 +225,9 @@ __device__ __forceinline__ float reduceW(const float (&s)[4], int lane) {
 // Phase-1 partial sums of W survivors (local rows li[0..W)): lane covers samples
 // 4*lane + 128*v .. +3 of beta1 = sum_i d(x_i, [L_i, U_i])^p.
 template <int W, int P, int NV, int NPAD>
-__device__ __forceinline__ float p1_group(const float *sX, const int (&li)[4], const float4 (&uq)[NV],
+__device__ __forceinline__ float p1_group(const float *sX, const int (&li)[8], const float4 (&uq)[NV],
                                           const float4 (&lq)[NV], int lane) {
-    float s[4] = {0.f, 0.f, 0.f, 0.f};
+    float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
         const float4 uu = uq[v], ll = lq[v];
@@ -229,10 +247,10 @@ __device__ __forceinline__ float p1_group(const float *sX, const int (&li)[4], c
 
 // Phase-2 partial sums: beta2 = sum_i max(y_i - max(U(x)_i, LU_i), min(L(x)_i, UL_i) - y_i, 0)^p.
 template <int W, int P, int NV, int NPAD>
-__device__ __forceinline__ float p2_group(const float *sU, const float *sL, const int (&li)[4],
+__device__ __forceinline__ float p2_group(const float *sU, const float *sL, const int (&li)[8],
                                           const float4 (&yq)[NV], const float4 (&luq)[NV],
                                           const float4 (&ulq)[NV], int lane) {
-    float s[4] = {0.f, 0.f, 0.f, 0.f};
+    float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
         const float4 y = yq[v], lu = luq[v], ul = ulq[v];
@@ -252,10 +270,15 @@ __device__ __forceinline__ float p2_group(const float *sU, const float *sL, cons
     return reduceW<W>(s, lane);
 }
 
-// Read the W list entries at g (g % 4 == 0 for W = 4, 2; any for W = 1).
+// Read the W list entries at g (g % W == 0).
 template <int W>
-__device__ __forceinline__ void read_group(const int *lst, int g, int (&li)[4]) {
-    if constexpr (W == 4) {
+__device__ __forceinline__ void read_group(const int *lst, int g, int (&li)[8]) {
+    if constexpr (W == 8) {
+        const int4 v = *reinterpret_cast<const int4 *>(lst + g);
+        const int4 u = *reinterpret_cast<const int4 *>(lst + g + 4);
+        li[0] = v.x; li[1] = v.y; li[2] = v.z; li[3] = v.w;
+        li[4] = u.x; li[5] = u.y; li[6] = u.z; li[7] = u.w;
+    } else if constexpr (W == 4) {
         const int4 v = *reinterpret_cast<const int4 *>(lst + g);
         li[0] = v.x; li[1] = v.y; li[2] = v.z; li[3] = v.w;
     } else if constexpr (W == 2) {
@@ -324,9 +347,9 @@ improved_kernel(ImprovedArgs a, int Ct) {
     }
     __syncthreads();
 
-    int *lst1 = sW + warp * 200;   // 68 ints
-    int *lst2 = lst1 + 68;         // 68 ints
-    float *b1v = reinterpret_cast<float *>(lst2 + 68);  // 64 floats
+    int *lst1 = sW + warp * 224;   // 72 ints
+    int *lst2 = lst1 + 72;         // 72 ints
+    float *b1v = reinterpret_cast<float *>(lst2 + 72);  // 72 floats
     unsigned long long evals1 = 0, evals2 = 0;
     const int *eq = a.tile_q + tile * a.Qb;
     const unsigned long long *em = a.tile_m + tile * a.Qb;
@@ -339,7 +362,6 @@ improved_kernel(ImprovedArgs a, int Ct) {
     int64_t qe = eq[e];
     unsigned long long mcur = (em[e] >> (sub * Ct)) & ctmask;
     load_p1<EPL, B1X, KO>(cur, a, qe, c0t, lane);
-    if (PREFETCH) load_p2<EPL, B1X, KO>(cur, a, qe, lane);
     while (true) {
         const int en = e + NW;
         const bool more = en < cnt;
@@ -348,11 +370,9 @@ improved_kernel(ImprovedArgs a, int Ct) {
         if (more) {
             qn = eq[en];
             mn = (em[en] >> (sub * Ct)) & ctmask;
-            if constexpr (PREFETCH) {
-                load_p1<EPL, B1X, KO>(nxt, a, qn, c0t, lane);
-                load_p2<EPL, B1X, KO>(nxt, a, qn, lane);
-            }
+            if constexpr (PREFETCH) load_p1<EPL, B1X, KO>(nxt, a, qn, c0t, lane);
         }
+        if (PREFETCH && mcur) load_p2<EPL, B1X, KO>(cur, a, qe, lane);  // in flight during phase 1
         const int64_t q = qe;
         float *gq = a.gate_w ? a.gate_w + q * a.ldb + c0 : nullptr;
         // ---------------- phase 1: beta1 (B1X) of the gate survivors -> phase-2 list
@@ -365,12 +385,12 @@ improved_kernel(ImprovedArgs a, int Ct) {
             evals1 += n1;
             auto phase1 = [&](auto wc, int g) {
                 constexpr int W = decltype(wc)::value;
-                constexpr int SH = W == 4 ? 3 : (W == 2 ? 4 : 5);
-                int li[4];
+                constexpr int SH = W == 8 ? 2 : (W == 4 ? 3 : (W == 2 ? 4 : 5));
+                int li[8];
                 read_group<W>(lst1, g, li);
                 const float b1 = p1_group<W, P, NV, NPAD>(sX, li, cur.u, cur.l, lane);
                 const int us = lane >> SH;
-                const int myl = W == 1 ? li[0] : pick4(make_int4(li[0], li[1], li[2], li[3]), us);
+                const int myl = W == 1 ? li[0] : lst1[g + us];
                 const bool pass = (lane & ((1 << SH) - 1)) == 0 && g + us < n1 && (DENSE || b1 <= cur.thr);
                 if constexpr (!DENSE) {
                     // keep beta1 for the DTW walk's cascading abandon: the gate slot (beta0,
@@ -395,11 +415,12 @@ improved_kernel(ImprovedArgs a, int Ct) {
                 }
             };
             int g = 0;
+            for (; n1 - g >= 7; g += 8) phase1(std::integral_constant<int, 8>{}, g);
             for (; n1 - g >= 3; g += 4) phase1(std::integral_constant<int, 4>{}, g);
             if (n1 - g == 2) phase1(std::integral_constant<int, 2>{}, g);
             else if (n1 - g == 1) phase1(std::integral_constant<int, 1>{}, g);
             if constexpr (!KO) {
-                if (lane < ((4 - (n2 & 3)) & 3)) lst2[n2 + lane] = 0;
+                if (lane < ((8 - (n2 & 7)) & 7)) lst2[n2 + lane] = 0;
             }
             __syncwarp();
         } else {
@@ -412,12 +433,12 @@ improved_kernel(ImprovedArgs a, int Ct) {
             evals2 += n2;
             auto phase2 = [&](auto wc, int g) {
                 constexpr int W = decltype(wc)::value;
-                constexpr int SH = W == 4 ? 3 : (W == 2 ? 4 : 5);
-                int li[4];
+                constexpr int SH = W == 8 ? 2 : (W == 4 ? 3 : (W == 2 ? 4 : 5));
+                int li[8];
                 read_group<W>(lst2, g, li);
                 const float b2 = p2_group<W, P, NV, NPAD>(sU, sL, li, cur.y, cur.lu, cur.ul, lane);
                 const int us = lane >> SH;
-                const int myl = W == 1 ? li[0] : pick4(make_int4(li[0], li[1], li[2], li[3]), us);
+                const int myl = W == 1 ? li[0] : lst2[g + us];
                 float b1;
                 if constexpr (B1X) {
                     b1 = b1v[min(g + us, n2 - 1)];
@@ -436,6 +457,7 @@ improved_kernel(ImprovedArgs a, int Ct) {
                 }
             };
             int g = 0;
+            for (; n2 - g >= 7; g += 8) phase2(std::integral_constant<int, 8>{}, g);
             for (; n2 - g >= 3; g += 4) phase2(std::integral_constant<int, 4>{}, g);
             if (n2 - g == 2) phase2(std::integral_constant<int, 2>{}, g);
             else if (n2 - g == 1) phase2(std::integral_constant<int, 1>{}, g);
@@ -460,7 +482,14 @@ improved_kernel(ImprovedArgs a, int Ct) {
         __syncwarp();
         if (!more) break;
         if constexpr (PREFETCH) {
-            cur = nxt;
+            if constexpr (B1X) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v) { cur.u[v] = nxt.u[v]; cur.l[v] = nxt.l[v]; }
+            } else {
+                cur.b1a = nxt.b1a;
+                cur.b1b = nxt.b1b;
+            }
+            cur.thr = nxt.thr;
         } else {
             load_p1<EPL, B1X, KO>(cur, a, qn, c0t, lane);
         }
@@ -481,7 +510,7 @@ int launch_imp_t(const ImprovedArgs &a, int64_t ntiles, cudaStream_t st) {
     const int arrays = (B1X ? 1 : 0) + (KO ? 0 : 2);
     // staged rows: at most 64 candidates and 192 KB (3 arrays) / 128 KB (2 arrays)
     const int Ct = std::min(64, 16384 / NPAD);
-    const size_t smem = (size_t)arrays * Ct * NPAD * sizeof(float) + (size_t)(NT / 32) * 200 * sizeof(int);
+    const size_t smem = (size_t)arrays * Ct * NPAD * sizeof(float) + (size_t)(NT / 32) * 224 * sizeof(int);
     auto k = improved_kernel<P, EPL, B1X, KO, DENSE>;
     DTWLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t grid = ntiles * (64 / Ct);
