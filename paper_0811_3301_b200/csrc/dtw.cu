@@ -144,6 +144,64 @@ __device__ __forceinline__ float band_min(const float (&B)[2 * WB + 2]) {
     return m;
 }
 
+// Merge a completed pair (key = DTW^p bits << 32 | c) into query q's top-k -- the k
+// smallest keys (float bits of r << 32 | c), ascending (reading c4: ties to the smaller
+// index) -- and lower thr[q] to (k-th distance)(1+eps) once k results exist.  Taken under
+// the query's lock; keys and thr are read/written through L2 (volatile), so every other
+// warp's next refill or abandon test sees the tightened threshold.  Independent-thread-
+// scheduling safe: the lane that wins the lock does the work inside the same iteration.
+__device__ __forceinline__ void walk_result(const DtwArgs &a, int64_t q, unsigned long long key) {
+    volatile float *thr = a.thr + q;
+    if (!(__uint_as_float((uint32_t)(key >> 32)) <= *thr)) return;  // cannot enter the top-k
+    volatile unsigned long long *tk = a.topk + q * a.k;
+    int *lock = a.topk_lock + q;
+    bool done = false;
+    while (!done) {
+        if (atomicCAS(lock, 0, 1) == 0) {
+            __threadfence();
+            if (key < tk[a.k - 1]) {
+                int j = a.k - 1;
+                while (j > 0 && tk[j - 1] > key) {
+                    tk[j] = tk[j - 1];
+                    --j;
+                }
+                tk[j] = key;
+                const unsigned long long kth = tk[a.k - 1];
+                if (kth != ~0ull) *thr = __uint_as_float((uint32_t)(kth >> 32)) * (1.0f + a.eps);
+            }
+            __threadfence();
+            atomicExch(lock, 0);
+            done = true;
+        }
+    }
+}
+
+// WALK: the lanes with has_res append their completed pair (query q, key (DTW^p, c)) to
+// the round's result buffer (one warp-aggregated atomic); topk_merge_kernel merges the
+// buffer into the top-k after the launch, so the DTW kernels carry no lock/insert code.
+__device__ __forceinline__ void walk_results_warp(const DtwArgs &a, bool has_res, int q, uint32_t c, float r,
+                                                  int lane) {
+    const unsigned m = __ballot_sync(0xffffffffu, has_res);
+    if (!m) return;
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(a.rcount, (unsigned)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (has_res) {
+        const unsigned pos = base + __popc(m & ((1u << lane) - 1u));
+        DCHECK(pos < a.rcap, "result buffer overflow pos=%u cap=%lld", pos, (long long)a.rcap);
+        a.rkey[pos] = pack_key(r, c);
+        a.rq[pos] = q;
+    }
+}
+
+// After a walk round: merge the round's completed pairs (few: most pairs are abandoned)
+// into the per-query top-k (grid-stride, one result per thread).
+__global__ void __launch_bounds__(256) topk_merge_kernel(DtwArgs a) {
+    const unsigned cnt = *a.rcount;
+    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x)
+        walk_result(a, a.rq[t], a.rkey[t]);
+}
+
 template <int WB, int P, bool EXACT, bool WALK>
 __global__ void __launch_bounds__(NT)
 dtw_kernel(DtwArgs a, int ipw) {
@@ -193,6 +251,7 @@ dtw_kernel(DtwArgs a, int ipw) {
 
     int64_t cursor = a0;
     bool has = false;
+    uint32_t cand = 0;  // WALK: candidate of the lane's pair
     int64_t item = 0;
     const float *xr = nullptr, *yb = nullptr;
     const int64_t ystride = WALK ? a.LP : a.ysh_stride_s;  // elements between shifted copies
@@ -220,10 +279,11 @@ dtw_kernel(DtwArgs a, int ipw) {
                     DCHECK(j >= 0 && j < a.cap, "dtw item %lld q=%d j=%lld", (long long)item, q, (long long)j);
                     const unsigned long long key = a.list[(int64_t)q * a.cap + j];
                     const uint32_t c = (uint32_t)(key & 0xffffffffu);
+                    cand = c;
                     DCHECK((int64_t)c < a.Ndb, "dtw key c=%u N=%lld q=%d j=%lld key=%llx", c, (long long)a.Ndb, q,
                            (long long)j, key);
                     beta = __uint_as_float((uint32_t)(key >> 32));
-                    thr = thr_q;
+                    thr = *reinterpret_cast<volatile float *>(a.thr + q);  // tightened by walk_result
                     xr = a.db + (int64_t)c * n;
                     yb = yq;
                     if (casc) {
@@ -238,7 +298,7 @@ dtw_kernel(DtwArgs a, int ipw) {
                 }
                 DCHECK(item < a.total, "dtw item %lld total %lld", (long long)item, (long long)a.total);
                 if (beta > thr) {
-                    a.res[item] = kInf;  // pruned by the bound under the current threshold
+                    if constexpr (!WALK) a.res[item] = kInf;  // (WALK: pruned by its bound, nothing to record)
                 } else {
                     has = true;
                     ++n_started;
@@ -254,6 +314,8 @@ dtw_kernel(DtwArgs a, int ipw) {
         }
         if (!__any_sync(0xffffffffu, has) && cursor >= a1) break;
 
+        bool has_res = false;
+        float res_v = 0.f;
         if (has) {
             // ---- advance this lane's pair by up to 8 rows ----
             // x of this block was loaded with the previous block (or at setup); issue the
@@ -290,14 +352,16 @@ dtw_kernel(DtwArgs a, int ipw) {
                     for (int d = 0; d < NB; ++d)
                         if (d == w) r = B[d];
                 }
-                a.res[item] = WALK ? r : rootp<P>(r);
+                if constexpr (WALK) { has_res = r <= thr; res_v = r; }
+                else a.res[item] = rootp<P>(r);
                 has = false;
             } else if (band_min<WB>(B) + rest > thr) {
-                a.res[item] = kInf;  // early abandon (readings c15, c19)
-                ++n_abandon;
+                if constexpr (!WALK) a.res[item] = kInf;
+                ++n_abandon;  // early abandon (readings c15, c19)
                 has = false;
             }
         }
+        if constexpr (WALK) walk_results_warp(a, has_res, q, cand, res_v, lane);
     }
     if (a.cells) {
         unsigned long long cells = rows_done * (unsigned long long)(2 * w + 1);
@@ -375,7 +439,7 @@ __device__ __forceinline__ void four_rows(float (&B)[2 * WB + 2], const float (&
 template <int WB>
 struct Dtw4Cfg {
     static constexpr int NY = (2 * WB + 4 + 3) / 4 * 4;
-    static constexpr int SL = NY + 20;
+    static constexpr int SL = NY + 20;  // y window, x[0..7], U[0..3], L[0..3], 2 spare, (q, c)
     static constexpr size_t smem = (size_t)NT * SL * sizeof(float) +
                                    (size_t)(NT / 32) * kChunk4 * (sizeof(unsigned long long) + sizeof(int));
 };
@@ -422,7 +486,7 @@ dtw4_kernel(DtwArgs a) {
             cp_wait<0>();
             if (st == kPending) {
                 if (beta_n > thr_n) {
-                    a.res[item] = kInf;  // pruned by its bound under the current threshold
+                    if constexpr (!WALK) a.res[item] = kInf;  // (WALK: pruned by its bound)
                     st = kFree;
                 } else {
 #pragma unroll
@@ -491,9 +555,12 @@ dtw4_kernel(DtwArgs a) {
                     const unsigned long long key = ckey[item - cbeg];
                     qy = cq[item - cbeg];
                     c = (int64_t)(key & 0xffffffffu);
+                    // the pair's (query, candidate), read back at completion (smem: no registers)
+                    reinterpret_cast<int *>(slot)[SL - 2] = (int)qy;
+                    reinterpret_cast<uint32_t *>(slot)[SL - 1] = (uint32_t)c;
                     DCHECK(c < a.Ndb, "dtw4 key c=%lld q=%lld", (long long)c, (long long)qy);
                     beta_n = __uint_as_float((uint32_t)(key >> 32));
-                    thr_n = a.thr[qy];
+                    thr_n = *reinterpret_cast<volatile float *>(a.thr + qy);
                     if (casc) {
                         rest_n = __ldg(a.b1 + qy * a.ldb + c);  // +-beta1 = sum of all row terms (|.| later)
                         ur = a.Uq + qy * n;
@@ -552,6 +619,8 @@ dtw4_kernel(DtwArgs a) {
             continue;
         }
         // ---- (c) advance the active lanes by up to 8 rows ----
+        bool has_res = false;
+        float res_v = 0.f;
         if (st == kActive) {
             const int i0 = i;
             // prefetch x of the next 8-row step: the loads of a candidate row miss L1 and
@@ -622,13 +691,21 @@ dtw4_kernel(DtwArgs a) {
                     for (int d = 0; d < NB; ++d)
                         if (d == w) r = B[d];
                 }
-                a.res[item] = WALK ? r : rootp<P>(r);
+                if constexpr (WALK) { has_res = r <= thr; res_v = r; }
+                else a.res[item] = rootp<P>(r);
                 st = kFree;
-            } else if (band_min<WB>(B) + rest > thr) {
-                a.res[item] = kInf;  // early abandon (readings c15, c19)
-                ++n_abandon;
-                st = kFree;
+            } else {
+                if (band_min<WB>(B) + rest > thr) {
+                    if constexpr (!WALK) a.res[item] = kInf;
+                    ++n_abandon;  // early abandon (readings c15, c19)
+                    st = kFree;
+                }
             }
+        }
+        if constexpr (WALK) {
+            if (__any_sync(0xffffffffu, has_res))
+                walk_results_warp(a, has_res, reinterpret_cast<const int *>(slot)[SL - 2],
+                                  reinterpret_cast<const uint32_t *>(slot)[SL - 1], res_v, lane);
         }
     }
     if (a.cells) {
@@ -657,14 +734,17 @@ __global__ void dtw_generic_kernel(DtwArgs a, const float *__restrict__ yraw, fl
     const int n = a.n, w = a.w, nb = 2 * w + 1;
     const float *xr, *yr;
     float thr = kInf;
+    int lo = 0;
+    uint32_t cand = 0;
     if constexpr (WALK) {
-        int lo = 0, hi = a.Qb;
+        int hi = a.Qb;
         while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (a.item_off[mid] <= item) lo = mid; else hi = mid; }
         const int64_t j = a.pos[lo] + (item - a.item_off[lo]);
         const unsigned long long key = a.list[(int64_t)lo * a.cap + j];
+        cand = (uint32_t)(key & 0xffffffffu);
         const float beta = __uint_as_float((uint32_t)(key >> 32));
-        thr = a.thr[lo];
-        if (beta > thr) { a.res[item] = kInf; return; }
+        thr = *reinterpret_cast<volatile float *>(a.thr + lo);
+        if (beta > thr) return;
         xr = a.db + (int64_t)(key & 0xffffffffu) * n;
         yr = yraw + (int64_t)lo * n;
     } else {
@@ -685,9 +765,20 @@ __global__ void dtw_generic_kernel(DtwArgs a, const float *__restrict__ yraw, fl
             prev = v;
             rmin = fminf(rmin, v);
         }
-        if (rmin > thr) { a.res[item] = kInf; return; }
+        if (rmin > thr) {
+            if constexpr (!WALK) a.res[item] = kInf;
+            return;
+        }
     }
-    a.res[item] = WALK ? B[w] : rootp<P>(B[w]);
+    if constexpr (WALK) {
+        if (B[w] <= thr) {
+            const unsigned pos = atomicAdd(a.rcount, 1u);
+            a.rkey[pos] = pack_key(B[w], cand);
+            a.rq[pos] = lo;
+        }
+    } else {
+        a.res[item] = rootp<P>(B[w]);
+    }
 }
 
 template <int WB, int P, bool EXACT, bool WALK>
@@ -764,6 +855,12 @@ int launch_build_ysh(const float *y, int64_t rows, int n, float *ysh, int LP, cu
 
 // Generic path needs raw query rows and a scratch band; the caller passes them via
 // the globals below (set by launch_dtw_generic).
+int launch_topk_merge(const DtwArgs &a, cudaStream_t st) {
+    topk_merge_kernel<<<148, 256, 0, st>>>(a);
+    DTWLB_LAUNCH_CHECK();
+    return DTWLB_OK;
+}
+
 int launch_dtw(const DtwArgs &a, int p, bool walk, cudaStream_t st) {
     if (a.total == 0) return DTWLB_OK;
     if (p == 1) return walk ? launch_dtw_p<1, true>(a, st) : launch_dtw_p<1, false>(a, st);

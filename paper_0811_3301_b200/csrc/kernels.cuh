@@ -89,7 +89,7 @@ struct DtwArgs {
     const unsigned long long *list;  // [Qb][cap]
     int64_t cap;
     int Qb;
-    const float *thr;      // [Qb] tau^p (1+eps)
+    float *thr;            // [Qb] tau^p (1+eps); WALK: lowered by walk_result as the top-k fills
     int64_t total;         // number of items
     float *res;            // [total] DTW^p, +inf if pruned/abandoned (PAIRS: rooted)
     unsigned long long *cells;  // stats: computed cells (may be NULL)
@@ -101,7 +101,19 @@ struct DtwArgs {
     const float *b1;
     int64_t ldb;
     const float *Uq, *Lq;
+    // WALK: completed pairs are merged into the query's top-k (keys (DTW^p bits << 32 | c),
+    // ascending, [Qb][k]) under a per-query lock, and thr[q] follows the k-th key
+    unsigned long long *topk;
+    int *topk_lock;
+    int k;
+    float eps;
+    // WALK: completed pairs of the round (appended by the DTW kernels, merged by launch_topk_merge)
+    unsigned long long *rkey;   // [rcap] (DTW^p bits << 32 | c)
+    int *rq;                    // [rcap] query
+    unsigned *rcount;           // appended so far (reset before each round)
+    int64_t rcap;
 };
+int launch_topk_merge(const DtwArgs &a, cudaStream_t st);
 constexpr int kYPadL = 64;
 constexpr int kDtwIpw = 64;  // items per warp chunk of the DTW walk  // left padding of query rows (>= largest register band)
 int dtw_padded_len(int n);

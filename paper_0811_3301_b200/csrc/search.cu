@@ -179,15 +179,16 @@ struct QState {
     int *item_off;   // [Qb+1] first result slot of each query this round
     int *chunk_off;  // [Qb+1] first warp chunk of each query this round
     int *counters;   // [0] total items of the round, [1] total warp chunks
-    unsigned long long *topk;  // [Qb][k]
-    int *topk_n;
+    unsigned long long *topk;  // [Qb][k] keys (DTW^p bits, index), ascending; ~0 = empty
+    int *lock;                 // [Qb] top-k insertion locks (dtw.cu walk_result)
+    int *prev_cnt;             // [Qb] items of the query in the previous walk round
     unsigned long long *stat;  // [0] improved evals, [1] dtw items started, [2] cells, [3] abandoned
 };
 
 __global__ void init_state_kernel(QState s, int Qb, int k) {
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < Qb; q += gridDim.x * blockDim.x) {
         s.thr[q] = kInf;
-        s.topk_n[q] = 0;
+        s.lock[q] = 0;
         for (int j = 0; j < k; ++j) s.topk[(int64_t)q * k + j] = ~0ull;
     }
 }
@@ -204,6 +205,7 @@ __global__ void start_walk_kernel(QState s, int Qb) {
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < Qb; q += gridDim.x * blockDim.x) {
         s.pos[q] = 0;
         s.rnd[q] = 0;
+        s.prev_cnt[q] = 0;
         s.active[q] = s.len[q] > 0;
     }
 }
@@ -238,16 +240,35 @@ __device__ __forceinline__ int2 block_scan2(int2 v, int2 *warp_sums, int2 &total
     return v;
 }
 
-__global__ void __launch_bounds__(1024) plan_kernel(QState s, int Qb) {
+// The previous round's items are consumed first (the DTW kernel merged its results
+// into the top-k and tau directly): the walk advances past them and skips the rest of
+// a sorted run once its next bound exceeds tau (1+eps).
+__global__ void __launch_bounds__(1024) plan_kernel(QState s, int Qb, const unsigned long long *__restrict__ list,
+                                                    int64_t cap) {
     __shared__ int2 warp_sums[32];
     int2 carry = make_int2(0, 0);
     for (int base = 0; base < Qb; base += blockDim.x) {
         const int q = base + threadIdx.x;
         int cnt = 0;
         if (q < Qb && s.active[q]) {
-            int d = kD0 << min(s.rnd[q], 11);
-            d = min(d, kDMax);
-            cnt = min(d, s.len[q] - s.pos[q]);
+            int pos = s.pos[q] + s.prev_cnt[q];
+            const int len = s.len[q];
+            if (s.prev_cnt[q] > 0) {
+                s.rnd[q] += 1;
+                const float thr = *reinterpret_cast<volatile float *>(s.thr + q);
+                const unsigned long long *lq = list + (int64_t)q * cap;
+                while (pos < len && __uint_as_float((uint32_t)(lq[pos] >> 32)) > thr)
+                    pos = (pos / kRun + 1) * kRun;
+            }
+            s.pos[q] = pos;
+            if (pos < len) {
+                int d = kD0 << min(s.rnd[q], 11);
+                d = min(d, kDMax);
+                cnt = min(d, len - pos);
+            } else {
+                s.active[q] = 0;
+            }
+            s.prev_cnt[q] = cnt;
         }
         const int2 mine = make_int2(cnt, (cnt + kDtwIpw - 1) / kDtwIpw);
         int2 tot;
@@ -264,93 +285,6 @@ __global__ void __launch_bounds__(1024) plan_kernel(QState s, int Qb) {
         s.chunk_off[Qb] = carry.y;
         s.counters[0] = carry.x;
         s.counters[1] = carry.y;
-    }
-}
-
-// Merge a round's DTW results into each query's top-k (keys (DTW^p bits, index),
-// ascending); advance its walk.  One warp per query; for k <= 32 the list lives in
-// registers (lane r = rank r) and an insertion is one ballot + one shuffle.
-__global__ void merge_kernel(QState s, int Qb, int k, float eps, const unsigned long long *__restrict__ list,
-                             int64_t cap, const float *__restrict__ res) {
-    const int lane = threadIdx.x & 31;
-    const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (q >= Qb) return;
-    const int o0 = s.item_off[q], o1 = s.item_off[q + 1];
-    if (o0 == o1) return;
-    unsigned long long *tk = s.topk + (int64_t)q * k;
-    const unsigned long long *lq = list + (int64_t)q * cap;
-    const int p0 = s.pos[q];
-    int cnt;
-    unsigned long long kth;
-    if (k <= 32) {
-        unsigned long long mykey = lane < k ? tk[lane] : ~0ull;
-        kth = __shfl_sync(0xffffffffu, mykey, k - 1);
-        for (int b = o0; b < o1; b += 32) {
-            const int t = b + lane;
-            unsigned long long key = ~0ull;
-            if (t < o1) {
-                DCHECK(p0 + (t - o0) < s.len[q], "merge q=%d t=%d o0=%d p0=%d len=%d", q, t, o0, p0, s.len[q]);
-                const float d = res[t];
-                if (d < kInf) key = pack_key(d, (uint32_t)(lq[p0 + (t - o0)] & 0xffffffffu));
-            }
-            unsigned m = __ballot_sync(0xffffffffu, key < kth);
-            while (m) {
-                const int src = __ffs(m) - 1;
-                m &= m - 1;
-                const unsigned long long kk = __shfl_sync(0xffffffffu, key, src);
-                if (kk >= kth) continue;
-                const int at = __popc(__ballot_sync(0xffffffffu, lane < k && mykey < kk));
-                const unsigned long long up = __shfl_up_sync(0xffffffffu, mykey, 1);
-                if (lane < k) {
-                    if (lane > at) mykey = up;
-                    else if (lane == at) mykey = kk;
-                }
-                kth = __shfl_sync(0xffffffffu, mykey, k - 1);
-            }
-        }
-        if (lane < k) tk[lane] = mykey;
-        cnt = __popc(__ballot_sync(0xffffffffu, lane < k && mykey != ~0ull));
-    } else {
-        cnt = s.topk_n[q];
-        kth = tk[k - 1];
-        for (int b = o0; b < o1; b += 32) {
-            const int t = b + lane;
-            unsigned long long key = ~0ull;
-            if (t < o1) {
-                const float d = res[t];
-                if (d < kInf) key = pack_key(d, (uint32_t)(lq[p0 + (t - o0)] & 0xffffffffu));
-            }
-            unsigned m = __ballot_sync(0xffffffffu, key < kth);
-            while (m) {
-                const int src = __ffs(m) - 1;
-                m &= m - 1;
-                const unsigned long long kk = __shfl_sync(0xffffffffu, key, src);
-                if (kk >= kth) continue;  // kth may have tightened
-                if (lane == 0) {          // sorted insertion of kk, dropping the current k-th
-                    int j = min(cnt, k - 1);
-                    while (j > 0 && tk[j - 1] > kk) { tk[j] = tk[j - 1]; --j; }
-                    tk[j] = kk;
-                    cnt = min(cnt + 1, k);
-                }
-                cnt = __shfl_sync(0xffffffffu, cnt, 0);
-                __syncwarp();
-                kth = tk[k - 1];
-            }
-        }
-    }
-    if (lane == 0) {
-        s.topk_n[q] = cnt;
-        float thr = kInf;
-        if (cnt >= k) thr = __uint_as_float((uint32_t)(kth >> 32)) * (1.0f + eps);
-        s.thr[q] = thr;
-        // advance; skip the rest of a sorted run once its next bound exceeds thr
-        int pos = p0 + (o1 - o0);
-        const int len = s.len[q];
-        while (pos < len && __uint_as_float((uint32_t)(lq[pos] >> 32)) > thr)
-            pos = (pos / kRun + 1) * kRun;
-        s.pos[q] = pos;
-        s.rnd[q] += 1;
-        s.active[q] = pos < len;
     }
 }
 
@@ -503,10 +437,10 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     if (!keogh_only) DTWLB_TRY(launch_envelope(db, n, w, dbenv, dbenv + (size_t)N * n, N, st));
     tm.mark();  // 1
 
-    // ---- query block size from free memory: beta1 (4N) + list (8N) + res (4N) per query ----
+    // ---- query block size from free memory: gate bound (4N) + list (8N) per query ----
     size_t free_b = 0, total_b = 0;
     DTWLB_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const size_t per_q = (size_t)N * 16 + 4096;
+    const size_t per_q = (size_t)N * 12 + 4096;
     int64_t Qb = opts && opts->query_block > 0 ? opts->query_block : (int64_t)(free_b * 0.45 / per_q);
     Qb = std::max<int64_t>(1, std::min<int64_t>(Qb, Q));
     if (Qb >= 64) Qb = Qb / 64 * 64;
@@ -515,15 +449,15 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
 
     float *beta1;
     unsigned long long *list;
-    float *res;
     DTWLB_TRY(wsget(S_BETA1, (size_t)Qb * ldb, &beta1));
     DTWLB_TRY(wsget(S_LIST, (size_t)Qb * cap, &list));
-    const int64_t res_cap = std::min<int64_t>(Qb * cap, Qb * (int64_t)kDMax);
-    DTWLB_TRY(wsget(S_RES, (size_t)res_cap, &res));
+    const int64_t res_cap = std::min<int64_t>(Qb * cap, Qb * (int64_t)kDMax);  // items of one walk round
+    char *rbuf;  // completed pairs of a round: keys [res_cap] u64 + queries [res_cap] int
+    DTWLB_TRY(wsget(S_RES, (size_t)res_cap * 12 + 64, &rbuf));
     char *imp_scratch;
     DTWLB_TRY(wsget(S_MASK, improved_scratch_bytes(Qb, N), &imp_scratch));
     char *stb;
-    const size_t st_bytes = (size_t)Qb * 4 * (8 + kMaxRanges) + (Qb + 1) * 8 + 64 + 64 + 16 * 16;
+    const size_t st_bytes = (size_t)Qb * 4 * (10 + kMaxRanges) + (Qb + 1) * 8 + 64 + 64 + 16 * 16;
     DTWLB_TRY(wsget(S_STATE, st_bytes, &stb));
     QState s;
     {
@@ -539,13 +473,12 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         s.pos = reinterpret_cast<int *>(take(Qb * 4));
         s.rnd = reinterpret_cast<int *>(take(Qb * 4));
         s.active = reinterpret_cast<int *>(take(Qb * 4));
+        s.lock = reinterpret_cast<int *>(take(Qb * 4));
+        s.prev_cnt = reinterpret_cast<int *>(take(Qb * 4));
         s.item_off = reinterpret_cast<int *>(take((Qb + 1) * 4));
         s.chunk_off = reinterpret_cast<int *>(take((Qb + 1) * 4));
     }
     DTWLB_TRY(wsget(S_TOPK, (size_t)Qb * k, &s.topk));
-    int *topk_n;
-    DTWLB_TRY(wsget(S_TMP, (size_t)Qb + 64, &topk_n));
-    s.topk_n = topk_n;
     float *scratch = nullptr;
     if (generic_dtw) DTWLB_TRY(wsget(S_SCRATCH, (size_t)res_cap * (2 * w + 2), &scratch));
     DTWLB_CUDA(cudaMemsetAsync(s.stat, 0, 8 * 8, st));
@@ -657,7 +590,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
             DTWLB_LAUNCH_CHECK();
             for (int round = 0;; ++round) {
                 ++walk_rounds;
-                plan_kernel<<<1, 1024, 0, st>>>(s, (int)qn);
+                plan_kernel<<<1, 1024, 0, st>>>(s, (int)qn, list, cap);
                 DTWLB_LAUNCH_CHECK();
                 int tot2[2] = {0, 0};
                 DTWLB_CUDA(cudaMemcpyAsync(tot2, s.counters, sizeof(tot2), cudaMemcpyDeviceToHost, st));
@@ -680,8 +613,16 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 da.cap = cap;
                 da.Qb = (int)qn;
                 da.thr = s.thr;
+                da.topk = s.topk;
+                da.topk_lock = s.lock;
+                da.k = k;
+                da.eps = eps;
+                da.rkey = reinterpret_cast<unsigned long long *>(rbuf);
+                da.rq = reinterpret_cast<int *>(rbuf + (size_t)res_cap * 8);
+                da.rcount = reinterpret_cast<unsigned *>(s.counters + 6);
+                da.rcap = res_cap;
+                DTWLB_CUDA(cudaMemsetAsync(da.rcount, 0, sizeof(unsigned), st));
                 da.total = total;
-                da.res = res;
                 da.cells = s.stat + 2;
                 da.abandoned = s.stat + 3;
                 da.started = s.stat + 1;
@@ -697,8 +638,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                     da.ysh = ysh + qb0 * LP;
                     DTWLB_TRY(launch_dtw(da, p, true, st));
                 }
-                merge_kernel<<<(unsigned)ceil_div(qn * 32, 256), 256, 0, st>>>(s, (int)qn, k, eps, list, cap, res);
-                DTWLB_LAUNCH_CHECK();
+                DTWLB_TRY(launch_topk_merge(da, st));  // a6: the round's completed pairs -> top-k, tau
             }
             if (stats) {
                 cudaEventRecord(ev[2], st);
