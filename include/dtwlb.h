@@ -105,7 +105,16 @@ typedef struct nn_opts {
                               DTWLB_NO_PREFILTER: LB_Keogh over every pair (Alg. 3
                               literally) instead of the piecewise-sum pre-filter;
                               DTWLB_NO_CASCADE: see below                           */
-    int32_t reserved[4];
+    /* Database-sharded search: called once per query block after the
+     * first (best-first) range, with thr = DEVICE pointer to the block's count
+     * thresholds tau_q^p (1+eps) (+inf until k results), stream-ordered on `stream`.
+     * The callee may lower them in place, e.g. to the minimum over all shards
+     * (an all-reduce MIN): a shard's k-th best is >= the global k-th best, so any
+     * shard's threshold is safe for every shard.  All ranks must use the same
+     * query_block so that the calls match.  NULL = no exchange. */
+    void (*exchange)(float *thr, int64_t count, void *user);
+    void *exchange_user;
+    int32_t reserved[2];
 } nn_opts;
 
 #define DTWLB_KEOGH_ONLY 1

@@ -29,9 +29,30 @@ class DtwlbError(RuntimeError):
         self.name = STATUS.get(status, str(status))
 
 
+EXCHANGE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p)
+
+
 class NnOpts(ctypes.Structure):
     _fields_ = [("eps", ctypes.c_float), ("index_base", ctypes.c_int64), ("query_block", ctypes.c_int32),
-                ("flags", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
+                ("flags", ctypes.c_int32), ("exchange", EXCHANGE_FN), ("exchange_user", ctypes.c_void_p),
+                ("reserved", ctypes.c_int32 * 2)]
+
+
+class _DeviceArray:
+    """__cuda_array_interface__ view of a library-owned float32 device array (no copy)."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f4", "data": (ptr, False),
+                                         "version": 3, "strides": None,
+                                         "stream": torch.cuda.current_stream().cuda_stream}
+
+
+def _exchange_callback(fn):
+    """Wrap fn(thr: torch.Tensor) (a float32 CUDA view of the block's thresholds, lowered
+    in place) as the C exchange callback of nn_opts."""
+    def cb(ptr, count, _user):
+        fn(torch.as_tensor(_DeviceArray(ptr, count), device=torch.device("cuda", torch.cuda.current_device())))
+    return EXCHANGE_FN(cb)
 
 
 class NnStats(ctypes.Structure):
@@ -153,8 +174,10 @@ def dtw_band(x: torch.Tensor, y: torch.Tensor, w: int, p: int) -> torch.Tensor:
     return out
 
 
-def _opts(eps, index_base, query_block, keogh_only, prefilter=True, cascade=True):
+def _opts(eps, index_base, query_block, keogh_only, prefilter=True, cascade=True, exchange=None):
     o = NnOpts()
+    if exchange is not None:
+        o.exchange = exchange
     o.eps = eps
     o.index_base = index_base
     o.query_block = query_block
@@ -164,13 +187,16 @@ def _opts(eps, index_base, query_block, keogh_only, prefilter=True, cascade=True
 
 def nn_search(queries, db, w: int, p: int, k: int, *, eps: float = 1e-3, index_base: int = 0,
               query_block: int = 0, keogh_only: bool = False, prefilter: bool = True, cascade: bool = True,
-              out=None,
+              exchange=None, out=None,
               return_stats: bool = False):
     """Exact k-NN under banded DTW_p.  Returns (idx int64 [Q][k], dist float32 [Q][k]).
 
     queries/db may be CUDA tensors (device path) or host tensors / numpy arrays
     (pinned host path: the library stages them; outputs are then host tensors).
-    ``out`` optionally supplies (idx, dist) output tensors.
+    ``out`` optionally supplies (idx, dist) output tensors.  ``exchange(thr)`` (sharded
+    search) is called once per query block after the first range with a float32 CUDA view
+    of the block's thresholds, which it may lower in place (e.g. all-reduce MIN across
+    shards; every rank must then pass the same ``query_block``).
     """
     host = not (isinstance(queries, torch.Tensor) and queries.is_cuda)
     if host:
@@ -188,7 +214,8 @@ def nn_search(queries, db, w: int, p: int, k: int, *, eps: float = 1e-3, index_b
         dist = torch.empty((Q, k), dtype=torch.float32, device=dev, pin_memory=host)
     else:
         idx, dist = out
-    o = _opts(eps, index_base, query_block, keogh_only, prefilter, cascade)
+    cb = _exchange_callback(exchange) if exchange is not None else None  # kept alive for the call
+    o = _opts(eps, index_base, query_block, keogh_only, prefilter, cascade, cb)
     st = NnStats()
     _check(load().nn_search(queries.data_ptr(), Q, db.data_ptr(), N, n, w, p, k, idx.data_ptr(),
                             dist.data_ptr(), ctypes.byref(o), ctypes.byref(st) if return_stats else None,

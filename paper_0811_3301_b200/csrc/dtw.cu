@@ -116,6 +116,12 @@ __device__ __forceinline__ void load_x8(float (&xv)[8], const float *__restrict_
 // in some column j with |i-j| <= w, at cost |x_i - y_j|^p >= this term, so the sum of
 // the terms of the rows not yet computed bounds what the path still has to pay
 // (cascading abandon, reading c19).
+// +-beta1 of the pair (LB_Keogh^p; the survivor kernel stored -rd(beta1) as __half with the
+// pre-filter, the dense LB_Keogh pass +beta1 as float without it); callers take |.|
+__device__ __forceinline__ float b1_at(const DtwArgs &a, int64_t idx) {
+    return a.b1 ? __ldg(a.b1 + idx) : __half2float(a.b1h[idx]);
+}
+
 template <int P>
 __device__ __forceinline__ float row_lb(float x, float u, float l) {
     const float d = max3f(x - u, l - x, 0.f);
@@ -167,7 +173,9 @@ __device__ __forceinline__ void walk_result(const DtwArgs &a, int64_t q, unsigne
                 }
                 tk[j] = key;
                 const unsigned long long kth = tk[a.k - 1];
-                if (kth != ~0ull) *thr = __uint_as_float((uint32_t)(kth >> 32)) * (1.0f + a.eps);
+                // thresholds only decrease (a shard exchange may have lowered thr below
+                // this shard's own k-th best)
+                if (kth != ~0ull) *thr = fminf(*thr, __uint_as_float((uint32_t)(kth >> 32)) * (1.0f + a.eps));
             }
             __threadfence();
             atomicExch(lock, 0);
@@ -260,7 +268,7 @@ dtw_kernel(DtwArgs a, int ipw) {
     float B[NB + 1];
     float xv[8];  // x of the current 8-row block
     // cascading abandon: rest = LB_Keogh^p terms of the rows not yet computed
-    const bool casc = WALK && a.b1 != nullptr;
+    const bool casc = WALK && (a.b1 != nullptr || a.b1h != nullptr);
     float rest = 0.f;
     const float *ur = nullptr, *lr = nullptr;
     unsigned long long rows_done = 0, n_abandon = 0, n_started = 0;
@@ -287,7 +295,7 @@ dtw_kernel(DtwArgs a, int ipw) {
                     xr = a.db + (int64_t)c * n;
                     yb = yq;
                     if (casc) {
-                        rest = fabsf(__ldg(a.b1 + (int64_t)q * a.ldb + c));  // beta1 = sum of all row terms
+                        rest = fabsf(b1_at(a, (int64_t)q * a.ldb + c));  // beta1 = sum of all row terms
                         ur = a.Uq + (int64_t)q * n;
                         lr = a.Lq + (int64_t)q * n;
                     }
@@ -474,7 +482,7 @@ dtw4_kernel(DtwArgs a) {
     float B[NB + 1], Y[NY];
     float xv[8];  // x of rows i .. i+7 (loaded one 8-row step ahead)
     // cascading abandon: rest = LB_Keogh^p terms of the rows not yet computed
-    const bool casc = WALK && a.b1 != nullptr;
+    const bool casc = WALK && (a.b1 != nullptr || a.b1h != nullptr);
     float rest = 0.f, rest_n = 0.f;
     const float *ur = nullptr, *lr = nullptr;
     float uc[4], lc[4];  // U(y), L(y) of the current 4-row block (loaded one block ahead)
@@ -562,7 +570,7 @@ dtw4_kernel(DtwArgs a) {
                     beta_n = __uint_as_float((uint32_t)(key >> 32));
                     thr_n = *reinterpret_cast<volatile float *>(a.thr + qy);
                     if (casc) {
-                        rest_n = __ldg(a.b1 + qy * a.ldb + c);  // +-beta1 = sum of all row terms (|.| later)
+                        rest_n = b1_at(a, qy * a.ldb + c);  // +-beta1 = sum of all row terms (|.| later)
                         ur = a.Uq + qy * n;
                         lr = a.Lq + qy * n;
                     }

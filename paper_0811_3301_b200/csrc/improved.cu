@@ -52,43 +52,72 @@ int improved_epl(int n) {
 namespace {
 
 // ---------------------------------------------------------------- masks
-// One warp per (query, group of 8 consecutive 64-candidate tiles).
-constexpr int kTilesPerWarp = 8;
+// One warp per (64-candidate tile, block of 32 queries): lane l reads candidates 2l and
+// 2l + 1 of the tile (one 8-byte / 4-byte vector per lane: the tile's row of a query in
+// one 256 / 128-byte access) for each query in turn; two ballots (even / odd candidates)
+// are bit-interleaved into the query's 64-bit survivor mask, lane j keeps query j's
+// mask, and the non-empty ones are appended to the tile's list with ONE atomic per warp.
+__device__ __forceinline__ float2 gate_pair(const float *g, int64_t i) {
+    return __ldg(reinterpret_cast<const float2 *>(g + i));
+}
+__device__ __forceinline__ float2 gate_pair(const __half *g, int64_t i) {
+    return __half22float2(*reinterpret_cast<const __half2 *>(g + i));
+}
+// bit k of x -> bit 2k of the result
+__device__ __forceinline__ unsigned long long spread_bits(unsigned x) {
+    unsigned long long v = x;
+    v = (v | (v << 16)) & 0x0000FFFF0000FFFFull;
+    v = (v | (v << 8)) & 0x00FF00FF00FF00FFull;
+    v = (v | (v << 4)) & 0x0F0F0F0F0F0F0F0Full;
+    v = (v | (v << 2)) & 0x3333333333333333ull;
+    v = (v | (v << 1)) & 0x5555555555555555ull;
+    return v;
+}
+
+template <typename T>
 __global__ void __launch_bounds__(256)
-select_mask_kernel(const float *__restrict__ gate, int64_t ldb, int64_t Qb, int64_t N,
+select_mask_kernel(const T *__restrict__ gate, int64_t ldb, int64_t Qb, int64_t N,
                    const float *__restrict__ lo, const float *__restrict__ hi, const float *__restrict__ thr,
                    bool all, unsigned long long *__restrict__ tile_m, int *__restrict__ tile_q,
                    int *__restrict__ tile_cnt, int64_t ntiles) {
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t groups = (ntiles + kTilesPerWarp - 1) / kTilesPerWarp;
-    const int64_t q = gw / groups;
-    if (q >= Qb) return;
-    const int64_t t0 = (gw - q * groups) * kTilesPerWarp;
-    const float l = all ? -kInf : (lo ? lo[q] : -kInf);
-    float h = all ? kInf : (hi ? hi[q] : kInf);
-    if (!all && thr) h = fminf(h, thr[q]);
-    const float *row = gate + q * ldb;
-    float v[2 * kTilesPerWarp];
-#pragma unroll
-    for (int t = 0; t < kTilesPerWarp; ++t) {
-        const int64_t c = (t0 + t) * 64 + lane;
-        v[2 * t] = c < N ? __ldg(row + c) : kInf;
-        v[2 * t + 1] = c + 32 < N ? __ldg(row + c + 32) : kInf;
+    const int64_t tt = gw % ntiles;   // tile
+    const int64_t qb = gw / ntiles;   // block of 32 queries
+    const int64_t q0 = qb * 32;
+    if (q0 >= Qb) return;
+    const int nq = Qb - q0 < 32 ? (int)(Qb - q0) : 32;
+    // this lane's query bounds (query q0 + lane), broadcast per iteration
+    float my_l = -kInf, my_h = kInf;
+    if (!all && lane < nq) {
+        if (lo) my_l = lo[q0 + lane];
+        if (hi) my_h = hi[q0 + lane];
+        if (thr) my_h = fminf(my_h, thr[q0 + lane]);
     }
-#pragma unroll
-    for (int t = 0; t < kTilesPerWarp; ++t) {
-        const int64_t c = (t0 + t) * 64 + lane;
-        // (test c < N explicitly: the +inf padding must not pass a range whose hi is +inf)
-        const unsigned m0 = __ballot_sync(0xffffffffu, c < N && v[2 * t] > l && v[2 * t] <= h);
-        const unsigned m1 = __ballot_sync(0xffffffffu, c + 32 < N && v[2 * t + 1] > l && v[2 * t + 1] <= h);
-        const unsigned long long m = ((unsigned long long)m1 << 32) | m0;
-        if (lane == t && t0 + t < ntiles && m) {  // append (q, mask) to the tile's list
-            const int64_t tt = t0 + t;
-            const int pos = atomicAdd(tile_cnt + tt, 1);
-            tile_q[tt * Qb + pos] = (int)q;
-            tile_m[tt * Qb + pos] = m;
-        }
+    const int64_t c0 = tt * 64 + 2 * lane;  // candidates c0, c0 + 1 (ldb is a multiple of 4)
+    const bool ok0 = c0 < N, ok1 = c0 + 1 < N;
+    unsigned my_e = 0, my_o = 0;  // even / odd candidate ballots of query q0 + lane
+#pragma unroll 8
+    for (int j = 0; j < nq; ++j) {
+        const T *row = gate + (q0 + j) * ldb;
+        float2 v = make_float2(kInf, kInf);
+        if (ok0) v = gate_pair(row, c0);  // c0 + 1 <= ldb - 1: in the padded row
+        const float l = __shfl_sync(0xffffffffu, my_l, j), h = __shfl_sync(0xffffffffu, my_h, j);
+        // (test c < N explicitly: the +inf / padding must not pass a range whose hi is +inf)
+        const unsigned me = __ballot_sync(0xffffffffu, ok0 && v.x > l && v.x <= h);
+        const unsigned mo = __ballot_sync(0xffffffffu, ok1 && v.y > l && v.y <= h);
+        if (lane == j) { my_e = me; my_o = mo; }
+    }
+    const unsigned long long my_m = spread_bits(my_e) | (spread_bits(my_o) << 1);
+    const unsigned has = __ballot_sync(0xffffffffu, my_m != 0);
+    if (!has) return;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(tile_cnt + tt, __popc(has));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (my_m) {
+        const int pos = base + __popc(has & ((1u << lane) - 1u));
+        tile_q[tt * Qb + pos] = (int)(q0 + lane);
+        tile_m[tt * Qb + pos] = my_m;
     }
 }
 
@@ -124,7 +153,7 @@ __device__ __forceinline__ void load_p1(QRegs<EPL / 4, B1X, KO> &r, const Improv
             r.l[v] = __ldg(reinterpret_cast<const float4 *>(lr + e));
         }
     } else {
-        const float *b = a.gate + q * a.ldb + c0t;
+        const float *b = static_cast<const float *>(a.gate) + q * a.ldb + c0t;  // float when !B1X
         const int64_t rem = a.N - c0t;
         r.b1a = lane < rem ? __ldg(b + lane) : kInf;
         r.b1b = lane + 32 < rem ? __ldg(b + lane + 32) : kInf;
@@ -259,6 +288,7 @@ __device__ __forceinline__ float p2_group(const float *sU, const float *sL, cons
             const int off = li[u] * NPAD + 4 * lane + 128 * v;
             const float4 ux = *reinterpret_cast<const float4 *>(sU + off);
             const float4 lx = *reinterpret_cast<const float4 *>(sL + off);
+            // d = max(y - max(Ux, LU), min(Lx, UL) - y, 0)
             float t = s[u];
             t = accp<P>(t, max3f(y.x - fmaxf(ux.x, lu.x), fminf(lx.x, ul.x) - y.x, 0.f));
             t = accp<P>(t, max3f(y.y - fmaxf(ux.y, lu.y), fminf(lx.y, ul.y) - y.y, 0.f));
@@ -305,7 +335,7 @@ __device__ __forceinline__ void append_keys(const ImprovedArgs &a, int64_t q, bo
 }
 
 template <int P, int EPL, bool B1X, bool KO, bool DENSE>
-__global__ void __launch_bounds__(ImpCfg<EPL, B1X>::NT)
+__global__ void __launch_bounds__(ImpCfg<EPL, B1X>::NT, 1)
 improved_kernel(ImprovedArgs a, int Ct) {
     constexpr int NT = ImpCfg<EPL, B1X>::NT;
     constexpr bool PREFETCH = ImpCfg<EPL, B1X>::PREFETCH;
@@ -356,25 +386,45 @@ improved_kernel(ImprovedArgs a, int Ct) {
     const int u_me = lane >> 3;  // survivor slot this lane ends up holding after reduce4
     const bool lead8 = (lane & 7) == 0;
     const unsigned lt = (1u << lane) - 1u;
-    int e = warp;
+    // this warp's entries are e = warp, warp + NW, ...; with several CTAs per 64-tile
+    // (Ct < 64) an entry may have no survivor in this CTA's part: seek skips those 32
+    // entries at a time (one coalesced read of their masks, one ballot)
+    auto seek = [&](int e0, unsigned long long &m) -> int {
+        if (subs == 1) {  // one CTA per 64-tile: every listed entry has survivors here
+            if (e0 < cnt) m = em[e0];
+            return e0 < cnt ? e0 : cnt;
+        }
+        while (e0 < cnt) {
+            const int ee = e0 + NW * lane;
+            const unsigned long long mm = ee < cnt ? (em[ee] >> (sub * Ct)) & ctmask : 0ull;
+            const unsigned bal = __ballot_sync(0xffffffffu, mm != 0ull);
+            if (bal) {
+                const int src = __ffs(bal) - 1;
+                m = __shfl_sync(0xffffffffu, mm, src);
+                return e0 + NW * src;
+            }
+            e0 += NW * 32;
+        }
+        return cnt;
+    };
+    unsigned long long mcur = 0;
+    int e = seek(warp, mcur);
     if (e >= cnt) return;
     QRegs<NV, B1X, KO> cur, nxt;
     int64_t qe = eq[e];
-    unsigned long long mcur = (em[e] >> (sub * Ct)) & ctmask;
     load_p1<EPL, B1X, KO>(cur, a, qe, c0t, lane);
     while (true) {
-        const int en = e + NW;
+        unsigned long long mn = 0;
+        const int en = seek(e + NW, mn);
         const bool more = en < cnt;
         int64_t qn = 0;
-        unsigned long long mn = 0;
         if (more) {
             qn = eq[en];
-            mn = (em[en] >> (sub * Ct)) & ctmask;
             if constexpr (PREFETCH) load_p1<EPL, B1X, KO>(nxt, a, qn, c0t, lane);
         }
         if (PREFETCH && mcur) load_p2<EPL, B1X, KO>(cur, a, qe, lane);  // in flight during phase 1
         const int64_t q = qe;
-        float *gq = a.gate_w ? a.gate_w + q * a.ldb + c0 : nullptr;
+        __half *gq = a.gate_w ? a.gate_w + q * a.ldb + c0 : nullptr;
         // ---------------- phase 1: beta1 (B1X) of the gate survivors -> phase-2 list
         // groups of 4 survivors; a tail of 1 or 2 runs as a 1- or 2-wide group (lane l then
         // holds slot l >> 5-log2(W)), so few slots are spent on padding
@@ -396,7 +446,7 @@ improved_kernel(ImprovedArgs a, int Ct) {
                     // keep beta1 for the DTW walk's cascading abandon: the gate slot (beta0,
                     // already consumed by this range's mask) takes -beta1 (<= 0, so no later
                     // range re-selects it; the walk reads |.|)
-                    if (pass) gq[myl] = -b1;
+                    if (pass) gq[myl] = __hneg(__float2half_rd(b1));
                 }
                 if constexpr (KO) {
                     if constexpr (DENSE) {
@@ -563,9 +613,15 @@ int launch_improved(const ImprovedArgs &a, int p, bool keogh_only, bool dense, c
     const int64_t ntiles = ceil_div(a.N, 64);
     {   // per-tile (query, survivor mask) lists into the caller-provided scratch
         DTWLB_CUDA(cudaMemsetAsync(a.tile_cnt, 0, sizeof(int) * ntiles, st));
-        const int64_t warps = ceil_div(ntiles, kTilesPerWarp) * a.Qb;
-        select_mask_kernel<<<(unsigned)ceil_div(warps * 32, 256), 256, 0, st>>>(
-            a.gate, a.ldb, a.Qb, a.N, a.lo, a.hi, a.thr, dense, a.tile_m, a.tile_q, a.tile_cnt, ntiles);
+        const int64_t warps = ntiles * ceil_div(a.Qb, 32);
+        if (a.gate_half)
+            select_mask_kernel<__half><<<(unsigned)ceil_div(warps * 32, 256), 256, 0, st>>>(
+                static_cast<const __half *>(a.gate), a.ldb, a.Qb, a.N, a.lo, a.hi, a.thr, dense, a.tile_m, a.tile_q,
+                a.tile_cnt, ntiles);
+        else
+            select_mask_kernel<float><<<(unsigned)ceil_div(warps * 32, 256), 256, 0, st>>>(
+                static_cast<const float *>(a.gate), a.ldb, a.Qb, a.N, a.lo, a.hi, a.thr, dense, a.tile_m, a.tile_q,
+                a.tile_cnt, ntiles);
         DTWLB_LAUNCH_CHECK();
     }
     const int epl = a.npadE / 32;

@@ -22,6 +22,8 @@
 // segment sums (PAA = true): D = n/8 "samples" per row, directed rounding.
 #include <cstdlib>
 
+#include <cuda_fp16.h>
+
 #include "kernels.cuh"
 
 namespace dtwlb {
@@ -68,6 +70,28 @@ __device__ __forceinline__ void stage_rows(float (*S)[KP], const float *__restri
 // PAA = true:  piecewise-sum bound over segment sums with directed rounding:
 //   d = max(Xlo - Uhi, Llo - Xhi, 0) (rounded down), acc += d^p (rounded down), so the
 //   result never exceeds the exact sum_j d(X_j, [L_j, U_j])^p; same 4 ops per element.
+// Two elements at once: the four subtractions are two packed FADD2 (sm_100 f32x2, per
+// component the same IEEE operation as FADD / FADD.RM), then FMNMX3 and the accumulation
+// per element: 3 issue slots per element instead of 4.
+template <int P, bool PAA>
+__device__ __forceinline__ float lb_elem2(float acc, float2 xl, float2 xh, float2 u, float2 l) {
+    float2 a, b;
+    if constexpr (PAA) {
+        a = __fadd2_rd(xl, make_float2(-u.x, -u.y));
+        b = __fadd2_rd(l, make_float2(-xh.x, -xh.y));
+    } else {
+        a = __fadd2_rn(xl, make_float2(-u.x, -u.y));
+        b = __fadd2_rn(l, make_float2(-xh.x, -xh.y));
+    }
+    const float d0 = max3f(a.x, b.x, 0.f), d1 = max3f(a.y, b.y, 0.f);
+    if constexpr (PAA) {
+        if constexpr (P == 1) return __fadd_rd(__fadd_rd(acc, d0), d1);
+        else return __fmaf_rd(d1, d1, __fmaf_rd(d0, d0, acc));
+    } else {
+        return accp<P>(accp<P>(acc, d0), d1);
+    }
+}
+
 template <int P, bool PAA>
 __device__ __forceinline__ float lb_elem(float acc, float xl, float xh, float u, float l) {
     if constexpr (PAA) {
@@ -82,7 +106,7 @@ __device__ __forceinline__ float lb_elem(float acc, float xl, float xh, float u,
 template <int P, bool VEC, bool ROOTED, bool PAA>
 __global__ void __launch_bounds__(NT, 2)
 keogh_tile_kernel(const float *__restrict__ U, const float *__restrict__ L, const float *__restrict__ db,
-                  const float *__restrict__ db2, int64_t Q, int64_t N, int n, float *__restrict__ out,
+                  const float *__restrict__ db2, int64_t Q, int64_t N, int n, void *__restrict__ out,
                   int64_t ldo, int nqt) {
     extern __shared__ __align__(16) unsigned char smraw[];
     Stage<PAA> *st = reinterpret_cast<Stage<PAA> *>(smraw);
@@ -119,11 +143,16 @@ keogh_tile_kernel(const float *__restrict__ U, const float *__restrict__ L, cons
         cp_wait<1>();
         __syncthreads();
         const Stage<PAA> &s = st[ch & 1];
-        float part[4][8];
+        // LB_Keogh: per-chunk partial sums (two-level summation); PAA: accumulate directly
+        // (rounded down, so any order stays a lower bound; frees 32 registers for the
+        // packed subtractions)
+        float part[PAA ? 1 : 4][PAA ? 1 : 8];
+        if constexpr (!PAA) {
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+            for (int r = 0; r < 4; ++r)
 #pragma unroll
-            for (int j = 0; j < 8; ++j) part[r][j] = 0.f;
+                for (int j = 0; j < 8; ++j) part[r][j] = 0.f;
+        }
 
 #pragma unroll 2
         for (int k = 0; k < KC; k += 4) {
@@ -140,19 +169,30 @@ keogh_tile_kernel(const float *__restrict__ U, const float *__restrict__ L, cons
                 if constexpr (PAA) xw = *reinterpret_cast<const float4 *>(&s.X2[cg + 16 * j][k]);
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    float t = part[r][j];
-                    t = lb_elem<P, PAA>(t, xv.x, xw.x, uv[r].x, lv[r].x);
-                    t = lb_elem<P, PAA>(t, xv.y, xw.y, uv[r].y, lv[r].y);
-                    t = lb_elem<P, PAA>(t, xv.z, xw.z, uv[r].z, lv[r].z);
-                    t = lb_elem<P, PAA>(t, xv.w, xw.w, uv[r].w, lv[r].w);
-                    part[r][j] = t;
+                    if constexpr (PAA) {
+                        float t = acc[r][j];
+                        t = lb_elem2<P, PAA>(t, make_float2(xv.x, xv.y), make_float2(xw.x, xw.y),
+                                             make_float2(uv[r].x, uv[r].y), make_float2(lv[r].x, lv[r].y));
+                        t = lb_elem2<P, PAA>(t, make_float2(xv.z, xv.w), make_float2(xw.z, xw.w),
+                                             make_float2(uv[r].z, uv[r].w), make_float2(lv[r].z, lv[r].w));
+                        acc[r][j] = t;
+                    } else {
+                        float t = part[r][j];
+                        t = lb_elem<P, PAA>(t, xv.x, xw.x, uv[r].x, lv[r].x);
+                        t = lb_elem<P, PAA>(t, xv.y, xw.y, uv[r].y, lv[r].y);
+                        t = lb_elem<P, PAA>(t, xv.z, xw.z, uv[r].z, lv[r].z);
+                        t = lb_elem<P, PAA>(t, xv.w, xw.w, uv[r].w, lv[r].w);
+                        part[r][j] = t;
+                    }
                 }
             }
         }
+        if constexpr (!PAA) {
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+            for (int r = 0; r < 4; ++r)
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[r][j] = PAA ? __fadd_rd(acc[r][j], part[r][j]) : acc[r][j] + part[r][j];
+                for (int j = 0; j < 8; ++j) acc[r][j] += part[r][j];
+        }
         __syncthreads();
     }
 
@@ -172,14 +212,17 @@ keogh_tile_kernel(const float *__restrict__ U, const float *__restrict__ L, cons
             } else if constexpr (ROOTED) {
                 v = rootp<P>(v);
             }
-            out[q * ldo + c] = v;
+            if constexpr (PAA && !ROOTED)  // nn_search's gate block: fp16, rounded down (still a lower bound)
+                reinterpret_cast<__half *>(out)[q * ldo + c] = __float2half_rd(v);
+            else
+                reinterpret_cast<float *>(out)[q * ldo + c] = v;
         }
     }
 }
 
 template <int P, bool VEC, bool ROOTED, bool PAA>
 int launch_tile_t(const float *U, const float *L, const float *db, const float *db2, int64_t Q, int64_t N,
-                  int n, float *out, int64_t ldo, cudaStream_t st) {
+                  int n, void *out, int64_t ldo, cudaStream_t st) {
     const size_t smem = 2 * sizeof(Stage<PAA>);
     auto k = keogh_tile_kernel<P, VEC, ROOTED, PAA>;
     DTWLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -196,7 +239,7 @@ int launch_tile_t(const float *U, const float *L, const float *db, const float *
 
 template <bool PAA>
 int launch_tile(const float *U, const float *L, const float *db, const float *db2, int64_t Q, int64_t N, int n,
-                int p, bool rooted, float *out, int64_t ldo, cudaStream_t st) {
+                int p, bool rooted, void *out, int64_t ldo, cudaStream_t st) {
     if (Q == 0 || N == 0) return DTWLB_OK;
     const bool vec = (n % 4 == 0) && ((reinterpret_cast<uintptr_t>(U) | reinterpret_cast<uintptr_t>(L) |
                                        reinterpret_cast<uintptr_t>(db) | reinterpret_cast<uintptr_t>(db2)) %
@@ -266,7 +309,7 @@ int launch_paa_env_sums(const float *U, const float *L, int64_t count, int n, fl
 }
 
 int launch_paa_bound(const float *Uhi, const float *Llo, const float *Xlo, const float *Xhi, int64_t Q,
-                     int64_t N, int n, int p, bool rooted, float *out, int64_t ldo, cudaStream_t st) {
+                     int64_t N, int n, int p, bool rooted, void *out, int64_t ldo, cudaStream_t st) {
     return launch_tile<true>(Uhi, Llo, Xlo, Xhi, Q, N, paa_pitch(n), p, rooted, out, ldo, st);
 }
 

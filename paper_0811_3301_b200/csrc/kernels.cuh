@@ -3,6 +3,8 @@
 
 #include <algorithm>
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace dtwlb {
@@ -28,9 +30,10 @@ int launch_paa_sums(const float *x, int64_t count, int n, float *lo, float *hi, 
 int launch_paa_env_sums(const float *U, const float *L, int64_t count, int n, float *Uhi, float *Llo,
                         cudaStream_t st);
 // beta0[q][c] = sum_j d(X_c,j, [Llo_q,j, Uhi_q,j])^p * (p == 2 ? 1/s : 1), directed rounding
-// (a lower bound of LB_Keogh^p, hence of DTW_p^p); rooted if `rooted`.
+// (a lower bound of LB_Keogh^p, hence of DTW_p^p).  rooted: float out (C-ABI lb_piecewise);
+// else __half out rounded down (nn_search's gate block).
 int launch_paa_bound(const float *Uhi, const float *Llo, const float *Xlo, const float *Xhi, int64_t Q,
-                     int64_t N, int n, int p, bool rooted, float *out, int64_t ldo, cudaStream_t st);
+                     int64_t N, int n, int p, bool rooted, void *out, int64_t ldo, cudaStream_t st);
 
 // Arguments of the survivor passes (improved.cu).  Padded per-query arrays:
 //   yq, LUq, ULq: [Q][npadE] (npadE = 32 * epl), zero padded;
@@ -42,10 +45,11 @@ struct ImprovedArgs {
     const float *Ux, *Lx;         // [N][n]
     const float *xdb;             // [N][n]: if set, beta1 (LB_Keogh^p) is computed in-kernel
                                   // from x (pre-filtered cascade); else read from `gate`
-    const float *gate;            // [Qb][ldb] dense gate bound (beta0 = piecewise-sum bound,
-                                  // or beta1 = LB_Keogh^p when xdb == NULL)
-    float *gate_w;                // = gate (LIST mode with xdb): slots of the pairs whose beta1
-                                  // passed are overwritten with -beta1 (for the DTW walk)
+    const void *gate;             // [Qb][ldb] dense gate bound: beta0 = piecewise-sum bound as
+                                  // __half (xdb != NULL), or beta1 = LB_Keogh^p as float
+    bool gate_half;               // gate element type (__half iff the pre-filter runs)
+    __half *gate_w;               // = gate (LIST mode with xdb): slots of the pairs whose beta1
+                                  // passed are overwritten with -rd(beta1) (for the DTW walk)
     int64_t ldb;
     int64_t Qb, N;
     int n, npadE;
@@ -96,9 +100,11 @@ struct DtwArgs {
     unsigned long long *abandoned;  // stats (may be NULL)
     unsigned long long *started;    // stats: pairs whose DTW started (may be NULL)
     unsigned *queue;                 // work-queue counter (scratch, 4 bytes) for the w <= 32 kernel
-    // WALK, cascading abandon (may be NULL = off): |b1[q*ldb + c]| = LB_Keogh^p of the pair,
-    // Uq/Lq [Qb][n] the query envelopes; abandon once rowmin + (terms of rows left) > thr
+    // WALK, cascading abandon (b1 and b1h NULL = off): |b1[q*ldb + c]| (float) or |b1h[...]|
+    // (__half, rounded down) = LB_Keogh^p of the pair, Uq/Lq [Qb][n] the query envelopes;
+    // abandon once rowmin + (terms of rows left) > thr
     const float *b1;
+    const __half *b1h;
     int64_t ldb;
     const float *Uq, *Lq;
     // WALK: completed pairs are merged into the query's top-k (keys (DTW^p bits << 32 | c),

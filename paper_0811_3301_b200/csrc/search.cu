@@ -103,7 +103,11 @@ __global__ void pad_rows_kernel(const float *__restrict__ src, int64_t rows, int
 // ascending order (selection thresholds only -- correctness does not depend on them).
 constexpr int kSample = 2048;
 constexpr int kMaxRanges = 8;
-__global__ void __launch_bounds__(512) sample_threshold_kernel(const float *__restrict__ beta1, int64_t ldb,
+__device__ __forceinline__ float gate_at(const float *g, int64_t i) { return g[i]; }
+__device__ __forceinline__ float gate_at(const __half *g, int64_t i) { return __half2float(g[i]); }
+
+template <typename T>
+__global__ void __launch_bounds__(512) sample_threshold_kernel(const T *__restrict__ beta1, int64_t ldb,
                                                                int64_t N, int64_t S, int R, int G,
                                                                float *__restrict__ tS, int Qb) {
     __shared__ float v[kSample];
@@ -111,7 +115,7 @@ __global__ void __launch_bounds__(512) sample_threshold_kernel(const float *__re
     const int M = N < kSample ? (int)N : kSample;
     for (int s = threadIdx.x; s < kSample; s += blockDim.x) {
         int64_t c = (int64_t)s * N / M;
-        v[s] = s < M ? beta1[q * ldb + c] : kInf;
+        v[s] = s < M ? gate_at(beta1, q * ldb + c) : kInf;
     }
     __syncthreads();
     // bitonic sort of kSample floats
@@ -244,7 +248,7 @@ __device__ __forceinline__ int2 block_scan2(int2 v, int2 *warp_sums, int2 &total
 // into the top-k and tau directly): the walk advances past them and skips the rest of
 // a sorted run once its next bound exceeds tau (1+eps).
 __global__ void __launch_bounds__(1024) plan_kernel(QState s, int Qb, const unsigned long long *__restrict__ list,
-                                                    int64_t cap) {
+                                                    int64_t cap, bool sorted) {
     __shared__ int2 warp_sums[32];
     int2 carry = make_int2(0, 0);
     for (int base = 0; base < Qb; base += blockDim.x) {
@@ -253,7 +257,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(QState s, int Qb, const unsi
         if (q < Qb && s.active[q]) {
             int pos = s.pos[q] + s.prev_cnt[q];
             const int len = s.len[q];
-            if (s.prev_cnt[q] > 0) {
+            if (s.prev_cnt[q] > 0 && sorted) {
                 s.rnd[q] += 1;
                 const float thr = *reinterpret_cast<volatile float *>(s.thr + q);
                 const unsigned long long *lq = list + (int64_t)q * cap;
@@ -440,7 +444,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     // ---- query block size from free memory: gate bound (4N) + list (8N) per query ----
     size_t free_b = 0, total_b = 0;
     DTWLB_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const size_t per_q = (size_t)N * 12 + 4096;
+    const size_t per_q = (size_t)N * (prefilter ? 10 : 12) + 4096;  // gate (2 or 4 B) + list (8 B) per pair
     int64_t Qb = opts && opts->query_block > 0 ? opts->query_block : (int64_t)(free_b * 0.45 / per_q);
     Qb = std::max<int64_t>(1, std::min<int64_t>(Qb, Q));
     if (Qb >= 64) Qb = Qb / 64 * 64;
@@ -449,7 +453,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
 
     float *beta1;
     unsigned long long *list;
-    DTWLB_TRY(wsget(S_BETA1, (size_t)Qb * ldb, &beta1));
+    DTWLB_TRY(wsget(S_BETA1, (size_t)Qb * ldb, &beta1));  // float (or __half with the pre-filter)
     DTWLB_TRY(wsget(S_LIST, (size_t)Qb * cap, &list));
     const int64_t res_cap = std::min<int64_t>(Qb * cap, Qb * (int64_t)kDMax);  // items of one walk round
     char *rbuf;  // completed pairs of a round: keys [res_cap] u64 + queries [res_cap] int
@@ -513,7 +517,11 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         if (stats) cudaEventRecord(ev[1], st);
         init_state_kernel<<<(unsigned)ceil_div(qn, 256), 256, 0, st>>>(s, (int)qn, k);
         DTWLB_LAUNCH_CHECK();
-        sample_threshold_kernel<<<(unsigned)qn, 512, 0, st>>>(beta1, ldb, N, S, R, G, s.tS, (int)qn);
+        if (prefilter)
+            sample_threshold_kernel<__half><<<(unsigned)qn, 512, 0, st>>>(reinterpret_cast<const __half *>(beta1),
+                                                                         ldb, N, S, R, G, s.tS, (int)qn);
+        else
+            sample_threshold_kernel<float><<<(unsigned)qn, 512, 0, st>>>(beta1, ldb, N, S, R, G, s.tS, (int)qn);
         DTWLB_LAUNCH_CHECK();
         if (stats) {
             cudaEventRecord(ev[2], st);
@@ -539,7 +547,8 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                     ia.Uq = qpad + 3 * (size_t)Q * npadE + qb0 * npadE;
                     ia.Lq = qpad + 4 * (size_t)Q * npadE + qb0 * npadE;
                     ia.xdb = db;
-                    ia.gate_w = beta1;
+                    ia.gate_w = reinterpret_cast<__half *>(beta1);
+                    ia.gate_half = true;
                     ia.n_eval_keogh = s.stat + 4;
                 }
                 ia.Ux = dbenv;
@@ -576,7 +585,9 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
             run_idx.clear();
             for (int q = 0; q < qn; ++q)
                 for (int r = 0; r * kRun < h_len[q]; ++r) { run_q.push_back(q); run_idx.push_back(r); }
-            if (!run_q.empty()) {
+            static const bool nosort2 = [] { const char *e = getenv("DTWLB_NOSORT2"); return e && atoi(e); }();
+            const bool sorted = !(nosort2 && macro > 0);
+            if (!run_q.empty() && sorted) {
                 const size_t nr = run_q.size();
                 DTWLB_TRY(wsget(S_COUNT, nr * 2 + 64, &d_runs));
                 DTWLB_CUDA(cudaMemcpyAsync(d_runs, run_q.data(), nr * 4, cudaMemcpyHostToDevice, st));
@@ -590,7 +601,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
             DTWLB_LAUNCH_CHECK();
             for (int round = 0;; ++round) {
                 ++walk_rounds;
-                plan_kernel<<<1, 1024, 0, st>>>(s, (int)qn, list, cap);
+                plan_kernel<<<1, 1024, 0, st>>>(s, (int)qn, list, cap, sorted);
                 DTWLB_LAUNCH_CHECK();
                 int tot2[2] = {0, 0};
                 DTWLB_CUDA(cudaMemcpyAsync(tot2, s.counters, sizeof(tot2), cudaMemcpyDeviceToHost, st));
@@ -628,7 +639,8 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 da.started = s.stat + 1;
                 da.queue = reinterpret_cast<unsigned *>(s.counters + 4);
                 if (cascade) {  // cascading abandon with the pair's LB_Keogh row terms
-                    da.b1 = beta1;
+                    if (prefilter) da.b1h = reinterpret_cast<const __half *>(beta1);
+                    else da.b1 = beta1;
                     da.ldb = ldb;
                     da.Uq = U + qb0 * n;
                     da.Lq = L + qb0 * n;
@@ -639,6 +651,11 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                     DTWLB_TRY(launch_dtw(da, p, true, st));
                 }
                 DTWLB_TRY(launch_topk_merge(da, st));  // a6: the round's completed pairs -> top-k, tau
+            }
+            if (opts && opts->exchange && macro + 1 < R) {
+                // a7: shard threshold exchange after the best-first range (stream-ordered)
+                opts->exchange(s.thr, qn, opts->exchange_user);
+                DTWLB_CUDA(cudaGetLastError());
             }
             if (stats) {
                 cudaEventRecord(ev[2], st);

@@ -2,11 +2,15 @@
 
 Rank r of G owns database rows [r*N//G, (r+1)*N//G); queries are replicated.
 Each rank runs the full cascade on its shard (``nn_search`` with
-``index_base`` = its first row), then the ranks exchange their [Q][k]
-(index, distance) lists with one NCCL all-gather and merge them (``nn_merge``:
-the k smallest by (distance, index) of the G*k entries).  A shard's local k-th
-best is >= the global k-th best, so every local prune is also globally safe,
-and the union of the shard lists contains the global k-NN.
+``index_base`` = its first row).  After each query block's first (best-first)
+range the ranks all-reduce (MIN) their per-query thresholds tau_q^p (1+eps)
+(``exchange``): a shard's local k-th best is >= the global k-th best, so the
+minimum over shards is a safe threshold for every shard and prunes each shard's
+second range as if it saw the whole database.  Finally the ranks exchange their
+[Q][k] (index, distance) lists with one NCCL all-gather and merge them
+(``nn_merge``: the k smallest by (distance, index) of the G*k entries).  No
+candidate of the global k-NN is ever pruned (its distance is <= every
+threshold), and the union of the shard lists contains the global k-NN.
 
 The search and merge callables are injectable so the protocol can be tested
 with ``gloo`` on CPU (tests/test_sharded_cpu.py); the product path uses the
@@ -25,10 +29,26 @@ def shard_range(N: int, world: int, rank: int):
     return rank * N // world, (rank + 1) * N // world
 
 
+def common_query_block(N_shard: int, group: Optional[dist.ProcessGroup] = None, device=None) -> int:
+    """Queries per pipeline block, identical on every rank (the threshold exchange is a
+    collective called once per block): the minimum over ranks of what each rank's free
+    device memory allows (~10 bytes per (query, candidate) pair, cf. nn_search)."""
+    if device is not None and device.type == "cuda":
+        free = torch.cuda.mem_get_info(device)[0]
+        qb = max(64, int(free * 0.4 / (max(1, N_shard) * 10 + 4096)) // 64 * 64)
+    else:
+        qb = 1 << 20
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        t = torch.tensor([qb], dtype=torch.int64, device=device if device is not None else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+        qb = int(t.item())
+    return qb
+
+
 def sharded_nn_search(queries: torch.Tensor, db_shard: torch.Tensor, shard_lo: int, w: int, p: int, k: int,
                       group: Optional[dist.ProcessGroup] = None,
                       search: Optional[Callable] = None, merge: Optional[Callable] = None,
-                      out_local=None, gather_bufs=None):
+                      out_local=None, gather_bufs=None, query_block: Optional[int] = None):
     """Global k-NN over the union of all ranks' shards; every rank gets the result.
 
     Shards with fewer than k rows contribute their whole shard padded with
@@ -42,14 +62,23 @@ def sharded_nn_search(queries: torch.Tensor, db_shard: torch.Tensor, shard_lo: i
     Q = queries.shape[0]
     dev = queries.device
     kk = min(k, db_shard.shape[0])
+    kw = {}
+    if world > 1:
+        # all ranks use the same blocking; thresholds are min-reduced after each block's first range
+        kw["query_block"] = query_block or common_query_block(db_shard.shape[0], group, dev)
+        kw["exchange"] = lambda thr: dist.all_reduce(thr, op=dist.ReduceOp.MIN, group=group)
     if kk > 0:
         if out_local is not None and kk == k:
-            idx, dst = search(queries, db_shard, w, p, k, index_base=shard_lo, out=out_local)
+            idx, dst = search(queries, db_shard, w, p, k, index_base=shard_lo, out=out_local, **kw)
         else:
-            idx, dst = search(queries, db_shard, w, p, kk, index_base=shard_lo)
+            idx, dst = search(queries, db_shard, w, p, kk, index_base=shard_lo, **kw)
     else:
         idx = torch.empty((Q, 0), dtype=torch.int64, device=dev)
         dst = torch.empty((Q, 0), dtype=torch.float32, device=dev)
+        if world > 1:  # an empty shard still takes part in every block's threshold exchange
+            qb = kw["query_block"]
+            for b0 in range(0, Q, qb):
+                kw["exchange"](torch.full((min(qb, Q - b0),), float("inf"), dtype=torch.float32, device=dev))
     if kk < k:  # pad to k
         pad_i = torch.full((Q, k - kk), -1, dtype=torch.int64, device=dev)
         pad_d = torch.full((Q, k - kk), float("inf"), dtype=torch.float32, device=dev)

@@ -139,6 +139,37 @@ def test_cascade_and_prefilter_switches(cuda_ok, name):
     assert st["dtw_evaluated"] <= st["improved_evaluated"] <= st["keogh_evaluated"] <= 24 * 6000
 
 
+def test_threshold_exchange_callback(cuda_ok):
+    """The sharded path's exchange hook (a7): called once per query block after the first
+    range with a CUDA view of the block's thresholds; lowering them to any value >= the
+    true k-th best (here: the global k-th best from the oracle, times 1+eps) keeps the
+    result exact, and an identity exchange changes nothing."""
+    from paper_0811_3301_b200 import nn_search
+    c = datagen.CONFIGS["C2p2"]
+    qs, db = datagen.make(c, Q=20, N=5000)
+    o_idx, o_dist, _ = oracle.nn_twopass(qs, db, c.w, c.p, 3 + EXTRA, threads=THREADS)
+    calls = []
+
+    def ident(thr):
+        calls.append(thr.numel())
+
+    a_idx, a_dist = nn_search(dev(qs), dev(db), c.w, c.p, 3, query_block=8, exchange=ident)
+    assert calls == [8, 8, 4]
+    tau = torch.tensor(o_dist[:, 2].astype(np.float64) ** c.p * (1 + 1e-3), dtype=torch.float32).cuda()
+    pos = [0]
+
+    def lower(thr):
+        n = thr.numel()
+        torch.minimum(thr, tau[pos[0]:pos[0] + n], out=thr)
+        pos[0] += n
+
+    b_idx, b_dist = nn_search(dev(qs), dev(db), c.w, c.p, 3, query_block=8, exchange=lower)
+    assert pos[0] == 20
+    assert_knn_match(a_idx.cpu().numpy(), a_dist.cpu().numpy(), o_idx, o_dist, 3)
+    assert np.array_equal(a_idx.cpu().numpy(), b_idx.cpu().numpy())
+    assert np.array_equal(a_dist.cpu().numpy(), b_dist.cpu().numpy())
+
+
 def test_host_buffers(cuda_ok):
     """e2e path: host (numpy) inputs and outputs through the same C-ABI call."""
     from paper_0811_3301_b200 import nn_search

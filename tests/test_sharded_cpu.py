@@ -26,9 +26,110 @@ def _free_port():
     return p
 
 
-def _oracle_search(queries, db, w, p, k, index_base=0, out=None):
+def _oracle_search(queries, db, w, p, k, index_base=0, out=None, **_):
     idx, dst = oracle.nn_brute(queries.numpy(), db.numpy(), w, p, k)
     return torch.from_numpy(idx + index_base), torch.from_numpy(dst.astype(np.float32))
+
+
+def _cascade_search(queries, db, w, p, k, index_base=0, out=None, query_block=None, exchange=None):
+    """CPU stand-in of nn_search's two-range protocol built from oracle primitives: per
+    query block, range 1 = the S candidates with the smallest LB_Keogh (exact DTW, local
+    top-k, tau); exchange(tau) may lower tau; range 2 = the other candidates whose
+    LB_Keogh <= tau (1+eps) with tau tightening as results arrive."""
+    qs, dbn = queries.numpy().astype(np.float64), db.numpy().astype(np.float64)
+    Q, N = qs.shape[0], dbn.shape[0]
+    eps = 1e-3
+    qb = query_block or Q
+    idx = np.full((Q, k), -1, dtype=np.int64)
+    dst = np.full((Q, k), np.inf)
+    for b0 in range(0, Q, qb):
+        rows = range(b0, min(Q, b0 + qb))
+        lbs = {q: np.array([oracle.lb_keogh(dbn[c], qs[q], w, p) ** p for c in range(N)]) for q in rows}
+        tops = {q: [] for q in rows}
+        thr = torch.full((len(rows),), float("inf"), dtype=torch.float32)
+        S = max(k, N // 4)
+
+        def visit(q, cands):
+            for c in cands:
+                if lbs[q][c] > thr[q - b0].item() * (1 + 1e-6):
+                    continue
+                d = oracle.dtw_pow(dbn[c], qs[q], w, p)
+                tops[q] = sorted(tops[q] + [(d, c)])[:k]
+                if len(tops[q]) == k:
+                    thr[q - b0] = min(thr[q - b0].item(), tops[q][-1][0] * (1 + eps))
+
+        for q in rows:
+            visit(q, np.argsort(lbs[q], kind="stable")[:S])
+        if exchange is not None:
+            exchange(thr)
+        for q in rows:
+            visit(q, np.argsort(lbs[q], kind="stable")[S:])
+            for r, (d, c) in enumerate(tops[q]):
+                idx[q, r] = c + index_base
+                dst[q, r] = d ** (1.0 / p)
+    return torch.from_numpy(idx), torch.from_numpy(dst.astype(np.float32))
+
+
+def _worker_exchange(rank, world, port, N, k, result_q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_0811_3301_b200.sharded import merge_reference, shard_range, sharded_nn_search
+        cfg = datagen.CONFIGS["C2p2"]
+        lo, hi = shard_range(N, world, rank)
+        qs, _ = datagen.make(cfg, Q=4, N=0)
+        qs = qs[:, :32].copy()
+        shard = datagen.series(cfg.family, hi - lo, cfg.n, cfg.seed, datagen.ROLE_DB, cfg.znorm, start=lo)[:, :32]
+        shard = np.ascontiguousarray(shard)
+        seen = []
+
+        def search(queries, db, w, p, kk, index_base=0, out=None, query_block=None, exchange=None):
+            def ex(t):
+                before = t.clone()
+                exchange(t)
+                seen.append((before.numpy().copy(), t.numpy().copy()))
+            return _cascade_search(queries, db, w, p, kk, index_base, out, query_block, ex)
+
+        idx, dst = sharded_nn_search(torch.from_numpy(qs), torch.from_numpy(shard), lo, 3, cfg.p, k,
+                                     search=search, merge=merge_reference, query_block=3)
+        result_q.put((rank, idx.numpy(), dst.numpy(), seen))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:
+        result_q.put((rank, None, repr(e), None))
+        raise
+
+
+def test_threshold_exchange_is_exact_and_tightens():
+    """After the first range each block's thresholds are min-reduced over the shards
+    (SURVEY 8(e) item 1); the merged result still equals the brute-force k-NN of the
+    whole database, and the exchange lowers at least one shard's thresholds."""
+    world, N, k = 2, 120, 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_exchange, args=(r, world, port, N, k, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    res.sort(key=lambda r: r[0])
+    for r in res:
+        assert r[1] is not None, r[2]
+    cfg = datagen.CONFIGS["C2p2"]
+    qs, db = datagen.make(cfg, Q=4, N=N)
+    o_idx, o_dst = oracle.nn_brute(np.ascontiguousarray(qs[:, :32]), np.ascontiguousarray(db[:, :32]), 3, cfg.p, k)
+    for rank, idx, dst, seen in res:
+        assert np.array_equal(idx, o_idx)
+        assert np.allclose(dst, o_dst, rtol=1e-6)
+        assert len(seen) == 2  # blocks of 3 queries: 4 queries -> 2 exchanges on every rank
+        for before, after in seen:
+            assert np.all(after <= before)
+    lowered = sum(int(np.any(a < b)) for _, _, _, seen in res for b, a in seen)
+    assert lowered >= 1
 
 
 def _worker(rank, world, port, N, k, result_q):
