@@ -120,8 +120,8 @@ int lb_piecewise(const float *q_env, const float *db, int64_t Q, int64_t N, int3
     cudaStream_t st = as_stream(stream);
     const int Dp = paa_pitch(n);
     float *xs, *qs;
-    DTWLB_TRY(ws_get_bytes(7, sizeof(float) * 2 * N * Dp, (void **)&xs));
-    DTWLB_TRY(ws_get_bytes(8, sizeof(float) * 2 * Q * Dp, (void **)&qs));
+    DTWLB_TRY(ws_get_bytes(8, sizeof(float) * 2 * N * Dp, (void **)&xs));
+    DTWLB_TRY(ws_get_bytes(9, sizeof(float) * 2 * Q * Dp, (void **)&qs));
     DTWLB_TRY(launch_paa_sums(db, N, n, xs, xs + N * Dp, st));
     DTWLB_TRY(launch_paa_env_sums(q_env, q_env + Q * n, Q, n, qs, qs + Q * Dp, st));
     DTWLB_TRY(launch_paa_bound(qs, qs + Q * Dp, xs, xs + N * Dp, Q, N, n, p, true, out, N, st));
@@ -192,7 +192,7 @@ int dtw_band(const float *x, const float *y, int32_t n, int32_t w, int32_t p, fl
     CHECK_ARG(n >= 1, "dtw_band: n = %d < 1", n);
     CHECK_ARG(w >= 0, "dtw_band: w = %d < 0", w);
     CHECK_ARG(count >= 0, "dtw_band: count < 0");
-    DTWLB_TRY(check_p(p));
+    if (p != 0) DTWLB_TRY(check_p(p));  // p = 0 encodes DTW_inf, dtw_band only
     if (count == 0) return DTWLB_OK;
     CHECK_ARG(x && y && out, "dtw_band: NULL pointer");
     DTWLB_TRY(require_device());

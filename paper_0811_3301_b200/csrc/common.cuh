@@ -80,8 +80,8 @@ __device__ __forceinline__ float accp(float acc, float d) {
 }
 template <int P>
 __device__ __forceinline__ float rootp(float v) {
-    if constexpr (P == 1) return v;
-    else return sqrtf(v);
+    if constexpr (P == 2) return sqrtf(v);
+    else return v;  // p = 1, and p = 0 (DTW_inf, a max: no root)
 }
 
 // (dist, idx) ordering key: non-negative float bits are monotone (reading c17: -0 -> +0).

@@ -32,6 +32,7 @@ constexpr int NT = 128;
 template <int P>
 __device__ __forceinline__ float cell(float m, float t) {
     if constexpr (P == 1) return m + fabsf(t);
+    else if constexpr (P == 0) return fmaxf(m, fabsf(t));  // DTW_inf: max, exact
     else return fmaf(t, t, m);
 }
 
@@ -871,6 +872,13 @@ int launch_topk_merge(const DtwArgs &a, cudaStream_t st) {
 
 int launch_dtw(const DtwArgs &a, int p, bool walk, cudaStream_t st) {
     if (a.total == 0) return DTWLB_OK;
+    if (p == 0) {  // DTW_inf: pairs mode only (dtw_band)
+        if (walk) {
+            set_error(DTWLB_EUNSUPPORTED, "nn_search: p = infinity unsupported");
+            return DTWLB_EUNSUPPORTED;
+        }
+        return launch_dtw_p<0, false>(a, st);
+    }
     if (p == 1) return walk ? launch_dtw_p<1, true>(a, st) : launch_dtw_p<1, false>(a, st);
     return walk ? launch_dtw_p<2, true>(a, st) : launch_dtw_p<2, false>(a, st);
 }
@@ -879,7 +887,13 @@ int launch_dtw_generic(const DtwArgs &a, const float *yraw, float *scratch, int 
                        cudaStream_t st) {
     if (a.total == 0) return DTWLB_OK;
     const int64_t grid = ceil_div(a.total, 128);
-    if (p == 1) {
+    if (p == 0) {
+        if (walk) {
+            set_error(DTWLB_EUNSUPPORTED, "nn_search: p = infinity unsupported");
+            return DTWLB_EUNSUPPORTED;
+        }
+        dtw_generic_kernel<0, false><<<(unsigned)grid, 128, 0, st>>>(a, yraw, scratch);
+    } else if (p == 1) {
         if (walk) dtw_generic_kernel<1, true><<<(unsigned)grid, 128, 0, st>>>(a, yraw, scratch);
         else dtw_generic_kernel<1, false><<<(unsigned)grid, 128, 0, st>>>(a, yraw, scratch);
     } else {

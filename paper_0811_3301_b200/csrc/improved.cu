@@ -124,7 +124,7 @@ select_mask_kernel(const T *__restrict__ gate, int64_t ldb, int64_t Qb, int64_t 
 // ---------------------------------------------------------------- survivor passes
 template <int EPL, bool B1X>
 struct ImpCfg {
-    static constexpr int NT = EPL <= 8 ? 512 : 256;
+    static constexpr int NT = EPL <= 8 ? 512 : (EPL == 16 ? 384 : 256);
     // prefetch the next entry's phase-1 query registers (U, L) while the current one is
     // evaluated, and issue the current entry's phase-2 loads (y, LU, UL) before its phase 1
     // (n <= 256; beyond that the extra query registers would spill)
@@ -390,10 +390,6 @@ improved_kernel(ImprovedArgs a, int Ct) {
     // (Ct < 64) an entry may have no survivor in this CTA's part: seek skips those 32
     // entries at a time (one coalesced read of their masks, one ballot)
     auto seek = [&](int e0, unsigned long long &m) -> int {
-        if (subs == 1) {  // one CTA per 64-tile: every listed entry has survivors here
-            if (e0 < cnt) m = em[e0];
-            return e0 < cnt ? e0 : cnt;
-        }
         while (e0 < cnt) {
             const int ee = e0 + NW * lane;
             const unsigned long long mm = ee < cnt ? (em[ee] >> (sub * Ct)) & ctmask : 0ull;
@@ -407,19 +403,29 @@ improved_kernel(ImprovedArgs a, int Ct) {
         }
         return cnt;
     };
+    // n <= 256: Ct = 64, one CTA per 64-tile and every listed entry has survivors here
+    constexpr bool ONE_CTA = NPAD * 64 <= 16384;
     unsigned long long mcur = 0;
-    int e = seek(warp, mcur);
-    if (e >= cnt) return;
+    int e = warp;
+    if (ONE_CTA || subs == 1) {
+        if (e >= cnt) return;
+        mcur = em[e];
+    } else {
+        e = seek(warp, mcur);
+        if (e >= cnt) return;
+    }
     QRegs<NV, B1X, KO> cur, nxt;
     int64_t qe = eq[e];
     load_p1<EPL, B1X, KO>(cur, a, qe, c0t, lane);
     while (true) {
         unsigned long long mn = 0;
-        const int en = seek(e + NW, mn);
+        int en = e + NW;
+        if (!ONE_CTA && subs != 1) en = seek(en, mn);
         const bool more = en < cnt;
         int64_t qn = 0;
         if (more) {
             qn = eq[en];
+            if (ONE_CTA || subs == 1) mn = em[en];
             if constexpr (PREFETCH) load_p1<EPL, B1X, KO>(nxt, a, qn, c0t, lane);
         }
         if (PREFETCH && mcur) load_p2<EPL, B1X, KO>(cur, a, qe, lane);  // in flight during phase 1

@@ -45,7 +45,9 @@ def test_argument_validation_precedes_device(lib):
     assert lib.lb_keogh(null, null, 1, 1, 8, 3, null, null) == 2          # p = 3 unsupported
     assert lib.lb_piecewise(null, null, 1, 1, 8, 3, null, null) == 2      # p = 3 unsupported
     assert lib.lb_piecewise(null, null, 1, 1, 0, 1, null, null) == 1      # n < 1
-    assert lib.dtw_band(null, null, 8, 2, 0, null, 1, null) == 2          # p = 0 (inf) unsupported on GPU
+    assert lib.dtw_band(null, null, 8, 2, 3, null, 1, null) == 2          # p = 3 unsupported
+    assert lib.dtw_band(null, null, 8, 2, 0, null, 1, null) == 1          # p = 0 (inf) ok, NULL pointers
+    assert lib.nn_search(null, 1, null, 4, 8, 1, 0, 1, null, null, None, None, null) == 2   # p = inf
     assert lib.nn_search(null, 1, null, 0, 8, 1, 1, 1, null, null, None, None, null) == 1   # N = 0
     assert lib.nn_search(null, 1, null, 4, 8, 1, 1, 5, null, null, None, None, null) == 1   # k > N
     assert lib.nn_search(null, 1, null, 4, 8, 1, 1, 0, null, null, None, None, null) == 1   # k < 1

@@ -151,6 +151,31 @@ def test_dtw_band_paper_values(cuda_ok):
     assert dtw_band(x, y, 0, 1).item() == pytest.approx(3.0)
 
 
+@pytest.mark.parametrize("n,w", [(1, 0), (4, 3), (9, 2), (128, 12), (256, 25), (257, 25), (512, 51), (300, 64),
+                                 (100, 99), (1000, 50)])
+def test_dtw_band_inf(cuda_ok, n, w):
+    """DTW_inf (p = 0 encodes p = infinity): a max of |x_i - y_j| along the best
+    path; the GPU rounds only |x_i - y_j| (exactly once), so it equals the fp64 oracle
+    rounded to fp32 bit for bit."""
+    from paper_0811_3301_b200 import dtw_band
+    count = 60
+    x, y = series(count, n), series(count, n)
+    x[0] = y[0]
+    out = dtw_band(dev(x), dev(y), w, 0).cpu().numpy()
+    ref = np.array([oracle.dtw(x[r], y[r], w, 0) for r in range(count)]).astype(np.float32)
+    assert np.array_equal(out, ref)
+    assert out[0] == 0.0
+
+
+def test_dtw_inf_paper_values(cuda_ok):
+    """P:983-984 (Appendix A): z = (7,7,7,0), y = (7,0,5,0), x = (7,0,1,0):
+    DTW_inf(z, y) = 5 and DTW_inf(z, x) = 1 (w >= 2)."""
+    from paper_0811_3301_b200 import dtw_band
+    z = dev([[7, 7, 7, 0], [7, 7, 7, 0]])
+    yx = dev([[7, 0, 5, 0], [7, 0, 1, 0]])
+    assert dtw_band(z, yx, 3, 0).cpu().numpy().tolist() == [5.0, 1.0]
+
+
 def test_bounds_strict_fixture(cuda_ok):
     """x=(4,0,3,2), y=(3,4,1,4), w=1: LB_Keogh^p 1, LB_Improved^p 2, DTW^p 5 (p=1) / 7 (p=2)."""
     from paper_0811_3301_b200 import dtw_band, lb_improved, lb_keogh
