@@ -275,13 +275,13 @@ __device__ __forceinline__ float p1_group(const float *sX, const int (&li)[8], c
 }
 
 // Phase-2 partial sums: beta2 = sum_i max(y_i - max(U(x)_i, LU_i), min(L(x)_i, UL_i) - y_i, 0)^p.
-template <int W, int P, int NV, int NPAD>
+template <int W, int P, int NV, int NPAD, int V0 = 0, int V1 = NV>
 __device__ __forceinline__ float p2_group(const float *sU, const float *sL, const int (&li)[8],
                                           const float4 (&yq)[NV], const float4 (&luq)[NV],
                                           const float4 (&ulq)[NV], int lane) {
     float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
+    for (int v = V0; v < V1; ++v) {
         const float4 y = yq[v], lu = luq[v], ul = ulq[v];
 #pragma unroll
         for (int u = 0; u < W; ++u) {
@@ -377,9 +377,10 @@ improved_kernel(ImprovedArgs a, int Ct) {
     }
     __syncthreads();
 
-    int *lst1 = sW + warp * 224;   // 72 ints
+    int *lst1 = sW + warp * 296;   // 72 ints (phase 1; reused for the phase-2b list)
     int *lst2 = lst1 + 72;         // 72 ints
     float *b1v = reinterpret_cast<float *>(lst2 + 72);  // 72 floats
+    float *b1w = b1v + 72;                              // 72 floats (phase 2a partial bounds)
     unsigned long long evals1 = 0, evals2 = 0;
     const int *eq = a.tile_q + tile * a.Qb;
     const unsigned long long *em = a.tile_m + tile * a.Qb;
@@ -484,7 +485,67 @@ improved_kernel(ImprovedArgs a, int Ct) {
             __syncwarp();
         }
         // ---------------- phase 2: beta2, LB_Improved^p = beta1 + beta2
-        if constexpr (!KO) {
+        // LIST mode, n > 128: in two halves.  2a: beta1 + beta2 over the first half of the
+        // samples (a lower bound of LB_Improved^p, so pruning on it is exact) for every
+        // phase-2 survivor; 2b: the second half only for the pairs 2a kept (~half of them
+        // fail already at 2a on C5: saves ~1/4 of the phase-2 work)
+        constexpr bool SPLIT = !DENSE && !KO && NV >= 2;
+        if constexpr (SPLIT) {
+            if (!PREFETCH && n2) load_p2<EPL, B1X, KO>(cur, a, q, lane);
+            evals2 += n2;
+            int n3 = 0;
+            auto phase2a = [&](auto wc, int g) {
+                constexpr int W = decltype(wc)::value;
+                constexpr int SH = W == 8 ? 2 : (W == 4 ? 3 : (W == 2 ? 4 : 5));
+                int li[8];
+                read_group<W>(lst2, g, li);
+                const float b2 = p2_group<W, P, NV, NPAD, 0, NV / 2>(sU, sL, li, cur.y, cur.lu, cur.ul, lane);
+                const int us = lane >> SH;
+                const int myl = W == 1 ? li[0] : lst2[g + us];
+                float b1;
+                if constexpr (B1X) {
+                    b1 = b1v[min(g + us, n2 - 1)];
+                } else {
+                    const int t64 = sub * Ct + myl;  // slot in the 64-tile
+                    const float va = __shfl_sync(0xffffffffu, cur.b1a, t64 & 31);
+                    const float vb = __shfl_sync(0xffffffffu, cur.b1b, t64 & 31);
+                    b1 = t64 < 32 ? va : vb;
+                }
+                const float part = b1 + b2;
+                const bool alive = (lane & ((1 << SH) - 1)) == 0 && g + us < n2 && part <= cur.thr;
+                const unsigned bal = __ballot_sync(0xffffffffu, alive);
+                if (alive) {
+                    const int pos = n3 + __popc(bal & lt);
+                    lst1[pos] = myl;
+                    b1w[pos] = part;
+                }
+                n3 += __popc(bal);
+            };
+            int g = 0;
+            for (; n2 - g >= 7; g += 8) phase2a(std::integral_constant<int, 8>{}, g);
+            for (; n2 - g >= 3; g += 4) phase2a(std::integral_constant<int, 4>{}, g);
+            if (n2 - g == 2) phase2a(std::integral_constant<int, 2>{}, g);
+            else if (n2 - g == 1) phase2a(std::integral_constant<int, 1>{}, g);
+            if (lane < ((8 - (n3 & 7)) & 7)) lst1[n3 + lane] = 0;
+            __syncwarp();
+            auto phase2b = [&](auto wc, int g) {
+                constexpr int W = decltype(wc)::value;
+                constexpr int SH = W == 8 ? 2 : (W == 4 ? 3 : (W == 2 ? 4 : 5));
+                int li[8];
+                read_group<W>(lst1, g, li);
+                const float b2 = p2_group<W, P, NV, NPAD, NV / 2, NV>(sU, sL, li, cur.y, cur.lu, cur.ul, lane);
+                const int us = lane >> SH;
+                const int myl = W == 1 ? li[0] : lst1[g + us];
+                const float beta = b1w[min(g + us, n3 - 1)] + b2;
+                const bool lead = (lane & ((1 << SH) - 1)) == 0 && g + us < n3;
+                append_keys(a, q, lead && beta <= cur.thr, beta, c0 + myl, lane);
+            };
+            g = 0;
+            for (; n3 - g >= 7; g += 8) phase2b(std::integral_constant<int, 8>{}, g);
+            for (; n3 - g >= 3; g += 4) phase2b(std::integral_constant<int, 4>{}, g);
+            if (n3 - g == 2) phase2b(std::integral_constant<int, 2>{}, g);
+            else if (n3 - g == 1) phase2b(std::integral_constant<int, 1>{}, g);
+        } else if constexpr (!KO) {
             if (!PREFETCH && n2) load_p2<EPL, B1X, KO>(cur, a, q, lane);
             evals2 += n2;
             auto phase2 = [&](auto wc, int g) {
@@ -566,7 +627,7 @@ int launch_imp_t(const ImprovedArgs &a, int64_t ntiles, cudaStream_t st) {
     const int arrays = (B1X ? 1 : 0) + (KO ? 0 : 2);
     // staged rows: at most 64 candidates and 192 KB (3 arrays) / 128 KB (2 arrays)
     const int Ct = std::min(64, 16384 / NPAD);
-    const size_t smem = (size_t)arrays * Ct * NPAD * sizeof(float) + (size_t)(NT / 32) * 224 * sizeof(int);
+    const size_t smem = (size_t)arrays * Ct * NPAD * sizeof(float) + (size_t)(NT / 32) * 296 * sizeof(int);
     auto k = improved_kernel<P, EPL, B1X, KO, DENSE>;
     DTWLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t grid = ntiles * (64 / Ct);
