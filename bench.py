@@ -207,6 +207,7 @@ def run_ours(args, cfg):
     stats_all = []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index) as clk:
+        time.sleep(0.5)  # let nvidia-smi start polling before the timed region (its start-up stalls the GPU)
         barrier()
         ev0.record(st)
         for _ in range(args.steps):

@@ -485,11 +485,12 @@ improved_kernel(ImprovedArgs a, int Ct) {
             __syncwarp();
         }
         // ---------------- phase 2: beta2, LB_Improved^p = beta1 + beta2
-        // LIST mode, n > 128: in two halves.  2a: beta1 + beta2 over the first half of the
+        // LIST mode, n > 256: in two halves.  2a: beta1 + beta2 over the first half of the
         // samples (a lower bound of LB_Improved^p, so pruning on it is exact) for every
         // phase-2 survivor; 2b: the second half only for the pairs 2a kept (~half of them
         // fail already at 2a on C5: saves ~1/4 of the phase-2 work)
-        constexpr bool SPLIT = !DENSE && !KO && NV >= 2;
+        // (n <= 256, NV = 2: the extra reduction per group costs more than it saves -- measured)
+        constexpr bool SPLIT = !DENSE && !KO && NV >= 4;
         if constexpr (SPLIT) {
             if (!PREFETCH && n2) load_p2<EPL, B1X, KO>(cur, a, q, lane);
             evals2 += n2;
