@@ -24,6 +24,8 @@
 #include <mutex>
 #include <vector>
 
+#include <cub/block/block_radix_sort.cuh>
+
 #include "kernels.cuh"
 
 namespace dtwlb {
@@ -145,34 +147,36 @@ __global__ void __launch_bounds__(512) sample_threshold_kernel(const T *__restri
     }
 }
 
-// Bitonic sort of runs of kRun u64 keys per query list (ascending (beta_lb, c)).
+// Sort runs of kRun keys of each query list by their bound (the walk's best-first order):
+// a block-wide LSD radix sort (CUB BlockRadixSort, in this kernel's shared memory) of the
+// 32-bit bound bits with the candidate index as payload; 512 threads x 8 keys = one run.
+// Non-negative float bits order like the floats; equal bounds keep their list order.
 constexpr int kRun = 4096;
-__global__ void __launch_bounds__(1024) sort_runs_kernel(unsigned long long *__restrict__ list, int64_t cap,
-                                                         const int *__restrict__ run_q,
-                                                         const int *__restrict__ run_idx,
-                                                         const int *__restrict__ len) {
-    __shared__ unsigned long long v[kRun];
+constexpr int kSortThreads = 512, kSortItems = kRun / kSortThreads;
+__global__ void __launch_bounds__(kSortThreads) sort_runs_kernel(unsigned long long *__restrict__ list, int64_t cap,
+                                                                 const int *__restrict__ run_q,
+                                                                 const int *__restrict__ run_idx,
+                                                                 const int *__restrict__ len) {
+    using BRS = cub::BlockRadixSort<unsigned, kSortThreads, kSortItems, unsigned>;
+    __shared__ typename BRS::TempStorage tmp;
     const int q = run_q[blockIdx.x], r = run_idx[blockIdx.x];
     const int64_t base = (int64_t)q * cap + (int64_t)r * kRun;
     const int m = min(kRun, len[q] - r * kRun);
     DCHECK(m > 0 && (int64_t)r * kRun + m <= cap, "sort q=%d r=%d m=%d cap=%lld", q, r, m, (long long)cap);
-    int P2 = 1;
-    while (P2 < m) P2 <<= 1;
-    for (int t = threadIdx.x; t < P2; t += blockDim.x) v[t] = t < m ? list[base + t] : ~0ull;
-    __syncthreads();
-    for (int k = 2; k <= P2; k <<= 1)
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int t = threadIdx.x; t < P2; t += blockDim.x) {
-                int u = t ^ j;
-                if (u > t) {
-                    bool up = (t & k) == 0;
-                    unsigned long long a = v[t], b = v[u];
-                    if ((a > b) == up) { v[t] = b; v[u] = a; }
-                }
-            }
-            __syncthreads();
-        }
-    for (int t = threadIdx.x; t < m; t += blockDim.x) list[base + t] = v[t];
+    unsigned key[kSortItems], val[kSortItems];
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const int i = threadIdx.x * kSortItems + j;
+        const unsigned long long k = i < m ? list[base + i] : ~0ull;
+        key[j] = (unsigned)(k >> 32);
+        val[j] = (unsigned)(k & 0xffffffffu);
+    }
+    BRS(tmp).Sort(key, val);
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const int i = threadIdx.x * kSortItems + j;
+        if (i < m) list[base + i] = ((unsigned long long)key[j] << 32) | val[j];
+    }
 }
 
 struct QState {
@@ -217,7 +221,7 @@ __global__ void start_walk_kernel(QState s, int Qb) {
 // Per-round plan: items of each active query = min(D0 * 2^round, remaining), and
 // the warp chunks (kDtwIpw items each, never spanning two queries) that hold them.
 // Two exclusive scans: item_off (results layout) and chunk_off (warp -> query).
-constexpr int kD0 = 32, kDMax = 65536;
+constexpr int kD0 = 128, kDMax = 65536;
 __device__ __forceinline__ int2 block_scan2(int2 v, int2 *warp_sums, int2 &total) {
     // inclusive block-wide scan of two ints; returns the inclusive value, sets total
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -248,7 +252,7 @@ __device__ __forceinline__ int2 block_scan2(int2 v, int2 *warp_sums, int2 &total
 // into the top-k and tau directly): the walk advances past them and skips the rest of
 // a sorted run once its next bound exceeds tau (1+eps).
 __global__ void __launch_bounds__(1024) plan_kernel(QState s, int Qb, const unsigned long long *__restrict__ list,
-                                                    int64_t cap, bool sorted) {
+                                                    int64_t cap, bool sorted, int d0) {
     __shared__ int2 warp_sums[32];
     int2 carry = make_int2(0, 0);
     for (int base = 0; base < Qb; base += blockDim.x) {
@@ -266,7 +270,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(QState s, int Qb, const unsi
             }
             s.pos[q] = pos;
             if (pos < len) {
-                int d = kD0 << min(s.rnd[q], 11);
+                int d = d0 << min(s.rnd[q], 11);
                 d = min(d, kDMax);
                 cnt = min(d, len - pos);
             } else {
@@ -448,6 +452,10 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     int64_t Qb = opts && opts->query_block > 0 ? opts->query_block : (int64_t)(free_b * 0.45 / per_q);
     Qb = std::max<int64_t>(1, std::min<int64_t>(Qb, Q));
     if (Qb >= 64) Qb = Qb / 64 * 64;
+    if (!(opts && opts->query_block > 0) && Qb >= 64) {  // balance the blocks (e.g. 2 x 4096, not 7168 + 1024)
+        const int64_t nb = ceil_div(Q, Qb);
+        Qb = std::min<int64_t>(Qb, ceil_div(ceil_div(Q, nb), 64) * 64);
+    }
     const int64_t cap = N;
     const int64_t ldb = (N + 3) / 4 * 4;
 
@@ -592,7 +600,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 DTWLB_TRY(wsget(S_COUNT, nr * 2 + 64, &d_runs));
                 DTWLB_CUDA(cudaMemcpyAsync(d_runs, run_q.data(), nr * 4, cudaMemcpyHostToDevice, st));
                 DTWLB_CUDA(cudaMemcpyAsync(d_runs + nr, run_idx.data(), nr * 4, cudaMemcpyHostToDevice, st));
-                sort_runs_kernel<<<(unsigned)nr, 1024, 0, st>>>(list, cap, d_runs, d_runs + nr, s.len);
+                sort_runs_kernel<<<(unsigned)nr, kSortThreads, 0, st>>>(list, cap, d_runs, d_runs + nr, s.len);
                 DTWLB_LAUNCH_CHECK();
             }
             if (stats) cudaEventRecord(ev[1], st);
@@ -601,7 +609,8 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
             DTWLB_LAUNCH_CHECK();
             for (int round = 0;; ++round) {
                 ++walk_rounds;
-                plan_kernel<<<1, 1024, 0, st>>>(s, (int)qn, list, cap, sorted);
+                static const int env_d0 = [] { const char *e = getenv("DTWLB_D0"); return e ? atoi(e) : 0; }();
+                plan_kernel<<<1, 1024, 0, st>>>(s, (int)qn, list, cap, sorted, env_d0 > 0 ? env_d0 : kD0);
                 DTWLB_LAUNCH_CHECK();
                 int tot2[2] = {0, 0};
                 DTWLB_CUDA(cudaMemcpyAsync(tot2, s.counters, sizeof(tot2), cudaMemcpyDeviceToHost, st));
