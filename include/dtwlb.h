@@ -78,6 +78,19 @@ int lb_keogh(const float *q_env, const float *db, int64_t Q, int64_t N, int32_t 
 int lb_piecewise(const float *q_env, const float *db, int64_t Q, int64_t N, int32_t n, int32_t p,
                  float *out, void *stream);
 
+/* Symmetric piecewise-sum bound, the gate nn_search runs over every pair
+ * (reading c20):
+ *   out[q][c] = max(lb_piecewise(x_c | envelope of y_q), lb_piecewise(y_q | envelope of x_c))
+ * The second term is the piecewise-sum bound with the roles of query and
+ * candidate exchanged -- a lower bound of LB_Keogh_p(y, x) <= DTW_p(y, x), and
+ * DTW_p is symmetric -- so the maximum is a lower bound of DTW_p(x, y).
+ * Both terms outward-rounded as lb_piecewise.  q: device [Q][n] queries; q_env:
+ * device [2][Q][n] envelope of q with locality w; db: device [N][n]; the
+ * candidates' envelopes (same w) are computed inside.  out: device [Q][N] rooted.
+ * Errors: as lb_keogh, plus EINVAL for w < 0. */
+int lb_piecewise_sym(const float *q, const float *q_env, const float *db, int64_t Q, int64_t N,
+                     int32_t n, int32_t w, int32_t p, float *out, void *stream);
+
 /* LB_Improved_p (section "LB_Improved"; Alg. 3 lines P:587-606):
  *   out[q][c]^p = LB_Keogh_p(x_c, y_q)^p + LB_Keogh_p(y_q, H(x_c, y_q))^p,
  * i.e. the first pass plus the distance of y to the envelope of the

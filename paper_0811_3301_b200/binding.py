@@ -89,11 +89,13 @@ def load():
         lib.lb_keogh.argtypes = [vp, vp, i64, i64, i32, i32, vp, vp]
         lib.lb_piecewise.argtypes = [vp, vp, i64, i64, i32, i32, vp, vp]
         lib.lb_improved.argtypes = [vp, vp, vp, i64, i64, i32, i32, i32, vp, vp]
+        lib.lb_piecewise_sym.argtypes = [vp, vp, vp, i64, i64, i32, i32, i32, vp, vp]
         lib.dtw_band.argtypes = [vp, vp, i32, i32, i32, vp, i64, vp]
         lib.nn_search.argtypes = [vp, i64, vp, i64, i32, i32, i32, i32, vp, vp,
                                   ctypes.POINTER(NnOpts), ctypes.POINTER(NnStats), vp]
         lib.nn_merge.argtypes = [vp, vp, i32, i64, i32, vp, vp, vp]
-        for f in ("lb_envelope", "lb_keogh", "lb_piecewise", "lb_improved", "dtw_band", "nn_search", "nn_merge"):
+        for f in ("lb_envelope", "lb_keogh", "lb_piecewise", "lb_piecewise_sym", "lb_improved", "dtw_band",
+                  "nn_search", "nn_merge"):
             getattr(lib, f).restype = ctypes.c_int
         lib.dtwlb_last_error.restype = ctypes.c_char_p
         lib.dtwlb_last_error.argtypes = []
@@ -151,6 +153,17 @@ def lb_piecewise(q_env: torch.Tensor, db: torch.Tensor, p: int) -> torch.Tensor:
     N = db.shape[0]
     out = torch.empty((Q, N), dtype=torch.float32, device=db.device)
     _check(load().lb_piecewise(q_env.data_ptr(), db.data_ptr(), Q, N, n, p, out.data_ptr(), _stream()))
+    return out
+
+
+def lb_piecewise_sym(q: torch.Tensor, q_env: torch.Tensor, db: torch.Tensor, w: int, p: int) -> torch.Tensor:
+    """[Q][N] symmetric piecewise-sum bound: max of lb_piecewise(x | env y) and (y | env x) (rooted)."""
+    q, q_env, db = _dev(q, "q"), _dev(q_env, "q_env"), _dev(db, "db")
+    Q, n = q.shape
+    N = db.shape[0]
+    out = torch.empty((Q, N), dtype=torch.float32, device=db.device)
+    _check(load().lb_piecewise_sym(q.data_ptr(), q_env.data_ptr(), db.data_ptr(), Q, N, n, w, p, out.data_ptr(),
+                                   _stream()))
     return out
 
 

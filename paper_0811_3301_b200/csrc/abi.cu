@@ -129,6 +129,38 @@ int lb_piecewise(const float *q_env, const float *db, int64_t Q, int64_t N, int3
     return DTWLB_OK;
 }
 
+int lb_piecewise_sym(const float *q, const float *q_env, const float *db, int64_t Q, int64_t N, int32_t n,
+                     int32_t w, int32_t p, float *out, void *stream) {
+    g_err[0] = 0;
+    CHECK_ARG(n >= 1, "lb_piecewise_sym: n = %d < 1", n);
+    CHECK_ARG(w >= 0, "lb_piecewise_sym: w = %d < 0", w);
+    CHECK_ARG(Q >= 0 && N >= 0, "lb_piecewise_sym: negative size");
+    DTWLB_TRY(check_p(p));
+    if (Q == 0 || N == 0) return DTWLB_OK;
+    CHECK_ARG(q && q_env && db && out, "lb_piecewise_sym: NULL pointer");
+    DTWLB_TRY(require_device());
+    std::lock_guard<std::mutex> lock(api_mutex());
+    cudaStream_t st = as_stream(stream);
+    const int Dp = paa_pitch(n);
+    w = std::min(w, n - 1);
+    float *xs, *qs, *dbenv;
+    DTWLB_TRY(ws_get_bytes(8, sizeof(float) * 4 * N * Dp, (void **)&xs));
+    DTWLB_TRY(ws_get_bytes(9, sizeof(float) * 4 * Q * Dp, (void **)&qs));
+    DTWLB_TRY(ws_get_bytes(3, sizeof(float) * 2 * N * n, (void **)&dbenv));
+    // forward: candidate sums against the query envelope sums
+    DTWLB_TRY(launch_paa_sums(db, N, n, xs, xs + N * Dp, st));
+    DTWLB_TRY(launch_paa_env_sums(q_env, q_env + Q * n, Q, n, qs, qs + Q * Dp, st));
+    DTWLB_TRY(launch_paa_bound(qs, qs + Q * Dp, xs, xs + N * Dp, Q, N, n, p, true, out, N, st));
+    // reverse: query sums against the candidate envelope sums, max-combined
+    DTWLB_TRY(launch_envelope(db, n, w, dbenv, dbenv + N * n, N, st));
+    DTWLB_TRY(launch_paa_env_sums(dbenv, dbenv + N * n, N, n, xs + 2 * N * Dp, xs + 3 * N * Dp, st));
+    DTWLB_TRY(launch_paa_sums(q, Q, n, qs + 2 * Q * Dp, qs + 3 * Q * Dp, st));
+    DTWLB_TRY(launch_paa_bound_rev(qs + 2 * Q * Dp, qs + 3 * Q * Dp, xs + 2 * N * Dp, xs + 3 * N * Dp, Q, N, n, p,
+                                   true, out, N, st));
+    DTWLB_CUDA(cudaStreamSynchronize(st));  // workspace reuse safety
+    return DTWLB_OK;
+}
+
 int lb_improved(const float *q, const float *q_env, const float *db, int64_t Q, int64_t N, int32_t n,
                 int32_t w, int32_t p, float *out, void *stream) {
     g_err[0] = 0;

@@ -19,7 +19,12 @@
 // sides, which contributes max(0-0, 0-0, 0) = 0.
 //
 // The same tile kernel evaluates the piecewise-sum pre-filter over
-// segment sums (PAA = true): D = n/8 "samples" per row, directed rounding.
+// segment sums (PAA = true): D = n/8 "samples" per row, directed rounding.  With
+// REV it evaluates the REVERSE piecewise-sum bound -- the query's segment sums
+// against the candidate's envelope sums, sum_j d(P(y)_j, [P(L(x))_j, P(U(x))_j])^p,
+// a lower bound of LB_Keogh_p(y, x) <= DTW_p(y, x) = DTW_p(x, y) (symmetry, P:1052;
+// DESIGN.md reading c20) -- and stores max(stored bound, reverse bound): the
+// symmetric gate of the cascade.
 #include <cstdlib>
 
 #include <cuda_fp16.h>
@@ -103,7 +108,7 @@ __device__ __forceinline__ float lb_elem(float acc, float xl, float xh, float u,
     }
 }
 
-template <int P, bool VEC, bool ROOTED, bool PAA>
+template <int P, bool VEC, bool ROOTED, bool PAA, bool REV>
 __global__ void __launch_bounds__(NT, 2)
 keogh_tile_kernel(const float *__restrict__ U, const float *__restrict__ L, const float *__restrict__ db,
                   const float *__restrict__ db2, int64_t Q, int64_t N, int n, void *__restrict__ out,
@@ -169,7 +174,16 @@ keogh_tile_kernel(const float *__restrict__ U, const float *__restrict__ L, cons
                 if constexpr (PAA) xw = *reinterpret_cast<const float4 *>(&s.X2[cg + 16 * j][k]);
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    if constexpr (PAA) {
+                    if constexpr (PAA && REV) {
+                        // query side (U, L slots) = (P(y) lo, P(y) hi); candidate side (X, X2
+                        // slots) = (P(U(x)) hi, P(L(x)) lo): d = max(ylo - Uxhi, Lxlo - yhi, 0)
+                        float t = acc[r][j];
+                        t = lb_elem2<P, PAA>(t, make_float2(uv[r].x, uv[r].y), make_float2(lv[r].x, lv[r].y),
+                                             make_float2(xv.x, xv.y), make_float2(xw.x, xw.y));
+                        t = lb_elem2<P, PAA>(t, make_float2(uv[r].z, uv[r].w), make_float2(lv[r].z, lv[r].w),
+                                             make_float2(xv.z, xv.w), make_float2(xw.z, xw.w));
+                        acc[r][j] = t;
+                    } else if constexpr (PAA) {
                         float t = acc[r][j];
                         t = lb_elem2<P, PAA>(t, make_float2(xv.x, xv.y), make_float2(xw.x, xw.y),
                                              make_float2(uv[r].x, uv[r].y), make_float2(lv[r].x, lv[r].y));
@@ -212,19 +226,23 @@ keogh_tile_kernel(const float *__restrict__ U, const float *__restrict__ L, cons
             } else if constexpr (ROOTED) {
                 v = rootp<P>(v);
             }
-            if constexpr (PAA && !ROOTED)  // nn_search's gate block: fp16, rounded down (still a lower bound)
-                reinterpret_cast<__half *>(out)[q * ldo + c] = __float2half_rd(v);
-            else
-                reinterpret_cast<float *>(out)[q * ldo + c] = v;
+            if constexpr (PAA && !ROOTED) {  // nn_search's gate block: fp16, rounded down (still a lower bound)
+                __half *o = reinterpret_cast<__half *>(out) + q * ldo + c;
+                const __half h = __float2half_rd(v);
+                *o = REV ? __hmax(*o, h) : h;  // max of two lower bounds
+            } else {
+                float *o = reinterpret_cast<float *>(out) + q * ldo + c;
+                *o = REV ? fmaxf(*o, v) : v;
+            }
         }
     }
 }
 
-template <int P, bool VEC, bool ROOTED, bool PAA>
+template <int P, bool VEC, bool ROOTED, bool PAA, bool REV>
 int launch_tile_t(const float *U, const float *L, const float *db, const float *db2, int64_t Q, int64_t N,
                   int n, void *out, int64_t ldo, cudaStream_t st) {
     const size_t smem = 2 * sizeof(Stage<PAA>);
-    auto k = keogh_tile_kernel<P, VEC, ROOTED, PAA>;
+    auto k = keogh_tile_kernel<P, VEC, ROOTED, PAA, REV>;
     DTWLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t nqt = ceil_div(Q, TQ), nct = ceil_div(N, TC);
     const int64_t tiles = nqt * nct;
@@ -237,14 +255,14 @@ int launch_tile_t(const float *U, const float *L, const float *db, const float *
     return DTWLB_OK;
 }
 
-template <bool PAA>
+template <bool PAA, bool REV = false>
 int launch_tile(const float *U, const float *L, const float *db, const float *db2, int64_t Q, int64_t N, int n,
                 int p, bool rooted, void *out, int64_t ldo, cudaStream_t st) {
     if (Q == 0 || N == 0) return DTWLB_OK;
     const bool vec = (n % 4 == 0) && ((reinterpret_cast<uintptr_t>(U) | reinterpret_cast<uintptr_t>(L) |
                                        reinterpret_cast<uintptr_t>(db) | reinterpret_cast<uintptr_t>(db2)) %
                                       16 == 0);
-#define DTWLB_K(P_, V_, R_) return launch_tile_t<P_, V_, R_, PAA>(U, L, db, db2, Q, N, n, out, ldo, st)
+#define DTWLB_K(P_, V_, R_) return launch_tile_t<P_, V_, R_, PAA, REV>(U, L, db, db2, Q, N, n, out, ldo, st)
     if (p == 1) {
         if (vec) { if (rooted) DTWLB_K(1, true, true); else DTWLB_K(1, true, false); }
         else { if (rooted) DTWLB_K(1, false, true); else DTWLB_K(1, false, false); }
@@ -311,6 +329,11 @@ int launch_paa_env_sums(const float *U, const float *L, int64_t count, int n, fl
 int launch_paa_bound(const float *Uhi, const float *Llo, const float *Xlo, const float *Xhi, int64_t Q,
                      int64_t N, int n, int p, bool rooted, void *out, int64_t ldo, cudaStream_t st) {
     return launch_tile<true>(Uhi, Llo, Xlo, Xhi, Q, N, paa_pitch(n), p, rooted, out, ldo, st);
+}
+
+int launch_paa_bound_rev(const float *Ylo, const float *Yhi, const float *Uxhi, const float *Lxlo, int64_t Q,
+                         int64_t N, int n, int p, bool rooted, void *out, int64_t ldo, cudaStream_t st) {
+    return launch_tile<true, true>(Ylo, Yhi, Uxhi, Lxlo, Q, N, paa_pitch(n), p, rooted, out, ldo, st);
 }
 
 int launch_keogh(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n, int p,

@@ -34,6 +34,12 @@ int launch_paa_env_sums(const float *U, const float *L, int64_t count, int n, fl
 // else __half out rounded down (nn_search's gate block).
 int launch_paa_bound(const float *Uhi, const float *Llo, const float *Xlo, const float *Xhi, int64_t Q,
                      int64_t N, int n, int p, bool rooted, void *out, int64_t ldo, cudaStream_t st);
+// Reverse piecewise-sum bound (reading c20): out[q][c] = max(out[q][c],
+// sum_j d(P(y_q)_j, [P(L(x_c))_j, P(U(x_c))_j])^p * (p == 2 ? 1/s : 1)), directed rounding.
+// Ylo/Yhi: query sums [Q][Dp] (launch_paa_sums of the queries); Uxhi/Llo: candidate
+// envelope sums [N][Dp] (launch_paa_env_sums of U(x), L(x)).  Same out types as above.
+int launch_paa_bound_rev(const float *Ylo, const float *Yhi, const float *Uxhi, const float *Lxlo, int64_t Q,
+                         int64_t N, int n, int p, bool rooted, void *out, int64_t ldo, cudaStream_t st);
 
 // Arguments of the survivor passes (improved.cu).  Padded per-query arrays:
 //   yq, LUq, ULq: [Q][npadE] (npadE = 32 * epl), zero padded;

@@ -76,7 +76,7 @@ std::mutex &ws_mutex() {
 
 enum Slot {
     S_QSTAGE, S_DBSTAGE, S_ENV, S_QPAD, S_YSH, S_DBENV, S_BETA1, S_LIST, S_RES, S_STATE, S_TOPK,
-    S_OUTSTAGE, S_SCRATCH, S_TMP, S_MASK, S_PAA, S_QPAA, S_COUNT
+    S_OUTSTAGE, S_SCRATCH, S_TMP, S_MASK, S_PAA, S_QPAA, S_RPAA, S_COUNT
 };
 
 template <typename T>
@@ -442,7 +442,16 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     }
     float *dbenv;  // U(x), L(x): [2][N][n]
     DTWLB_TRY(wsget(S_DBENV, (size_t)2 * N * n, &dbenv));
-    if (!keogh_only) DTWLB_TRY(launch_envelope(db, n, w, dbenv, dbenv + (size_t)N * n, N, st));
+    if (!keogh_only || prefilter) DTWLB_TRY(launch_envelope(db, n, w, dbenv, dbenv + (size_t)N * n, N, st));
+    // symmetric gate (reading c20): reverse piecewise sums P(U(x)) up, P(L(x)) down [2][N][Dp]
+    // and P(y) down / up [2][Q][Dp]
+    float *rpaa = nullptr;
+    if (prefilter) {
+        DTWLB_TRY(wsget(S_RPAA, (size_t)2 * N * Dp + (size_t)2 * Q * Dp, &rpaa));
+        DTWLB_TRY(launch_paa_env_sums(dbenv, dbenv + (size_t)N * n, N, n, rpaa, rpaa + (size_t)N * Dp, st));
+        float *yp = rpaa + (size_t)2 * N * Dp;
+        DTWLB_TRY(launch_paa_sums(queries, Q, n, yp, yp + (size_t)Q * Dp, st));
+    }
     tm.mark();  // 1
 
     // ---- query block size from free memory: gate bound (4N) + list (8N) per query ----
@@ -517,10 +526,14 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         // ---- dense gate pass for the block: the piecewise-sum bound beta0 (pre-filter,
         //      LB_Keogh then runs on its survivors inside the survivor pass), or a2 itself ----
         if (stats) cudaEventRecord(ev[0], st);
-        if (prefilter)
+        if (prefilter) {
             DTWLB_TRY(launch_paa_bound(qpaa + qb0 * Dp, qpaa + (size_t)Q * Dp + qb0 * Dp, xpaa,
                                        xpaa + (size_t)N * Dp, qn, N, n, p, false, beta1, ldb, st));
-        else
+            // symmetric gate: max with the reverse piecewise-sum bound (reading c20)
+            const float *yp = rpaa + (size_t)2 * N * Dp;
+            DTWLB_TRY(launch_paa_bound_rev(yp + qb0 * Dp, yp + (size_t)Q * Dp + qb0 * Dp, rpaa,
+                                           rpaa + (size_t)N * Dp, qn, N, n, p, false, beta1, ldb, st));
+        } else
             DTWLB_TRY(launch_keogh(U + qb0 * n, L + qb0 * n, db, qn, N, n, p, false, beta1, ldb, st));
         if (stats) cudaEventRecord(ev[1], st);
         init_state_kernel<<<(unsigned)ceil_div(qn, 256), 256, 0, st>>>(s, (int)qn, k);

@@ -25,7 +25,7 @@ def lib():
 
 def test_header_declares_the_boundary():
     fns = _header_functions()
-    for f in ["lb_envelope", "lb_keogh", "lb_piecewise", "lb_improved", "dtw_band", "nn_search", "nn_merge",
+    for f in ["lb_envelope", "lb_keogh", "lb_piecewise", "lb_piecewise_sym", "lb_improved", "dtw_band", "nn_search", "nn_merge",
               "dtwlb_last_error", "dtwlb_release_workspace"]:
         assert f in fns, fns
 
@@ -45,6 +45,8 @@ def test_argument_validation_precedes_device(lib):
     assert lib.lb_keogh(null, null, 1, 1, 8, 3, null, null) == 2          # p = 3 unsupported
     assert lib.lb_piecewise(null, null, 1, 1, 8, 3, null, null) == 2      # p = 3 unsupported
     assert lib.lb_piecewise(null, null, 1, 1, 0, 1, null, null) == 1      # n < 1
+    assert lib.lb_piecewise_sym(null, null, null, 1, 1, 8, 1, 3, null, null) == 2   # p = 3 unsupported
+    assert lib.lb_piecewise_sym(null, null, null, 1, 1, 8, -1, 1, null, null) == 1  # w < 0
     assert lib.dtw_band(null, null, 8, 2, 3, null, 1, null) == 2          # p = 3 unsupported
     assert lib.dtw_band(null, null, 8, 2, 0, null, 1, null) == 1          # p = 0 (inf) ok, NULL pointers
     assert lib.nn_search(null, 1, null, 4, 8, 1, 0, 1, null, null, None, None, null) == 2   # p = inf

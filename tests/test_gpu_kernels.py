@@ -114,6 +114,29 @@ def test_lb_piecewise(cuda_ok, n, w, p):
     assert pw[3, 5] == 0.0
 
 
+@pytest.mark.parametrize("n,w", BOUND_CASES + [(1, 0), (9, 2), (1001, 50)])
+@pytest.mark.parametrize("p", [1, 2])
+def test_lb_piecewise_sym(cuda_ok, n, w, p):
+    """Symmetric gate (reading c20): max of the forward and the reverse piecewise-sum
+    bounds, at or below the exact fp64 value (outward rounding), within relative 1e-5 of
+    it, never above DTW_p."""
+    from paper_0811_3301_b200 import dtw_band, lb_piecewise_sym
+    Q, N = 37, 200
+    if n >= 512:
+        Q, N = 7, 90
+    kind = "raw" if n == 128 else "rw"
+    qs, db = series(Q, n, kind), series(N, n, kind)
+    db[5] = qs[3]
+    ps = lb_piecewise_sym(dev(qs), _env_dev(qs, w), dev(db), w, p).cpu().numpy().astype(np.float64)
+    op = np.array([[max(oracle.lb_piecewise(db[c], qs[q], w, p, 8), oracle.lb_piecewise(qs[q], db[c], w, p, 8))
+                    for c in range(N)] for q in range(Q)])
+    assert np.all(ps <= op * (1 + 1e-7) + 1e-30), "outward rounding violated"
+    close(ps, op, 1e-5, 1e-5)
+    assert ps[3, 5] == 0.0
+    d = dtw_band(dev(np.repeat(db[:16], 1, 0)), dev(np.repeat(qs[:1], 16, 0)), w, p).cpu().numpy()
+    assert np.all(ps[0, :16] <= d * (1 + 1e-5) + 1e-6)
+
+
 def test_lb_piecewise_golden(cuda_ok):
     from paper_0811_3301_b200 import lb_piecewise
     x = np.array([[2, 3, 0, 0, 5, 0, 0, 0, 0]], np.float32)

@@ -279,6 +279,39 @@ def test_lb_improved_rejects_infinity():
 
 
 # ---------------------------------------------------------------- piecewise-sum pre-filter
+def test_reverse_piecewise_symmetric_gate():
+    """Reading c20: the piecewise-sum bound with query and candidate exchanged,
+    lb_piecewise(y | envelope of x), is a lower bound of LB_Keogh_p(y, x) <= DTW_p(y, x)
+    = DTW_p(x, y) (symmetry), so max(forward, reverse) <= DTW_p(x, y).  Pinned by:
+    s = 1 reverse == sum_i d(y_i, [L(x)_i, U(x)_i])^p with numpy's sliding-window envelope
+    of x; the chain on random cases; and the hand-checked fixture x = (0,0,0), y = (0,5,0),
+    w = 1: forward 0 (x inside the envelope of y), reverse 5 = DTW_1 (p = 1),
+    and with one interval (s = 3) reverse^2 = 5^2 / 3 for p = 2."""
+    from numpy.lib.stride_tricks import sliding_window_view as swv
+    x, y = np.zeros(3), np.array([0.0, 5.0, 0.0])
+    assert oracle.lb_piecewise(x, y, 1, 1, 1) == 0.0
+    assert oracle.lb_piecewise(y, x, 1, 1, 1) == 5.0 == oracle.dtw(x, y, 1, 1)
+    assert oracle.lb_piecewise(y, x, 1, 2, 3) ** 2 == pytest.approx(25.0 / 3, rel=1e-12)
+    for _ in range(1000):
+        n = int(RNG.integers(1, 14))
+        integer = RNG.random() < 0.5
+        x = rand_int_series(n) if integer else RNG.standard_normal(n)
+        y = rand_int_series(n) if integer else RNG.standard_normal(n)
+        w = int(RNG.integers(0, n + 1))
+        we = min(w, n - 1)
+        xp = np.pad(np.asarray(x, float), (we, we), mode="edge")
+        Ux, Lx = swv(xp, 2 * we + 1).max(axis=1), swv(xp, 2 * we + 1).min(axis=1)
+        yv = np.asarray(y, float)
+        for p in (1, 2):
+            rev_keogh = float(np.sum(np.maximum(np.maximum(yv - Ux, Lx - yv), 0.0) ** p))
+            assert oracle.lb_piecewise(y, x, w, p, 1) ** p == pytest.approx(rev_keogh, rel=1e-12, abs=1e-12)
+            d = oracle.dtw(x, y, w, p)
+            tol = 1e-12 * (1 + d)
+            for s in (1, 2, 4, 8):
+                sym = max(oracle.lb_piecewise(x, y, w, p, s), oracle.lb_piecewise(y, x, w, p, s))
+                assert sym <= d + tol
+
+
 @pytest.mark.parametrize("case", GOLDEN["piecewise"], ids=lambda c: c["cite"][:30])
 def test_piecewise_golden(case):
     """Hand-derived values of the piecewise-sum bound (p = 2 reading c18)."""
