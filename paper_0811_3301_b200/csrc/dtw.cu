@@ -124,9 +124,28 @@ __device__ __forceinline__ float b1_at(const DtwArgs &a, int64_t idx) {
 }
 
 template <int P>
+__device__ __forceinline__ float col_lb(float y, float ux, float lx, float lu, float ul) {
+    // LB_Improved column term d(y_j, [L(H)_j, U(H)_j])^p by the closed form (improved.cu)
+    const float d = max3f(y - fmaxf(ux, lu), fminf(lx, ul) - y, 0.f);
+    return P == 1 ? d : d * d;
+}
+
+template <int P>
 __device__ __forceinline__ float row_lb(float x, float u, float l) {
     const float d = max3f(x - u, l - x, 0.f);
     return P == 1 ? d : d * d;
+}
+
+// cp.async of r[i0 .. i0+7] (zero beyond n) into dst[0..8) (16-byte copies when aligned)
+__device__ __forceinline__ void stage_rows8(float *dst, const float *r, int i0, int n) {
+    if (((n & 3) == 0)) {
+        const bool ok0 = i0 + 4 <= n, ok1 = i0 + 8 <= n;
+        cp_async16(dst, ok0 ? r + i0 : r, ok0 ? 16 : 0);
+        cp_async16(dst + 4, ok1 ? r + i0 + 4 : r, ok1 ? 16 : 0);
+    } else {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) cp_async4(dst + t, i0 + t < n ? r + i0 + t : r, i0 + t < n ? 4 : 0);
+    }
 }
 
 // 8 values v[i0 .. i0+7] of a row of length n (fill beyond n); vector loads when aligned
@@ -448,7 +467,12 @@ __device__ __forceinline__ void four_rows(float (&B)[2 * WB + 2], const float (&
 template <int WB>
 struct Dtw4Cfg {
     static constexpr int NY = (2 * WB + 4 + 3) / 4 * 4;
-    static constexpr int SL = NY + 20;  // y window, x[0..7], U[0..3], L[0..3], 2 spare, (q, c)
+    // [0, NY) the y window and [NY] the gate word (refill, read at activation); while the lane
+    // is active [0, 40) stages the row+column cascade's column data (reading c21);
+    // [XA, XA + 8) x and [XA + 8, XA + 24) U(y), L(y) of the next step's 8 rows (written by
+    // the refill for rows 0..7, then one step ahead); [SL - 2, SL) the pair's (q, c)
+    static constexpr int XA = NY + 4 > 40 ? NY + 4 : 40;
+    static constexpr int SL = XA + 28;
     static constexpr size_t smem = (size_t)NT * SL * sizeof(float) +
                                    (size_t)(NT / 32) * kChunk4 * (sizeof(unsigned long long) + sizeof(int));
 };
@@ -462,6 +486,7 @@ dtw4_kernel(DtwArgs a) {
     constexpr int NB = 2 * WB + 1;
     constexpr int NY = Dtw4Cfg<WB>::NY;  // window length, a multiple of 4 (aligned refills)
     constexpr int SL = Dtw4Cfg<WB>::SL;
+    constexpr int XA = Dtw4Cfg<WB>::XA;
     extern __shared__ __align__(16) float dsm[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     float *slot = dsm + (size_t)threadIdx.x * SL;  // this lane's staging slot
@@ -474,20 +499,24 @@ dtw4_kernel(DtwArgs a) {
     const int64_t nchunks = (total + kChunk4 - 1) / kChunk4;
     const unsigned lt = (1u << lane) - 1u;
 
-    int64_t cbeg = 0, cend = 0, cursor = 0;
+    int cbeg = 0, cend = 0, cursor = 0;  // item indices (< 2^31: one walk round)
     int st = kFree;
-    int64_t item = 0;
+    int item = 0;
     const float *xr = nullptr, *yr = nullptr;
     float thr = kInf, thr_n = kInf, beta_n = 0.f;
     int i = 0;
     float B[NB + 1], Y[NY];
-    float xv[8];  // x of rows i .. i+7 (loaded one 8-row step ahead)
+    float xv[8];  // x of rows i .. i+7 (staged in the slot one 8-row step ahead)
     // cascading abandon: rest = LB_Keogh^p terms of the rows not yet computed
     const bool casc = WALK && (a.b1 != nullptr || a.b1h != nullptr);
+    // row+column cascade (reading c21): the gate word holds rest0 = LB_Improved^p minus the
+    // column terms of [0, col_c0) (rest0_kernel); each step subtracts its rows' LB_Keogh terms
+    // and the column terms of [C(i0), C(i0 + 8)), C(i) = i + col_c0
+    // (col_c0 > 0 requires n % 4 == 0 and the __half gate block)
+    const bool casc2 = casc && a.col_c0 > 0 && a.b1h != nullptr;
     float rest = 0.f, rest_n = 0.f;
     const float *ur = nullptr, *lr = nullptr;
-    float uc[4], lc[4];  // U(y), L(y) of the current 4-row block (loaded one block ahead)
-    unsigned long long rows_done = 0, n_abandon = 0, n_started = 0;
+    unsigned rows_done = 0, n_abandon = 0, n_started = 0;  // per-lane counters
 
     while (true) {
         // ---- (a) activate the lanes whose refill copies were issued one step ago ----
@@ -503,17 +532,19 @@ dtw4_kernel(DtwArgs a) {
                         const float4 v = *reinterpret_cast<const float4 *>(slot + d);
                         Y[d] = v.x; Y[d + 1] = v.y; Y[d + 2] = v.z; Y[d + 3] = v.w;
                     }
-                    const float4 x0 = *reinterpret_cast<const float4 *>(slot + NY);
-                    const float4 x1 = *reinterpret_cast<const float4 *>(slot + NY + 4);
+                    const float4 x0 = *reinterpret_cast<const float4 *>(slot + XA);
+                    const float4 x1 = *reinterpret_cast<const float4 *>(slot + XA + 4);
                     xv[0] = x0.x; xv[1] = x0.y; xv[2] = x0.z; xv[3] = x0.w;
                     xv[4] = x1.x; xv[5] = x1.y; xv[6] = x1.z; xv[7] = x1.w;
-                    if (casc) {
-                        const float4 u0 = *reinterpret_cast<const float4 *>(slot + NY + 8);
-                        const float4 l0 = *reinterpret_cast<const float4 *>(slot + NY + 12);
-                        uc[0] = u0.x; uc[1] = u0.y; uc[2] = u0.z; uc[3] = u0.w;
-                        lc[0] = l0.x; lc[1] = l0.y; lc[2] = l0.z; lc[3] = l0.w;
-                    }
                     thr = thr_n;
+                    if (casc) {
+                        // the pair's gate word, copied with the refill (no register wait on a
+                        // random HBM gather): +-beta1 / rest0, fp32 or the __half at c & 1
+                        const uint32_t wv = reinterpret_cast<const uint32_t *>(slot)[NY];
+                        const uint32_t c = reinterpret_cast<const uint32_t *>(slot)[SL - 1];
+                        const unsigned short hb = (unsigned short)((c & 1u) ? wv >> 16 : wv & 0xffffu);
+                        rest_n = a.b1 ? __uint_as_float(wv) : __half2float(__ushort_as_half(hb));
+                    }
                     rest = fabsf(rest_n);
                     st = kActive;
                     ++n_started;
@@ -528,8 +559,8 @@ dtw4_kernel(DtwArgs a) {
             if (lane == 0) c = atomicAdd(a.queue, 1u);
             c = __shfl_sync(0xffffffffu, c, 0);
             if (c < nchunks) {
-                cbeg = c * kChunk4;
-                cend = cbeg + kChunk4 < total ? cbeg + kChunk4 : total;
+                cbeg = (int)c * kChunk4;
+                cend = (int)(cbeg + kChunk4 < total ? cbeg + kChunk4 : total);
                 cursor = cbeg;
                 if constexpr (WALK) {
                     // stage the chunk's keys and queries: items are in query order, each
@@ -541,7 +572,7 @@ dtw4_kernel(DtwArgs a) {
                     }
                     int q = lo;
                     for (int t = 0; t < kChunk4 / 32; ++t) {
-                        const int64_t it = cbeg + lane + 32 * t;
+                        const int it = cbeg + lane + 32 * t;
                         if (it < cend) {
                             while (it >= a.item_off[q + 1]) ++q;
                             const int64_t j = a.pos[q] + (it - a.item_off[q]);
@@ -555,7 +586,7 @@ dtw4_kernel(DtwArgs a) {
             }
         }
         if (need && cursor < cend) {
-            const int64_t mine = cursor + __popc(need & lt);
+            const int mine = cursor + __popc(need & lt);
             cursor += __popc(need);
             if (st == kFree && mine < cend) {
                 item = mine;
@@ -571,7 +602,10 @@ dtw4_kernel(DtwArgs a) {
                     beta_n = __uint_as_float((uint32_t)(key >> 32));
                     thr_n = *reinterpret_cast<volatile float *>(a.thr + qy);
                     if (casc) {
-                        rest_n = b1_at(a, qy * a.ldb + c);  // +-beta1 = sum of all row terms (|.| later)
+                        // +-beta1: the 4-byte word holding it -> slot[NY]
+                        const int64_t gi = qy * a.ldb + c;
+                        if (a.b1) cp_async4(slot + NY, a.b1 + gi, 4);
+                        else cp_async4(slot + NY, reinterpret_cast<const float *>(a.b1h + (gi & ~(int64_t)1)), 4);
                         ur = a.Uq + qy * n;
                         lr = a.Lq + qy * n;
                     }
@@ -586,24 +620,10 @@ dtw4_kernel(DtwArgs a) {
                 const float *ys = yr + (kYPadL - w - sh);
 #pragma unroll
                 for (int d = 0; d < NY; d += 4) cp_async16(slot + d, ys + d, 16);
-                if (((n & 3) == 0) && n >= 8) {
-                    cp_async16(slot + NY, xr, 16);
-                    cp_async16(slot + NY + 4, xr + 4, 16);
-                } else {
-#pragma unroll
-                    for (int t = 0; t < 8; ++t) cp_async4(slot + NY + t, t < n ? xr + t : xr, t < n ? 4 : 0);
-                }
+                stage_rows8(slot + XA, xr, 0, n);
                 if (casc) {
-                    if (((n & 3) == 0) && n >= 4) {
-                        cp_async16(slot + NY + 8, ur, 16);
-                        cp_async16(slot + NY + 12, lr, 16);
-                    } else {
-#pragma unroll
-                        for (int t = 0; t < 4; ++t) {
-                            cp_async4(slot + NY + 8 + t, t < n ? ur + t : ur, t < n ? 4 : 0);
-                            cp_async4(slot + NY + 12 + t, t < n ? lr + t : lr, t < n ? 4 : 0);
-                        }
-                    }
+                    stage_rows8(slot + XA + 8, ur, 0, n);
+                    stage_rows8(slot + XA + 16, lr, 0, n);
                 }
                 cp_commit();
 #pragma unroll
@@ -632,34 +652,45 @@ dtw4_kernel(DtwArgs a) {
         float res_v = 0.f;
         if (st == kActive) {
             const int i0 = i;
-            // prefetch x of the next 8-row step: the loads of a candidate row miss L1 and
-            // their latency hides behind this step's cells
-            float xn[8];
-            load8(xn, xr, i0 + 8, n, 0.f);
+            if (casc) {
+                // LB_Keogh terms of this step's rows (their envelope was staged one step ahead)
+                const float4 u0 = *reinterpret_cast<const float4 *>(slot + XA + 8);
+                const float4 u1 = *reinterpret_cast<const float4 *>(slot + XA + 12);
+                const float4 l0 = *reinterpret_cast<const float4 *>(slot + XA + 16);
+                const float4 l1 = *reinterpret_cast<const float4 *>(slot + XA + 20);
+                const float uu[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+                const float ll[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+                float rs = 0.f;
+#pragma unroll
+                for (int t = 0; t < 8; ++t) rs += i0 + t < n ? row_lb<P>(xv[t], uu[t], ll[t]) : 0.f;
+                rest -= rs;  // (rs consumed before the slot is overwritten below)
+            }
+            // x (and the envelope) of the next step's rows into the slot: the gathers of a
+            // candidate row miss L1 and their latency hides behind this step's cells
+            stage_rows8(slot + XA, xr, i0 + 8, n);
+            if (casc) {
+                stage_rows8(slot + XA + 8, ur, i0 + 8, n);
+                stage_rows8(slot + XA + 16, lr, i0 + 8, n);
+            }
+            // row+column cascade: the column terms of [C(i0), C(i0) + 8) (y, U(L(y)), L(U(y))
+            // of the query, U(x), L(x) of the candidate) are copied into the lane's slot (free
+            // while the lane is active) and subtracted at the end of the step
+            if (casc2) {
+                const int qy = reinterpret_cast<const int *>(slot)[SL - 2];
+                const int64_t cx = (int64_t)reinterpret_cast<const uint32_t *>(slot)[SL - 1];
+                const int cc = i0 + a.col_c0;
+                stage_rows8(slot, a.yq + (int64_t)qy * n, cc, n);
+                stage_rows8(slot + 8, a.LUq + (int64_t)qy * n, cc, n);
+                stage_rows8(slot + 16, a.ULq + (int64_t)qy * n, cc, n);
+                stage_rows8(slot + 24, a.Uxdb + cx * n, cc, n);
+                stage_rows8(slot + 32, a.Lxdb + cx * n, cc, n);
+            }
+            cp_commit();
             // up to two blocks of four rows, then the abandon test
 #pragma unroll 1
             for (int blk = 0; blk < 2; ++blk) {
                 if (i + 4 > n) break;
                 const float x4[4] = {xv[0], xv[1], xv[2], xv[3]};
-                if (casc) {  // LB_Keogh terms of these 4 rows; envelope of the next block in flight
-                    rest -= row_lb<P>(x4[0], uc[0], lc[0]) + row_lb<P>(x4[1], uc[1], lc[1]) +
-                            row_lb<P>(x4[2], uc[2], lc[2]) + row_lb<P>(x4[3], uc[3], lc[3]);
-                    const int inx = i + 4;
-                    if ((n & 3) == 0) {
-                        if (inx < n) {
-                            const float4 uu = __ldg(reinterpret_cast<const float4 *>(ur + inx));
-                            const float4 ll = __ldg(reinterpret_cast<const float4 *>(lr + inx));
-                            uc[0] = uu.x; uc[1] = uu.y; uc[2] = uu.z; uc[3] = uu.w;
-                            lc[0] = ll.x; lc[1] = ll.y; lc[2] = ll.z; lc[3] = ll.w;
-                        }
-                    } else {
-#pragma unroll
-                        for (int t = 0; t < 4; ++t) {
-                            uc[t] = inx + t < n ? __ldg(ur + inx + t) : 0.f;
-                            lc[t] = inx + t < n ? __ldg(lr + inx + t) : 0.f;
-                        }
-                    }
-                }
                 four_rows<WB, P, EXACT>(B, Y, x4, w2);
                 i += 4;
 #pragma unroll
@@ -674,7 +705,6 @@ dtw4_kernel(DtwArgs a) {
             }
             if (i + 4 > n && i < n && i - i0 < 8) {  // tail rows (n % 4 != 0): one row at a time
                 while (i < n) {
-                    if (casc) rest -= row_lb<P>(__ldg(xr + i), __ldg(ur + i), __ldg(lr + i));
                     float prev = kInf;
 #pragma unroll
                     for (int d = 0; d < NB; ++d) {
@@ -689,9 +719,31 @@ dtw4_kernel(DtwArgs a) {
                     Y[NY - 1] = __ldg(yr + (kYPadL - w - sh) + i + NY - 1);
                 }
             }
+            rows_done += (unsigned)(i - i0);
+            cp_wait<0>();
+            {
+                const float4 x0 = *reinterpret_cast<const float4 *>(slot + XA);
+                const float4 x1 = *reinterpret_cast<const float4 *>(slot + XA + 4);
+                xv[0] = x0.x; xv[1] = x0.y; xv[2] = x0.z; xv[3] = x0.w;
+                xv[4] = x1.x; xv[5] = x1.y; xv[6] = x1.z; xv[7] = x1.w;
+            }
+            if (casc2) {
+                // the columns [C(i0), C(i)) may have been visited by the rows just computed; the
+                // columns >= C(i) only by rows >= i (reading c21)
+                const int ncol = i - i0;  // 4 or 8 (n % 4 == 0)
 #pragma unroll
-            for (int t = 0; t < 8; ++t) xv[t] = xn[t];
-            rows_done += (unsigned long long)(i - i0);
+                for (int h = 0; h < 2; ++h) {
+                    if (4 * h < ncol) {
+                        const float4 yv = *reinterpret_cast<const float4 *>(slot + 4 * h);
+                        const float4 lu = *reinterpret_cast<const float4 *>(slot + 8 + 4 * h);
+                        const float4 ul = *reinterpret_cast<const float4 *>(slot + 16 + 4 * h);
+                        const float4 ux = *reinterpret_cast<const float4 *>(slot + 24 + 4 * h);
+                        const float4 lx = *reinterpret_cast<const float4 *>(slot + 32 + 4 * h);
+                        rest -= col_lb<P>(yv.x, ux.x, lx.x, lu.x, ul.x) + col_lb<P>(yv.y, ux.y, lx.y, lu.y, ul.y) +
+                                col_lb<P>(yv.z, ux.z, lx.z, lu.z, ul.z) + col_lb<P>(yv.w, ux.w, lx.w, lu.w, ul.w);
+                    }
+                }
+            }
             // ---- (d) finished or abandoned lanes become free ----
             if (i >= n) {
                 float r = B[WB];
@@ -706,7 +758,7 @@ dtw4_kernel(DtwArgs a) {
             } else {
                 if (band_min<WB>(B) + rest > thr) {
                     if constexpr (!WALK) a.res[item] = kInf;
-                    ++n_abandon;  // early abandon (readings c15, c19)
+                    ++n_abandon;  // early abandon (readings c15, c19, c21)
                     st = kFree;
                 }
             }
@@ -718,7 +770,7 @@ dtw4_kernel(DtwArgs a) {
         }
     }
     if (a.cells) {
-        unsigned long long cells = rows_done * (unsigned long long)(2 * w + 1);
+        unsigned long long cells = (unsigned long long)rows_done * (unsigned long long)(2 * w + 1);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) cells += __shfl_xor_sync(0xffffffffu, cells, o);
         if (lane == 0) atomicAdd(a.cells, cells);
@@ -726,12 +778,12 @@ dtw4_kernel(DtwArgs a) {
     if (a.started) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) n_started += __shfl_xor_sync(0xffffffffu, n_started, o);
-        if (lane == 0 && n_started) atomicAdd(a.started, n_started);
+        if (lane == 0 && n_started) atomicAdd(a.started, (unsigned long long)n_started);
     }
     if (a.abandoned) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) n_abandon += __shfl_xor_sync(0xffffffffu, n_abandon, o);
-        if (lane == 0 && n_abandon) atomicAdd(a.abandoned, n_abandon);
+        if (lane == 0 && n_abandon) atomicAdd(a.abandoned, (unsigned long long)n_abandon);
     }
 }
 

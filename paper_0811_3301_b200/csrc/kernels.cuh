@@ -113,6 +113,14 @@ struct DtwArgs {
     const __half *b1h;
     int64_t ldb;
     const float *Uq, *Lq;
+    // row+column cascade (reading c21; dtw4_kernel, col_c0 > 0, with b1h): besides the rows'
+    // LB_Keogh terms, rest holds the LB_Improved column terms beta2_j of the columns the
+    // remaining rows must still visit; their total is key - next_up(|b1h|) (a lower bound of
+    // beta2), the columns [0, C(i)), C(i) = min(n, i + col_c0), col_c0 = round_up(w, 4),
+    // are subtracted (up to 16 per 8-row step; the column part joins the abandon test once
+    // caught up).  yq, LUq, ULq: [Qb][n] y, U(L(y)), L(U(y)); Uxdb, Lxdb: [N][n] U(x), L(x).
+    int col_c0;
+    const float *yq, *LUq, *ULq, *Uxdb, *Lxdb;
     // WALK: completed pairs are merged into the query's top-k (keys (DTW^p bits << 32 | c),
     // ascending, [Qb][k]) under a per-query lock, and thr[q] follows the k-th key
     unsigned long long *topk;

@@ -179,6 +179,52 @@ __global__ void __launch_bounds__(kSortThreads) sort_runs_kernel(unsigned long l
     }
 }
 
+// Row+column cascade start values (reading c21) of the keys appended in this
+// range: the gate slot of pair (q, c) takes -rd(LB_Improved^p - sum_{j < c0} beta2_j), beta2_j
+// = d(y_j, [L(H)_j, U(H)_j])^p by the closed form of improved.cu.  One CTA per sorted run;
+// a warp takes four keys at a time, lane l & 7 covers the columns 4 (l & 7) .. + 3 (c0 <= 32).
+template <int P>
+__global__ void __launch_bounds__(256) rest0_kernel(const unsigned long long *__restrict__ list, int64_t cap,
+                                                    const int *__restrict__ run_q, const int *__restrict__ run_idx,
+                                                    const int *__restrict__ len, const float *__restrict__ yq,
+                                                    const float *__restrict__ LUq, const float *__restrict__ ULq,
+                                                    const float *__restrict__ Ux, const float *__restrict__ Lx, int n,
+                                                    int c0, __half *__restrict__ gate, int64_t ldb) {
+    const int q = run_q[blockIdx.x], r = run_idx[blockIdx.x];
+    const int m = min(kRun, len[q] - r * kRun);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, src = lane & 7, grp = lane >> 3;
+    const bool mine = 4 * src < c0;
+    float4 y = make_float4(0.f, 0.f, 0.f, 0.f), lu = y, ul = y;
+    if (mine) {
+        y = __ldg(reinterpret_cast<const float4 *>(yq + (int64_t)q * n + 4 * src));
+        lu = __ldg(reinterpret_cast<const float4 *>(LUq + (int64_t)q * n + 4 * src));
+        ul = __ldg(reinterpret_cast<const float4 *>(ULq + (int64_t)q * n + 4 * src));
+    }
+    const unsigned long long *lq = list + (int64_t)q * cap + (int64_t)r * kRun;
+    for (int j0 = warp * 4; j0 < m; j0 += (blockDim.x >> 5) * 4) {
+        const int j = j0 + grp;
+        float s = 0.f, beta = 0.f;
+        uint32_t c = 0;
+        if (j < m) {
+            const unsigned long long key = lq[j];
+            c = (uint32_t)(key & 0xffffffffu);
+            beta = __uint_as_float((uint32_t)(key >> 32));
+            if (mine) {
+                const float4 ux = __ldg(reinterpret_cast<const float4 *>(Ux + (int64_t)c * n + 4 * src));
+                const float4 lx = __ldg(reinterpret_cast<const float4 *>(Lx + (int64_t)c * n + 4 * src));
+                s = accp<P>(s, max3f(y.x - fmaxf(ux.x, lu.x), fminf(lx.x, ul.x) - y.x, 0.f));
+                s = accp<P>(s, max3f(y.y - fmaxf(ux.y, lu.y), fminf(lx.y, ul.y) - y.y, 0.f));
+                s = accp<P>(s, max3f(y.z - fmaxf(ux.z, lu.z), fminf(lx.z, ul.z) - y.z, 0.f));
+                s = accp<P>(s, max3f(y.w - fmaxf(ux.w, lu.w), fminf(lx.w, ul.w) - y.w, 0.f));
+            }
+        }
+        s += __shfl_xor_sync(0xffffffffu, s, 4);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        if (j < m && src == 0) gate[(int64_t)q * ldb + c] = __hneg(__float2half_rd(fmaxf(__fsub_rd(beta, s), 0.f)));
+    }
+}
+
 struct QState {
     float *thr;      // tau^p (1+eps) (+inf until k results)
     float *lo, *hi;  // current range of beta1
@@ -434,6 +480,12 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         DTWLB_TRY(launch_paa_env_sums(U, L, Q, n, qpaa, qpaa + (size_t)Q * Dp, st));
     }
     const bool generic_dtw = w > 64;
+    // row+column cascade of the w <= 32 DTW kernel (reading c21; C(i) = i + col_c0).  Off by
+    // default: at C5 it cuts the computed DTW cells by 31 % but the per-step column work and
+    // the rest0 pass cost as much as the cells save; DTWLB_COLCASC=1 enables it.
+    static const bool env_col = [] { const char *e = getenv("DTWLB_COLCASC"); return e && atoi(e); }();
+    const int col_c0 =
+        (prefilter && !keogh_only && cascade && env_col && w <= 32 && n % 4 == 0) ? (w + 3) / 4 * 4 : 0;
     const int LP = dtw_padded_len(n);
     float *ysh = nullptr;
     if (!generic_dtw) {
@@ -608,13 +660,22 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 for (int r = 0; r * kRun < h_len[q]; ++r) { run_q.push_back(q); run_idx.push_back(r); }
             static const bool nosort2 = [] { const char *e = getenv("DTWLB_NOSORT2"); return e && atoi(e); }();
             const bool sorted = !(nosort2 && macro > 0);
-            if (!run_q.empty() && sorted) {
+            if (!run_q.empty() && (sorted || col_c0 > 0)) {
                 const size_t nr = run_q.size();
                 DTWLB_TRY(wsget(S_COUNT, nr * 2 + 64, &d_runs));
                 DTWLB_CUDA(cudaMemcpyAsync(d_runs, run_q.data(), nr * 4, cudaMemcpyHostToDevice, st));
                 DTWLB_CUDA(cudaMemcpyAsync(d_runs + nr, run_idx.data(), nr * 4, cudaMemcpyHostToDevice, st));
-                sort_runs_kernel<<<(unsigned)nr, kSortThreads, 0, st>>>(list, cap, d_runs, d_runs + nr, s.len);
-                DTWLB_LAUNCH_CHECK();
+                if (sorted) {
+                    sort_runs_kernel<<<(unsigned)nr, kSortThreads, 0, st>>>(list, cap, d_runs, d_runs + nr, s.len);
+                    DTWLB_LAUNCH_CHECK();
+                }
+                if (col_c0 > 0) {  // row+column cascade start values (reading c21)
+                    auto rk = p == 1 ? rest0_kernel<1> : rest0_kernel<2>;
+                    rk<<<(unsigned)nr, 256, 0, st>>>(list, cap, d_runs, d_runs + nr, s.len, queries + qb0 * n,
+                                                     LU + qb0 * n, UL + qb0 * n, dbenv, dbenv + (size_t)N * n, n,
+                                                     col_c0, reinterpret_cast<__half *>(beta1), ldb);
+                    DTWLB_LAUNCH_CHECK();
+                }
             }
             if (stats) cudaEventRecord(ev[1], st);
             // ---- a5: DTW walk ----
@@ -666,6 +727,14 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                     da.ldb = ldb;
                     da.Uq = U + qb0 * n;
                     da.Lq = L + qb0 * n;
+                    if (col_c0 > 0) {
+                        da.col_c0 = col_c0;
+                        da.yq = queries + qb0 * n;
+                        da.LUq = LU + qb0 * n;
+                        da.ULq = UL + qb0 * n;
+                        da.Uxdb = dbenv;
+                        da.Lxdb = dbenv + (size_t)N * n;
+                    }
                 }
                 if (generic_dtw) DTWLB_TRY(launch_dtw_generic(da, queries + qb0 * n, scratch, p, true, st));
                 else {
