@@ -495,8 +495,9 @@ dtw4_kernel(DtwArgs a) {
                                       (NT / 32) * kChunk4) + wid * kChunk4;
     const int n = a.n, w = EXACT ? WB : a.w, w2 = 2 * w;
     const int sh = (kYPadL - w) & 3;  // alignment class of (i - w) for i % 4 == 0
-    const int64_t total = a.total;
+    const int64_t total = (WALK && a.dev_total) ? (int64_t)*a.dev_total : a.total;
     const int64_t nchunks = (total + kChunk4 - 1) / kChunk4;
+    if (total == 0) return;
     const unsigned lt = (1u << lane) - 1u;
 
     int cbeg = 0, cend = 0, cursor = 0;  // item indices (< 2^31: one walk round)

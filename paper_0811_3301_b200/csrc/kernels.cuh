@@ -100,7 +100,9 @@ struct DtwArgs {
     int64_t cap;
     int Qb;
     float *thr;            // [Qb] tau^p (1+eps); WALK: lowered by walk_result as the top-k fills
-    int64_t total;         // number of items
+    int64_t total;         // number of items (WALK with dev_total: an upper bound, see below)
+    const int *dev_total;  // WALK, w <= 32 kernel: if set, the round's item count is read here
+                           // (written by the plan kernel: no host round trip per walk round)
     float *res;            // [total] DTW^p, +inf if pruned/abandoned (PAIRS: rooted)
     unsigned long long *cells;  // stats: computed cells (may be NULL)
     unsigned long long *abandoned;  // stats (may be NULL)

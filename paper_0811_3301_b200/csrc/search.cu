@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include <cub/block/block_radix_sort.cuh>
@@ -76,7 +77,7 @@ std::mutex &ws_mutex() {
 
 enum Slot {
     S_QSTAGE, S_DBSTAGE, S_ENV, S_QPAD, S_YSH, S_DBENV, S_BETA1, S_LIST, S_RES, S_STATE, S_TOPK,
-    S_OUTSTAGE, S_SCRATCH, S_TMP, S_MASK, S_PAA, S_QPAA, S_RPAA, S_COUNT
+    S_OUTSTAGE, S_SCRATCH, S_TMP, S_MASK, S_PAA, S_QPAA, S_RPAA, S_SNAP, S_COUNT
 };
 
 template <typename T>
@@ -153,13 +154,55 @@ __global__ void __launch_bounds__(512) sample_threshold_kernel(const T *__restri
 // Non-negative float bits order like the floats; equal bounds keep their list order.
 constexpr int kRun = 4096;
 constexpr int kSortThreads = 512, kSortItems = kRun / kSortThreads;
+// Runs of the range's lists, built on the device (no host round trip): run t = (query,
+// index) with t over sum_q ceil(len_q / kRun); the count goes to *nruns.  One CTA.
+__global__ void __launch_bounds__(1024) make_runs_kernel(const int *__restrict__ len, int Qb, int *__restrict__ run_q,
+                                                         int *__restrict__ run_idx, int *__restrict__ nruns) {
+    __shared__ int warp_sums[32];
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int base = 0; base < Qb; base += blockDim.x) {
+        const int q = base + threadIdx.x;
+        const int m = q < Qb ? (len[q] + kRun - 1) / kRun : 0;
+        int v = m;  // inclusive scan
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += t;
+        }
+        if (lane == 31) warp_sums[wid] = v;
+        __syncthreads();
+        if (wid == 0) {
+            int u = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, u, o);
+                if (lane >= o) u += t;
+            }
+            warp_sums[lane] = u;
+        }
+        __syncthreads();
+        const int off = carry + v - m + (wid ? warp_sums[wid - 1] : 0);
+        for (int r = 0; r < m; ++r) { run_q[off + r] = q; run_idx[off + r] = r; }
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry = off + m;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *nruns = carry;
+}
+
 __global__ void __launch_bounds__(kSortThreads) sort_runs_kernel(unsigned long long *__restrict__ list, int64_t cap,
                                                                  const int *__restrict__ run_q,
                                                                  const int *__restrict__ run_idx,
-                                                                 const int *__restrict__ len) {
+                                                                 const int *__restrict__ len,
+                                                                 const int *__restrict__ nruns) {
     using BRS = cub::BlockRadixSort<unsigned, kSortThreads, kSortItems, unsigned>;
     __shared__ typename BRS::TempStorage tmp;
-    const int q = run_q[blockIdx.x], r = run_idx[blockIdx.x];
+    const int nr = *nruns;
+    for (int t = blockIdx.x; t < nr; t += gridDim.x) {
+    const int q = run_q[t], r = run_idx[t];
     const int64_t base = (int64_t)q * cap + (int64_t)r * kRun;
     const int m = min(kRun, len[q] - r * kRun);
     DCHECK(m > 0 && (int64_t)r * kRun + m <= cap, "sort q=%d r=%d m=%d cap=%lld", q, r, m, (long long)cap);
@@ -177,6 +220,8 @@ __global__ void __launch_bounds__(kSortThreads) sort_runs_kernel(unsigned long l
         const int i = threadIdx.x * kSortItems + j;
         if (i < m) list[base + i] = ((unsigned long long)key[j] << 32) | val[j];
     }
+    __syncthreads();  // temp storage reuse
+    }
 }
 
 // Row+column cascade start values (reading c21) of the keys appended in this
@@ -186,13 +231,16 @@ __global__ void __launch_bounds__(kSortThreads) sort_runs_kernel(unsigned long l
 template <int P>
 __global__ void __launch_bounds__(256) rest0_kernel(const unsigned long long *__restrict__ list, int64_t cap,
                                                     const int *__restrict__ run_q, const int *__restrict__ run_idx,
-                                                    const int *__restrict__ len, const float *__restrict__ yq,
+                                                    const int *__restrict__ len, const int *__restrict__ nruns,
+                                                    const float *__restrict__ yq,
                                                     const float *__restrict__ LUq, const float *__restrict__ ULq,
                                                     const float *__restrict__ Ux, const float *__restrict__ Lx, int n,
                                                     int c0, __half *__restrict__ gate, int64_t ldb) {
-    const int q = run_q[blockIdx.x], r = run_idx[blockIdx.x];
-    const int m = min(kRun, len[q] - r * kRun);
+    const int nr = *nruns;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, src = lane & 7, grp = lane >> 3;
+    for (int t = blockIdx.x; t < nr; t += gridDim.x) {
+    const int q = run_q[t], r = run_idx[t];
+    const int m = min(kRun, len[q] - r * kRun);
     const bool mine = 4 * src < c0;
     float4 y = make_float4(0.f, 0.f, 0.f, 0.f), lu = y, ul = y;
     if (mine) {
@@ -222,6 +270,7 @@ __global__ void __launch_bounds__(256) rest0_kernel(const unsigned long long *__
         s += __shfl_xor_sync(0xffffffffu, s, 2);
         s += __shfl_xor_sync(0xffffffffu, s, 1);
         if (j < m && src == 0) gate[(int64_t)q * ldb + c] = __hneg(__float2half_rd(fmaxf(__fsub_rd(beta, s), 0.f)));
+    }
     }
 }
 
@@ -268,6 +317,7 @@ __global__ void start_walk_kernel(QState s, int Qb) {
 // the warp chunks (kDtwIpw items each, never spanning two queries) that hold them.
 // Two exclusive scans: item_off (results layout) and chunk_off (warp -> query).
 constexpr int kD0 = 128, kDMax = 65536;
+constexpr int kRoundBatch = 4;  // walk rounds queued per host check (w <= 32 DTW kernel)
 __device__ __forceinline__ int2 block_scan2(int2 v, int2 *warp_sums, int2 &total) {
     // inclusive block-wide scan of two ints; returns the inclusive value, sets total
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -564,20 +614,30 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     const int R = std::min(kMaxRanges, std::max(2, env_R > 0 ? env_R : 2));
     const int G = std::max(2, env_G > 0 ? env_G : 8);
 
-    std::vector<int> h_len(Qb), run_q, run_idx;
+    // run lists of the sort: at most Qb * ceil(cap / kRun) runs of (query, index), + the count
+    const int64_t max_runs = Qb * ceil_div(cap, kRun);
     int *d_runs;
-    double ms_keogh = 0, ms_select = 0, ms_improved = 0, ms_dtw = 0;
-    unsigned long long r1[3] = {0, 0, 0}, r1_base[4] = {0, 0, 0, 0};
+    DTWLB_TRY(wsget(S_COUNT, (size_t)max_runs * 2 + 64, &d_runs));
+    int *d_nruns = d_runs + 2 * max_runs;
+    double ms_keogh = 0, ms_select = 0, ms_improved = 0, ms_dtw = 0, ms_survivor = 0;
     int64_t walk_rounds = 0;
-    cudaEvent_t ev[6];
-    double ms_survivor = 0;
-    if (stats) for (auto &e : ev) cudaEventCreate(&e);
+    // stats: CUDA-event spans resolved after the call's final synchronisation (no host waits
+    // inside the pipeline); the range-1 counters are device-to-device snapshots
+    std::vector<cudaEvent_t> evpool;
+    std::vector<std::tuple<cudaEvent_t, cudaEvent_t, double *>> spans;
+    auto new_ev = [&]() { cudaEvent_t e; cudaEventCreate(&e); evpool.push_back(e); return e; };
+    auto rec = [&]() { cudaEvent_t e = new_ev(); cudaEventRecord(e, st); return e; };
+    auto span = [&](cudaEvent_t a, cudaEvent_t b, double *acc) { spans.emplace_back(a, b, acc); };
+    const int64_t nblocks = ceil_div(Q, Qb);
+    unsigned long long *snap = nullptr;  // [nblocks][2][4]: stat after range 1, after the last range
+    if (stats) DTWLB_TRY(wsget(S_SNAP, (size_t)nblocks * 8, &snap));
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
 
     for (int64_t qb0 = 0; qb0 < Q; qb0 += Qb) {
         const int64_t qn = std::min<int64_t>(Qb, Q - qb0);
         // ---- dense gate pass for the block: the piecewise-sum bound beta0 (pre-filter,
         //      LB_Keogh then runs on its survivors inside the survivor pass), or a2 itself ----
-        if (stats) cudaEventRecord(ev[0], st);
+        if (stats) ev0 = rec();
         if (prefilter) {
             DTWLB_TRY(launch_paa_bound(qpaa + qb0 * Dp, qpaa + (size_t)Q * Dp + qb0 * Dp, xpaa,
                                        xpaa + (size_t)N * Dp, qn, N, n, p, false, beta1, ldb, st));
@@ -587,7 +647,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                                            rpaa + (size_t)N * Dp, qn, N, n, p, false, beta1, ldb, st));
         } else
             DTWLB_TRY(launch_keogh(U + qb0 * n, L + qb0 * n, db, qn, N, n, p, false, beta1, ldb, st));
-        if (stats) cudaEventRecord(ev[1], st);
+        if (stats) ev1 = rec();
         init_state_kernel<<<(unsigned)ceil_div(qn, 256), 256, 0, st>>>(s, (int)qn, k);
         DTWLB_LAUNCH_CHECK();
         if (prefilter)
@@ -597,19 +657,15 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
             sample_threshold_kernel<float><<<(unsigned)qn, 512, 0, st>>>(beta1, ldb, N, S, R, G, s.tS, (int)qn);
         DTWLB_LAUNCH_CHECK();
         if (stats) {
-            cudaEventRecord(ev[2], st);
-            cudaEventSynchronize(ev[2]);
-            float a = 0, b = 0;
-            cudaEventElapsedTime(&a, ev[0], ev[1]);
-            cudaEventElapsedTime(&b, ev[1], ev[2]);
-            ms_keogh += a;
-            ms_select += b;
+            const cudaEvent_t e2 = rec();
+            span(ev0, ev1, &ms_keogh);
+            span(ev1, e2, &ms_select);
         }
 
         for (int macro = 0; macro < R; ++macro) {
             set_range_kernel<<<(unsigned)ceil_div(qn, 256), 256, 0, st>>>(s, (int)qn, macro, R);
             DTWLB_LAUNCH_CHECK();
-            if (stats) cudaEventRecord(ev[0], st);
+            if (stats) ev0 = rec();
             // ---- a4: LB_Improved on the range's LB_Keogh survivors ----
             if (fast_improved) {
                 ImprovedArgs ia{};
@@ -639,109 +695,114 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 ia.cap = cap;
                 ia.list_len = s.len;
                 ia.n_eval = s.stat + 0;
-                if (stats) { ia.ev0 = ev[4]; ia.ev1 = ev[5]; }
+                if (stats) { ev_s0 = new_ev(); ev_s1 = new_ev(); ia.ev0 = ev_s0; ia.ev1 = ev_s1; }
                 improved_scratch_bind(ia, imp_scratch);
                 DTWLB_TRY(launch_improved(ia, p, keogh_only, false, st));
             } else {
                 set_error(DTWLB_EUNSUPPORTED, "nn_search: n = %d > 1024 not supported", n);
                 return DTWLB_EUNSUPPORTED;
             }
-            // ---- a3: sort each query's list in runs ----
-            DTWLB_CUDA(cudaMemcpyAsync(h_len.data(), s.len, sizeof(int) * qn, cudaMemcpyDeviceToHost, st));
-            DTWLB_CUDA(cudaStreamSynchronize(st));
-            if (stats) {
-                float t = 0;
-                cudaEventElapsedTime(&t, ev[4], ev[5]);
-                ms_survivor += t;
-            }
-            run_q.clear();
-            run_idx.clear();
-            for (int q = 0; q < qn; ++q)
-                for (int r = 0; r * kRun < h_len[q]; ++r) { run_q.push_back(q); run_idx.push_back(r); }
+            // ---- a3: sort each query's list in runs (run list built on the device) ----
+            if (stats) span(ev_s0, ev_s1, &ms_survivor);
             static const bool nosort2 = [] { const char *e = getenv("DTWLB_NOSORT2"); return e && atoi(e); }();
             const bool sorted = !(nosort2 && macro > 0);
-            if (!run_q.empty() && (sorted || col_c0 > 0)) {
-                const size_t nr = run_q.size();
-                DTWLB_TRY(wsget(S_COUNT, nr * 2 + 64, &d_runs));
-                DTWLB_CUDA(cudaMemcpyAsync(d_runs, run_q.data(), nr * 4, cudaMemcpyHostToDevice, st));
-                DTWLB_CUDA(cudaMemcpyAsync(d_runs + nr, run_idx.data(), nr * 4, cudaMemcpyHostToDevice, st));
+            if (sorted || col_c0 > 0) {
+                make_runs_kernel<<<1, 1024, 0, st>>>(s.len, (int)qn, d_runs, d_runs + max_runs, d_nruns);
+                DTWLB_LAUNCH_CHECK();
+                const unsigned grid = (unsigned)std::min<int64_t>(max_runs, 148 * 8);
                 if (sorted) {
-                    sort_runs_kernel<<<(unsigned)nr, kSortThreads, 0, st>>>(list, cap, d_runs, d_runs + nr, s.len);
+                    sort_runs_kernel<<<grid, kSortThreads, 0, st>>>(list, cap, d_runs, d_runs + max_runs, s.len,
+                                                                    d_nruns);
                     DTWLB_LAUNCH_CHECK();
                 }
                 if (col_c0 > 0) {  // row+column cascade start values (reading c21)
                     auto rk = p == 1 ? rest0_kernel<1> : rest0_kernel<2>;
-                    rk<<<(unsigned)nr, 256, 0, st>>>(list, cap, d_runs, d_runs + nr, s.len, queries + qb0 * n,
-                                                     LU + qb0 * n, UL + qb0 * n, dbenv, dbenv + (size_t)N * n, n,
-                                                     col_c0, reinterpret_cast<__half *>(beta1), ldb);
+                    rk<<<grid, 256, 0, st>>>(list, cap, d_runs, d_runs + max_runs, s.len, d_nruns, queries + qb0 * n,
+                                             LU + qb0 * n, UL + qb0 * n, dbenv, dbenv + (size_t)N * n, n, col_c0,
+                                             reinterpret_cast<__half *>(beta1), ldb);
                     DTWLB_LAUNCH_CHECK();
                 }
             }
-            if (stats) cudaEventRecord(ev[1], st);
+            if (stats) ev1 = rec();
             // ---- a5: DTW walk ----
             start_walk_kernel<<<(unsigned)ceil_div(qn, 256), 256, 0, st>>>(s, (int)qn);
             DTWLB_LAUNCH_CHECK();
-            for (int round = 0;; ++round) {
-                ++walk_rounds;
-                static const int env_d0 = [] { const char *e = getenv("DTWLB_D0"); return e ? atoi(e) : 0; }();
-                plan_kernel<<<1, 1024, 0, st>>>(s, (int)qn, list, cap, sorted, env_d0 > 0 ? env_d0 : kD0);
-                DTWLB_LAUNCH_CHECK();
-                int tot2[2] = {0, 0};
-                DTWLB_CUDA(cudaMemcpyAsync(tot2, s.counters, sizeof(tot2), cudaMemcpyDeviceToHost, st));
-                DTWLB_CUDA(cudaStreamSynchronize(st));
-                const int total = tot2[0];
-                if (total == 0) break;
-                DtwArgs da{};
-                da.ysh = ysh;
-                da.ysh_stride_s = (int64_t)Q * LP;
-                da.LP = LP;
-                da.db = db;
-                da.Ndb = N;
-                da.n = n;
-                da.w = w;
-                da.item_off = s.item_off;
-                da.chunk_off = s.chunk_off;
-                da.nchunks = tot2[1];
-                da.pos = s.pos;
-                da.list = list;
-                da.cap = cap;
-                da.Qb = (int)qn;
-                da.thr = s.thr;
-                da.topk = s.topk;
-                da.topk_lock = s.lock;
-                da.k = k;
-                da.eps = eps;
-                da.rkey = reinterpret_cast<unsigned long long *>(rbuf);
-                da.rq = reinterpret_cast<int *>(rbuf + (size_t)res_cap * 8);
-                da.rcount = reinterpret_cast<unsigned *>(s.counters + 6);
-                da.rcap = res_cap;
-                DTWLB_CUDA(cudaMemsetAsync(da.rcount, 0, sizeof(unsigned), st));
-                da.total = total;
-                da.cells = s.stat + 2;
-                da.abandoned = s.stat + 3;
-                da.started = s.stat + 1;
-                da.queue = reinterpret_cast<unsigned *>(s.counters + 4);
-                if (cascade) {  // cascading abandon with the pair's LB_Keogh row terms
-                    if (prefilter) da.b1h = reinterpret_cast<const __half *>(beta1);
-                    else da.b1 = beta1;
-                    da.ldb = ldb;
-                    da.Uq = U + qb0 * n;
-                    da.Lq = L + qb0 * n;
-                    if (col_c0 > 0) {
-                        da.col_c0 = col_c0;
-                        da.yq = queries + qb0 * n;
-                        da.LUq = LU + qb0 * n;
-                        da.ULq = UL + qb0 * n;
-                        da.Uxdb = dbenv;
-                        da.Lxdb = dbenv + (size_t)N * n;
+            // The w <= 32 DTW kernel reads each round's item count from device memory (written by
+            // the plan kernel), so rounds are queued in batches of kRoundBatch with one host
+            // check per batch; the other DTW kernels size their grids from it (one check per round).
+            const bool dev_rounds = !generic_dtw && w <= 32;
+            const int batch = dev_rounds ? kRoundBatch : 1;
+            for (bool walking = true; walking;) {
+                for (int b = 0; b < batch && walking; ++b) {
+                    ++walk_rounds;
+                    static const int env_d0 = [] { const char *e = getenv("DTWLB_D0"); return e ? atoi(e) : 0; }();
+                    plan_kernel<<<1, 1024, 0, st>>>(s, (int)qn, list, cap, sorted, env_d0 > 0 ? env_d0 : kD0);
+                    DTWLB_LAUNCH_CHECK();
+                    int tot2[2] = {0, 0};
+                    if (!dev_rounds) {
+                        DTWLB_CUDA(cudaMemcpyAsync(tot2, s.counters, sizeof(tot2), cudaMemcpyDeviceToHost, st));
+                        DTWLB_CUDA(cudaStreamSynchronize(st));
+                        if (tot2[0] == 0) { walking = false; break; }
                     }
+                    DtwArgs da{};
+                    da.ysh = ysh;
+                    da.ysh_stride_s = (int64_t)Q * LP;
+                    da.LP = LP;
+                    da.db = db;
+                    da.Ndb = N;
+                    da.n = n;
+                    da.w = w;
+                    da.item_off = s.item_off;
+                    da.chunk_off = s.chunk_off;
+                    da.nchunks = tot2[1];
+                    da.pos = s.pos;
+                    da.list = list;
+                    da.cap = cap;
+                    da.Qb = (int)qn;
+                    da.thr = s.thr;
+                    da.topk = s.topk;
+                    da.topk_lock = s.lock;
+                    da.k = k;
+                    da.eps = eps;
+                    da.rkey = reinterpret_cast<unsigned long long *>(rbuf);
+                    da.rq = reinterpret_cast<int *>(rbuf + (size_t)res_cap * 8);
+                    da.rcount = reinterpret_cast<unsigned *>(s.counters + 6);
+                    da.rcap = res_cap;
+                    DTWLB_CUDA(cudaMemsetAsync(da.rcount, 0, sizeof(unsigned), st));
+                    da.total = dev_rounds ? res_cap : tot2[0];  // (dev_rounds: grid bound only)
+                    da.dev_total = dev_rounds ? s.counters : nullptr;
+                    da.cells = s.stat + 2;
+                    da.abandoned = s.stat + 3;
+                    da.started = s.stat + 1;
+                    da.queue = reinterpret_cast<unsigned *>(s.counters + 4);
+                    if (cascade) {  // cascading abandon with the pair's LB_Keogh row terms
+                        if (prefilter) da.b1h = reinterpret_cast<const __half *>(beta1);
+                        else da.b1 = beta1;
+                        da.ldb = ldb;
+                        da.Uq = U + qb0 * n;
+                        da.Lq = L + qb0 * n;
+                        if (col_c0 > 0) {
+                            da.col_c0 = col_c0;
+                            da.yq = queries + qb0 * n;
+                            da.LUq = LU + qb0 * n;
+                            da.ULq = UL + qb0 * n;
+                            da.Uxdb = dbenv;
+                            da.Lxdb = dbenv + (size_t)N * n;
+                        }
+                    }
+                    if (generic_dtw) DTWLB_TRY(launch_dtw_generic(da, queries + qb0 * n, scratch, p, true, st));
+                    else {
+                        da.ysh = ysh + qb0 * LP;
+                        DTWLB_TRY(launch_dtw(da, p, true, st));
+                    }
+                    DTWLB_TRY(launch_topk_merge(da, st));  // a6: the round's completed pairs -> top-k, tau
                 }
-                if (generic_dtw) DTWLB_TRY(launch_dtw_generic(da, queries + qb0 * n, scratch, p, true, st));
-                else {
-                    da.ysh = ysh + qb0 * LP;
-                    DTWLB_TRY(launch_dtw(da, p, true, st));
+                if (dev_rounds && walking) {  // one host check per batch: did the last round have items?
+                    int tot0 = 0;
+                    DTWLB_CUDA(cudaMemcpyAsync(&tot0, s.counters, sizeof(int), cudaMemcpyDeviceToHost, st));
+                    DTWLB_CUDA(cudaStreamSynchronize(st));
+                    walking = tot0 > 0;
                 }
-                DTWLB_TRY(launch_topk_merge(da, st));  // a6: the round's completed pairs -> top-k, tau
             }
             if (opts && opts->exchange && macro + 1 < R) {
                 // a7: shard threshold exchange after the best-first range (stream-ordered)
@@ -749,22 +810,12 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 DTWLB_CUDA(cudaGetLastError());
             }
             if (stats) {
-                cudaEventRecord(ev[2], st);
-                cudaEventSynchronize(ev[2]);
-                float a = 0, b = 0;
-                cudaEventElapsedTime(&a, ev[0], ev[1]);
-                cudaEventElapsedTime(&b, ev[1], ev[2]);
-                ms_improved += a;
-                ms_dtw += b;
-                if (macro == 0) {  // cumulative counters after range 1 (diagnostics)
-                    unsigned long long h[4];
-                    cudaMemcpy(h, s.stat, sizeof(h), cudaMemcpyDeviceToHost);
-                    r1[0] += h[0] - r1_base[0];
-                    r1[1] += h[1] - r1_base[1];
-                    r1[2] += h[2] - r1_base[2];
-                } else {
-                    cudaMemcpy(r1_base, s.stat, sizeof(r1_base), cudaMemcpyDeviceToHost);
-                }
+                const cudaEvent_t e2 = rec();
+                span(ev0, ev1, &ms_improved);
+                span(ev1, e2, &ms_dtw);
+                if (macro == 0 || macro == R - 1)  // cumulative counters after range 1 / the block
+                    DTWLB_CUDA(cudaMemcpyAsync(snap + (qb0 / Qb) * 8 + (macro == 0 ? 0 : 4), s.stat, 32,
+                                               cudaMemcpyDeviceToDevice, st));
             }
         }
         finalize_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(qn * k, 256), 4096)), 256, 0, st>>>(
@@ -778,7 +829,17 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     tm.mark();  // 2
     DTWLB_CUDA(cudaStreamSynchronize(st));
     if (stats) {
-        for (auto &e : ev) cudaEventDestroy(e);
+        for (auto &sp : spans) {
+            float t = 0;
+            cudaEventElapsedTime(&t, std::get<0>(sp), std::get<1>(sp));
+            *std::get<2>(sp) += t;
+        }
+        for (auto &e : evpool) cudaEventDestroy(e);
+        std::vector<unsigned long long> hs((size_t)nblocks * 8);
+        DTWLB_CUDA(cudaMemcpy(hs.data(), snap, hs.size() * 8, cudaMemcpyDeviceToHost));
+        unsigned long long r1[3] = {0, 0, 0};
+        for (int64_t b = 0; b < nblocks; ++b)
+            for (int j = 0; j < 3; ++j) r1[j] += hs[b * 8 + j] - (b ? hs[(b - 1) * 8 + 4 + j] : 0ull);
         unsigned long long h[8];
         DTWLB_CUDA(cudaMemcpy(h, s.stat, sizeof(h), cudaMemcpyDeviceToHost));
         stats->pairs = Q * N;
