@@ -317,6 +317,7 @@ __global__ void start_walk_kernel(QState s, int Qb) {
 // the warp chunks (kDtwIpw items each, never spanning two queries) that hold them.
 // Two exclusive scans: item_off (results layout) and chunk_off (warp -> query).
 constexpr int kD0 = 128, kDMax = 65536;
+constexpr int kSeedCap = 2048;   // cap of the best-first seed range size S (nn_search)
 constexpr int kRoundBatch = 4;  // walk rounds queued per host check (w <= 32 DTW kernel)
 __device__ __forceinline__ int2 block_scan2(int2 v, int2 *warp_sums, int2 &total) {
     // inclusive block-wide scan of two ints; returns the inclusive value, sets total
@@ -606,8 +607,13 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     if (generic_dtw) DTWLB_TRY(wsget(S_SCRATCH, (size_t)res_cap * (2 * w + 2), &scratch));
     DTWLB_CUDA(cudaMemsetAsync(s.stat, 0, 8 * 8, st));
 
-    // target size of the first (best-first) range
-    const int64_t S = std::max<int64_t>(std::max<int64_t>(256, 4LL * k), std::min<int64_t>(8192, N / 64));
+    // target size of the first (best-first) range: ~kSeedCap candidates per query.  Measured at
+    // C5 (ms/step): 8192 -> 323, 4096 -> 310, 2048 -> 304, 1536 -> 303, 1024 -> 302-322; three
+    // ranges were slower (326-338): the seed range's survivor pass is dominated by per-entry
+    // cost (about one survivor per (query, 64-tile) entry), so a smaller seed is cheaper
+    static const int env_S = [] { const char *e = getenv("DTWLB_SEED"); return e ? atoi(e) : 0; }();
+    const int64_t S = std::max<int64_t>(std::max<int64_t>(256, 4LL * k),
+                                        std::min<int64_t>(env_S > 0 ? env_S : kSeedCap, N / 64));
     // number of ranges R and the growth G of their sampled sizes (S, S*G, S*G^2, ..., rest)
     static const int env_R = [] { const char *e = getenv("DTWLB_RANGES"); return e ? atoi(e) : 0; }();
     static const int env_G = [] { const char *e = getenv("DTWLB_RANGE_GROWTH"); return e ? atoi(e) : 0; }();
@@ -828,6 +834,14 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     }
     tm.mark();  // 2
     DTWLB_CUDA(cudaStreamSynchronize(st));
+    static const bool dbg_spans = [] { const char *e = getenv("DTWLB_DEBUG_SPANS"); return e && atoi(e); }();
+    if (stats && dbg_spans) {  // uncovered device time between consecutive spans (debug)
+        for (size_t t = 0; t + 1 < evpool.size(); ++t) {
+            float g = 0;
+            if (cudaEventElapsedTime(&g, evpool[t], evpool[t + 1]) == cudaSuccess && g > 0.5f)
+                fprintf(stderr, "[dtwlb] events %zu -> %zu: %.2f ms\n", t, t + 1, g);
+        }
+    }
     if (stats) {
         for (auto &sp : spans) {
             float t = 0;
