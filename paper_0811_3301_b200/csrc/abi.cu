@@ -179,7 +179,7 @@ int lb_improved(const float *q, const float *q_env, const float *db, int64_t Q, 
     std::lock_guard<std::mutex> lock(api_mutex());
     cudaStream_t st = as_stream(stream);
     const int npadE = 32 * epl;
-    const int64_t ldb = (N + 3) / 4 * 4;
+    const int64_t ldb = (N + 7) / 8 * 8;  // 16-byte rows of the fp16 gate block
     float *beta1, *env, *qpad, *dbenv;
     DTWLB_TRY(ws_get_bytes(0, sizeof(float) * Q * ldb, (void **)&beta1));
     DTWLB_TRY(ws_get_bytes(1, sizeof(float) * 3 * Q * n, (void **)&env));

@@ -121,6 +121,79 @@ select_mask_kernel(const T *__restrict__ gate, int64_t ldb, int64_t Qb, int64_t 
     }
 }
 
+// fp16 gate block (the pre-filtered cascade): one warp per (256-candidate super-tile, block
+// of 32 queries); lane l reads candidates 8l .. 8l+7 of the super-tile (one 16-byte vector
+// per query row: 512 bytes per row per warp, eight rows in flight), eight ballots per row;
+// lane j keeps query j's ballots and turns them into the four 64-bit tile masks (candidate
+// 64t + 8m + k = bit 8m + k of tile t: byte t of ballot k, spread to bits 8m).
+__device__ __forceinline__ unsigned long long spread8(unsigned x) {  // bit m -> bit 8m
+    unsigned long long v = x & 0xffu;
+    v = (v | (v << 28)) & 0x0000000F0000000Full;
+    v = (v | (v << 14)) & 0x0003000300030003ull;
+    v = (v | (v << 7)) & 0x0101010101010101ull;
+    return v;
+}
+
+__global__ void __launch_bounds__(256)
+select_mask8_kernel(const __half *__restrict__ gate, int64_t ldb, int64_t Qb, int64_t N,
+                    const float *__restrict__ lo, const float *__restrict__ hi, const float *__restrict__ thr,
+                    bool all, unsigned long long *__restrict__ tile_m, int *__restrict__ tile_q,
+                    int *__restrict__ tile_cnt, int64_t ntiles) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nst = (ntiles + 3) / 4;
+    const int64_t sti = gw % nst;  // super-tile
+    const int64_t qb = gw / nst;   // block of 32 queries
+    const int64_t q0 = qb * 32;
+    if (q0 >= Qb) return;
+    const int nq = Qb - q0 < 32 ? (int)(Qb - q0) : 32;
+    float my_l = -kInf, my_h = kInf;
+    if (!all && lane < nq) {
+        if (lo) my_l = lo[q0 + lane];
+        if (hi) my_h = hi[q0 + lane];
+        if (thr) my_h = fminf(my_h, thr[q0 + lane]);
+    }
+    const int64_t c0 = sti * 256 + 8 * lane;  // this lane's 8 candidates (ldb % 8 == 0)
+    const bool inrow = c0 < ldb;
+    const int nvalid = c0 >= N ? 0 : (N - c0 >= 8 ? 8 : (int)(N - c0));
+    unsigned bk[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // query q0 + lane: ballot k (candidate 8l + k of lane l)
+#pragma unroll 8
+    for (int j = 0; j < nq; ++j) {
+        uint4 raw = make_uint4(0x7c007c00u, 0x7c007c00u, 0x7c007c00u, 0x7c007c00u);  // +inf
+        if (inrow) raw = __ldg(reinterpret_cast<const uint4 *>(gate + (q0 + j) * ldb + c0));
+        const float l = __shfl_sync(0xffffffffu, my_l, j), h = __shfl_sync(0xffffffffu, my_h, j);
+        const unsigned wv[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float v = __half2float(__ushort_as_half((unsigned short)((k & 1) ? wv[k >> 1] >> 16 : wv[k >> 1] & 0xffffu)));
+            // (test c < N explicitly: the +inf / padding must not pass a range whose hi is +inf)
+            const unsigned b = __ballot_sync(0xffffffffu, k < nvalid && v > l && v <= h);
+            if (lane == j) bk[k] = b;
+        }
+    }
+    unsigned long long m[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        m[t] = 0ull;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m[t] |= spread8(bk[k] >> (8 * t)) << k;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const int64_t tt = sti * 4 + t;
+        const unsigned has = __ballot_sync(0xffffffffu, m[t] != 0ull);
+        if (!has || tt >= ntiles) continue;
+        int base = 0;
+        if (lane == 0) base = atomicAdd(tile_cnt + tt, __popc(has));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (m[t]) {
+            const int pos = base + __popc(has & ((1u << lane) - 1u));
+            tile_q[tt * Qb + pos] = (int)(q0 + lane);
+            tile_m[tt * Qb + pos] = m[t];
+        }
+    }
+}
+
 // ---------------------------------------------------------------- survivor passes
 template <int EPL, bool B1X>
 struct ImpCfg {
@@ -682,7 +755,12 @@ int launch_improved(const ImprovedArgs &a, int p, bool keogh_only, bool dense, c
     {   // per-tile (query, survivor mask) lists into the caller-provided scratch
         DTWLB_CUDA(cudaMemsetAsync(a.tile_cnt, 0, sizeof(int) * ntiles, st));
         const int64_t warps = ntiles * ceil_div(a.Qb, 32);
-        if (a.gate_half)
+        if (a.gate_half && a.ldb % 8 == 0) {
+            const int64_t warps8 = ceil_div(ntiles, 4) * ceil_div(a.Qb, 32);
+            select_mask8_kernel<<<(unsigned)ceil_div(warps8 * 32, 256), 256, 0, st>>>(
+                static_cast<const __half *>(a.gate), a.ldb, a.Qb, a.N, a.lo, a.hi, a.thr, dense, a.tile_m, a.tile_q,
+                a.tile_cnt, ntiles);
+        } else if (a.gate_half)
             select_mask_kernel<__half><<<(unsigned)ceil_div(warps * 32, 256), 256, 0, st>>>(
                 static_cast<const __half *>(a.gate), a.ldb, a.Qb, a.N, a.lo, a.hi, a.thr, dense, a.tile_m, a.tile_q,
                 a.tile_cnt, ntiles);

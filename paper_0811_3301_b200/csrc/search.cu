@@ -569,7 +569,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         Qb = std::min<int64_t>(Qb, ceil_div(ceil_div(Q, nb), 64) * 64);
     }
     const int64_t cap = N;
-    const int64_t ldb = (N + 3) / 4 * 4;
+    const int64_t ldb = (N + 7) / 8 * 8;  // 16-byte rows of the fp16 gate block
 
     float *beta1;
     unsigned long long *list;
