@@ -437,7 +437,31 @@ improved_kernel(ImprovedArgs a, int Ct) {
     const unsigned long long ctmask = Ct == 64 ? ~0ull : ((1ull << Ct) - 1);
 
     // stage the tile: x padded with 0 (the query's padded U = +inf, L = -inf give d = 0);
-    // U(x) = +inf, L(x) = -inf padding gives d = 0 in phase 2
+    // U(x) = +inf, L(x) = -inf padding gives d = 0 in phase 2.  n % 4 == 0: 16-byte cp.async
+    // copies (all of a thread's copies in flight at once), pads by plain stores
+    if (n % 4 == 0) {
+        constexpr int V = NPAD / 4;
+        for (int t = threadIdx.x; t < Ct * V; t += NT) {
+            const int r = t / V, i = 4 * (t - r * V);
+            const int o = r * NPAD + i;
+            if (r < ct && i < n) {
+                const int64_t g = (c0 + r) * (int64_t)n + i;
+                if constexpr (B1X) cp_async16(sX + o, a.xdb + g, 16);
+                if constexpr (!KO) {
+                    cp_async16(sU + o, a.Ux + g, 16);
+                    cp_async16(sL + o, a.Lx + g, 16);
+                }
+            } else {
+                if constexpr (B1X) *reinterpret_cast<float4 *>(sX + o) = make_float4(0.f, 0.f, 0.f, 0.f);
+                if constexpr (!KO) {
+                    *reinterpret_cast<float4 *>(sU + o) = make_float4(kInf, kInf, kInf, kInf);
+                    *reinterpret_cast<float4 *>(sL + o) = make_float4(-kInf, -kInf, -kInf, -kInf);
+                }
+            }
+        }
+        cp_commit();
+        cp_wait<0>();
+    } else
     for (int t = threadIdx.x; t < Ct * NPAD; t += NT) {
         const int r = t / NPAD, i = t - r * NPAD;
         const bool ok = r < ct && i < n;

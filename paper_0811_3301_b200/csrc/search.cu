@@ -835,6 +835,13 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     tm.mark();  // 2
     DTWLB_CUDA(cudaStreamSynchronize(st));
     static const bool dbg_spans = [] { const char *e = getenv("DTWLB_DEBUG_SPANS"); return e && atoi(e); }();
+    if (stats && dbg_spans && !evpool.empty()) {
+        float g0 = 0, g1 = 0;
+        cudaEventElapsedTime(&g0, tm.e[1], evpool.front());
+        cudaEventElapsedTime(&g1, evpool.back(), tm.e[2]);
+        fprintf(stderr, "[dtwlb] setup->first span %.2f ms, last span->end %.2f ms, envelope %.2f ms\n", g0, g1,
+                tm.ms(0, 1));
+    }
     if (stats && dbg_spans) {  // uncovered device time between consecutive spans (debug)
         for (size_t t = 0; t + 1 < evpool.size(); ++t) {
             float g = 0;
