@@ -47,6 +47,7 @@ struct Workspace {
         ptr.clear();
         size.clear();
     }
+    size_t cur_size(int slot) const { return slot < (int)size.size() ? size[slot] : 0; }
     int get(int slot, size_t bytes, void **out) {
         if ((int)ptr.size() <= slot) { ptr.resize(slot + 1, nullptr); size.resize(slot + 1, 0); }
         bytes = std::max<size_t>(bytes, 256);
@@ -560,8 +561,13 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     // ---- query block size from free memory: gate bound (4N) + list (8N) per query ----
     size_t free_b = 0, total_b = 0;
     DTWLB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    // the block-sized slots this call would reuse count as free: the block size (hence the
+    // pipeline) is then the same on every call of a given problem, not smaller after the first
+    for (int sl : {S_BETA1, S_LIST, S_RES, S_MASK}) free_b += ws().cur_size(sl);
     const size_t per_q = (size_t)N * (prefilter ? 10 : 12) + 4096;  // gate (2 or 4 B) + list (8 B) per pair
-    int64_t Qb = opts && opts->query_block > 0 ? opts->query_block : (int64_t)(free_b * 0.45 / per_q);
+    static const double env_mem = [] { const char *e = getenv("DTWLB_BLOCK_MEM_FRAC"); return e ? atof(e) : 0.0; }();
+    const double mem_frac = env_mem > 0 ? env_mem : 0.45;
+    int64_t Qb = opts && opts->query_block > 0 ? opts->query_block : (int64_t)(free_b * mem_frac / per_q);
     Qb = std::max<int64_t>(1, std::min<int64_t>(Qb, Q));
     if (Qb >= 64) Qb = Qb / 64 * 64;
     if (!(opts && opts->query_block > 0) && Qb >= 64) {  // balance the blocks (e.g. 2 x 4096, not 7168 + 1024)
@@ -835,6 +841,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     tm.mark();  // 2
     DTWLB_CUDA(cudaStreamSynchronize(st));
     static const bool dbg_spans = [] { const char *e = getenv("DTWLB_DEBUG_SPANS"); return e && atoi(e); }();
+    if (stats && dbg_spans) fprintf(stderr, "[dtwlb] Q %lld N %lld: query block %lld\n", (long long)Q, (long long)N, (long long)Qb);
     if (stats && dbg_spans && !evpool.empty()) {
         float g0 = 0, g1 = 0;
         cudaEventElapsedTime(&g0, tm.e[1], evpool.front());
