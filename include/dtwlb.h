@@ -157,6 +157,8 @@ typedef struct nn_stats {
     int32_t reserved_;
     double ms_survivor_kernel;   /* device time of the survivor-pass kernels (LB_Keogh /
                                     LB_Improved on sparse pairs), part of ms_improved   */
+    double ms_dtw_kernel;        /* device time of the banded-DTW kernel launches of the
+                                    walk, part of ms_dtw                                */
 } nn_stats;
 
 /* Exact k-nearest-neighbour search under banded DTW_p: for each query y_q,

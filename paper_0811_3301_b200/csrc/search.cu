@@ -631,7 +631,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     int *d_runs;
     DTWLB_TRY(wsget(S_COUNT, (size_t)max_runs * 2 + 64, &d_runs));
     int *d_nruns = d_runs + 2 * max_runs;
-    double ms_keogh = 0, ms_select = 0, ms_improved = 0, ms_dtw = 0, ms_survivor = 0;
+    double ms_keogh = 0, ms_select = 0, ms_improved = 0, ms_dtw = 0, ms_survivor = 0, ms_dtw_kernel = 0;
     int64_t walk_rounds = 0;
     // stats: CUDA-event spans resolved after the call's final synchronisation (no host waits
     // inside the pipeline); the range-1 counters are device-to-device snapshots
@@ -805,7 +805,9 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                     if (generic_dtw) DTWLB_TRY(launch_dtw_generic(da, queries + qb0 * n, scratch, p, true, st));
                     else {
                         da.ysh = ysh + qb0 * LP;
+                        const cudaEvent_t d0 = stats ? rec() : nullptr;
                         DTWLB_TRY(launch_dtw(da, p, true, st));
+                        if (stats) span(d0, rec(), &ms_dtw_kernel);
                     }
                     DTWLB_TRY(launch_topk_merge(da, st));  // a6: the round's completed pairs -> top-k, tau
                 }
@@ -884,6 +886,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         stats->ms_select = ms_select;
         stats->ms_improved = ms_improved;
         stats->ms_survivor_kernel = ms_survivor;
+        stats->ms_dtw_kernel = ms_dtw_kernel;
         stats->ms_dtw = ms_dtw;
         stats->ms_total = tm.ms(0, 2);
         stats->kernel_launches = (int64_t)(__atomic_load_n(&g_launches, __ATOMIC_RELAXED) - launches0);
