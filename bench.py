@@ -53,10 +53,13 @@ class ClockSampler:
         self.lines = []
 
     def __enter__(self):
+        if os.environ.get("DTWLB_BENCH_NO_CLOCKS") == "1":  # (interference experiments only)
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", os.environ.get("DTWLB_BENCH_CLOCK_MS", "200")], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -403,8 +406,14 @@ def main():
                     help="Alg. 2 (LB_Keogh then DTW, no LB_Improved pass): the paper's comparison point")
     ap.add_argument("--no-prefilter", action="store_true",
                     help="LB_Keogh over every pair (Alg. 3 as printed) instead of the piecewise-sum pre-filter")
+    ap.add_argument("--w", type=int, default=None,
+                    help="override the config's band w (the paper's w sweep, P:832-856); the workload "
+                         "name gets a -w<w> suffix")
     args = ap.parse_args()
     cfg = datagen.CONFIGS[args.config]
+    if args.w is not None and args.w != cfg.w:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, w=args.w, name=f"{cfg.name}-w{args.w}")
     if args.impl == "reference":
         return run_reference(args, cfg)
     return run_ours(args, cfg)

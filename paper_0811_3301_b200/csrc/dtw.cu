@@ -807,6 +807,7 @@ __global__ void dtw_generic_kernel(DtwArgs a, const float *__restrict__ yraw, fl
         const float beta = __uint_as_float((uint32_t)(key >> 32));
         thr = *reinterpret_cast<volatile float *>(a.thr + lo);
         if (beta > thr) return;
+        if (a.started) atomicAdd(a.started, 1ull);
         xr = a.db + (int64_t)(key & 0xffffffffu) * n;
         yr = yraw + (int64_t)lo * n;
     } else {
@@ -829,9 +830,12 @@ __global__ void dtw_generic_kernel(DtwArgs a, const float *__restrict__ yraw, fl
         }
         if (rmin > thr) {
             if constexpr (!WALK) a.res[item] = kInf;
+            if (a.cells) atomicAdd(a.cells, (unsigned long long)(i + 1) * (unsigned long long)nb);
+            if (a.abandoned) atomicAdd(a.abandoned, 1ull);
             return;
         }
     }
+    if (a.cells) atomicAdd(a.cells, (unsigned long long)n * (unsigned long long)nb);
     if constexpr (WALK) {
         if (B[w] <= thr) {
             const unsigned pos = atomicAdd(a.rcount, 1u);

@@ -802,7 +802,11 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                             da.Lxdb = dbenv + (size_t)N * n;
                         }
                     }
-                    if (generic_dtw) DTWLB_TRY(launch_dtw_generic(da, queries + qb0 * n, scratch, p, true, st));
+                    if (generic_dtw) {
+                        const cudaEvent_t d0 = stats ? rec() : nullptr;
+                        DTWLB_TRY(launch_dtw_generic(da, queries + qb0 * n, scratch, p, true, st));
+                        if (stats) span(d0, rec(), &ms_dtw_kernel);
+                    }
                     else {
                         da.ysh = ysh + qb0 * LP;
                         const cudaEvent_t d0 = stats ? rec() : nullptr;
@@ -848,13 +852,16 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         float g0 = 0, g1 = 0;
         cudaEventElapsedTime(&g0, tm.e[1], evpool.front());
         cudaEventElapsedTime(&g1, evpool.back(), tm.e[2]);
-        fprintf(stderr, "[dtwlb] setup->first span %.2f ms, last span->end %.2f ms, envelope %.2f ms\n", g0, g1,
-                tm.ms(0, 1));
+        float gfl = 0, g12 = 0;
+        cudaEventElapsedTime(&gfl, evpool.front(), evpool.back());
+        cudaEventElapsedTime(&g12, tm.e[1], tm.e[2]);
+        fprintf(stderr, "[dtwlb] setup->first span %.2f ms, last span->end %.2f ms, envelope %.2f ms, first->last %.2f, "
+                "mark1->mark2 %.2f, total %.2f, %zu events\n", g0, g1, tm.ms(0, 1), gfl, g12, tm.ms(0, 2), evpool.size());
     }
     if (stats && dbg_spans) {  // uncovered device time between consecutive spans (debug)
         for (size_t t = 0; t + 1 < evpool.size(); ++t) {
             float g = 0;
-            if (cudaEventElapsedTime(&g, evpool[t], evpool[t + 1]) == cudaSuccess && g > 0.5f)
+            if (cudaEventElapsedTime(&g, evpool[t], evpool[t + 1]) == cudaSuccess && g > 0.02f)
                 fprintf(stderr, "[dtwlb] events %zu -> %zu: %.2f ms\n", t, t + 1, g);
         }
     }
