@@ -461,17 +461,58 @@ __device__ __forceinline__ void four_rows(float (&B)[2 * WB + 2], const float (&
     }
 }
 
+// four_rows with the y window read from global memory (L1: the lanes of a warp mostly walk
+// the same query) instead of registers: frees 2w+4 registers (w up to 64 fits; more warps
+// per SM) and removes the per-block window shift; yb[k] = y[i - w + k] (+inf padded).
+template <int WB, int P, bool EXACT>
+__device__ __forceinline__ void four_rows_g(float (&B)[2 * WB + 2], const float *yb,
+                                            const float (&x)[4], int w2) {
+    constexpr int NB = 2 * WB + 1;
+    float yy[NB + 3];
+    float pl0 = kInf, pl1 = kInf, pl2 = kInf, pl3 = kInf;
+    float h1_0 = kInf, h2_0 = kInf, h1_1 = kInf, h2_1 = kInf, h1_2 = kInf, h2_2 = kInf;
+#pragma unroll
+    for (int d = 0; d < NB + 6; ++d) {
+        if (d < NB + 3) yy[d] = yb[d];  // (generic load: shared or global)
+        float c0 = kInf, c1 = kInf, c2 = kInf;
+        if (d < NB) {
+            c0 = cell<P>(min3f(B[d], B[d + 1], pl0), x[0] - yy[d]);
+            if (!EXACT && d > w2) c0 = kInf;
+            pl0 = c0;
+        }
+        if (d >= 2 && d - 2 < NB) {
+            c1 = cell<P>(min3f(h2_0, h1_0, pl1), x[1] - yy[d - 1]);
+            if (!EXACT && d - 2 > w2) c1 = kInf;
+            pl1 = c1;
+        }
+        if (d >= 4 && d - 4 < NB) {
+            c2 = cell<P>(min3f(h2_1, h1_1, pl2), x[2] - yy[d - 2]);
+            if (!EXACT && d - 4 > w2) c2 = kInf;
+            pl2 = c2;
+        }
+        if (d >= 6) {
+            float c3 = cell<P>(min3f(h2_2, h1_2, pl3), x[3] - yy[d - 3]);
+            if (!EXACT && d - 6 > w2) c3 = kInf;
+            pl3 = c3;
+            B[d - 6] = c3;
+        }
+        h2_0 = h1_0; h1_0 = c0;
+        h2_1 = h1_1; h1_1 = c1;
+        h2_2 = h1_2; h1_2 = c2;
+    }
+}
+
 // Per-lane staging slot of the pipelined refill: the y window (NY floats), x[0..7] and
 // the query envelope U[0..3], L[0..3] of the lane's next pair, written by cp.async while
 // the lane still waits one step; +4 floats of padding rotate the banks between lanes.
-template <int WB>
+template <int WB, bool YG = false>
 struct Dtw4Cfg {
-    static constexpr int NY = (2 * WB + 4 + 3) / 4 * 4;
+    static constexpr int NY = YG ? 0 : (2 * WB + 4 + 3) / 4 * 4;  // (YG: no y window in the slot)
     // [0, NY) the y window and [NY] the gate word (refill, read at activation); while the lane
     // is active [0, 40) stages the row+column cascade's column data (reading c21);
     // [XA, XA + 8) x and [XA + 8, XA + 24) U(y), L(y) of the next step's 8 rows (written by
     // the refill for rows 0..7, then one step ahead); [SL - 2, SL) the pair's (q, c)
-    static constexpr int XA = NY + 4 > 40 ? NY + 4 : 40;
+    static constexpr int XA = NY + 4 > 40 ? NY + 4 : 40;  // (YG: the gate word sits at [0])
     static constexpr int SL = XA + 28;
     static constexpr size_t smem = (size_t)NT * SL * sizeof(float) +
                                    (size_t)(NT / 32) * kChunk4 * (sizeof(unsigned long long) + sizeof(int));
@@ -480,13 +521,16 @@ struct Dtw4Cfg {
 // Lane states of dtw4_kernel
 constexpr int kFree = 0, kPending = 1, kActive = 2;
 
-template <int WB, int P, bool EXACT, bool WALK>
-__global__ void __launch_bounds__(NT, (WB <= 25 ? 3 : 2))
+template <int WB, bool YG>
+constexpr int dtw4_min_blocks() { return YG ? (WB <= 32 ? 4 : 3) : (WB <= 25 ? 3 : 2); }
+
+template <int WB, int P, bool EXACT, bool WALK, bool YG>
+__global__ void __launch_bounds__(NT, (dtw4_min_blocks<WB, YG>()))
 dtw4_kernel(DtwArgs a) {
     constexpr int NB = 2 * WB + 1;
-    constexpr int NY = Dtw4Cfg<WB>::NY;  // window length, a multiple of 4 (aligned refills)
-    constexpr int SL = Dtw4Cfg<WB>::SL;
-    constexpr int XA = Dtw4Cfg<WB>::XA;
+    constexpr int NY = Dtw4Cfg<WB, YG>::NY;  // window length, a multiple of 4 (aligned refills)
+    constexpr int SL = Dtw4Cfg<WB, YG>::SL;
+    constexpr int XA = Dtw4Cfg<WB, YG>::XA;
     extern __shared__ __align__(16) float dsm[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     float *slot = dsm + (size_t)threadIdx.x * SL;  // this lane's staging slot
@@ -495,8 +539,20 @@ dtw4_kernel(DtwArgs a) {
                                       (NT / 32) * kChunk4) + wid * kChunk4;
     const int n = a.n, w = EXACT ? WB : a.w, w2 = 2 * w;
     const int sh = (kYPadL - w) & 3;  // alignment class of (i - w) for i % 4 == 0
+    // YG, WALK: the padded row of the query of the warp's current chunk staged in shared
+    // memory (lanes on that query read their y values there, others from global/L1)
+    float *wrow = reinterpret_cast<float *>(reinterpret_cast<int *>(reinterpret_cast<unsigned long long *>(
+                      dsm + (size_t)NT * SL) + (NT / 32) * kChunk4) + (NT / 32) * kChunk4) + (size_t)wid * a.LP;
+    int staged_q = -1;
+    bool ysm = false;           // this lane's y row is the staged one
+    const float *ybase = nullptr;  // YG: start of this lane's padded y row (shared or global)
     const int64_t total = (WALK && a.dev_total) ? (int64_t)*a.dev_total : a.total;
-    const int64_t nchunks = (total + kChunk4 - 1) / kChunk4;
+    // chunk size: kChunk4 items per warp grab, smaller (down to 32) when the round is too
+    // small to give every resident warp a few chunks (few long pairs: C3, C4)
+    const int64_t nwarps = (int64_t)gridDim.x * (NT / 32);
+    const int64_t chunk_w = (total / (4 * nwarps) + 31) / 32 * 32;
+    const int chunk = (int)(chunk_w > kChunk4 ? kChunk4 : (chunk_w < 32 ? 32 : chunk_w));
+    const int64_t nchunks = (total + chunk - 1) / chunk;
     if (total == 0) return;
     const unsigned lt = (1u << lane) - 1u;
 
@@ -506,7 +562,7 @@ dtw4_kernel(DtwArgs a) {
     const float *xr = nullptr, *yr = nullptr;
     float thr = kInf, thr_n = kInf, beta_n = 0.f;
     int i = 0;
-    float B[NB + 1], Y[NY];
+    float B[NB + 1], Y[YG ? 1 : NY];
     float xv[8];  // x of rows i .. i+7 (staged in the slot one 8-row step ahead)
     // cascading abandon: rest = LB_Keogh^p terms of the rows not yet computed
     const bool casc = WALK && (a.b1 != nullptr || a.b1h != nullptr);
@@ -528,10 +584,12 @@ dtw4_kernel(DtwArgs a) {
                     if constexpr (!WALK) a.res[item] = kInf;  // (WALK: pruned by its bound)
                     st = kFree;
                 } else {
+                    if constexpr (!YG) {
 #pragma unroll
-                    for (int d = 0; d < NY; d += 4) {
-                        const float4 v = *reinterpret_cast<const float4 *>(slot + d);
-                        Y[d] = v.x; Y[d + 1] = v.y; Y[d + 2] = v.z; Y[d + 3] = v.w;
+                        for (int d = 0; d < NY; d += 4) {
+                            const float4 v = *reinterpret_cast<const float4 *>(slot + d);
+                            Y[d] = v.x; Y[d + 1] = v.y; Y[d + 2] = v.z; Y[d + 3] = v.w;
+                        }
                     }
                     const float4 x0 = *reinterpret_cast<const float4 *>(slot + XA);
                     const float4 x1 = *reinterpret_cast<const float4 *>(slot + XA + 4);
@@ -560,8 +618,8 @@ dtw4_kernel(DtwArgs a) {
             if (lane == 0) c = atomicAdd(a.queue, 1u);
             c = __shfl_sync(0xffffffffu, c, 0);
             if (c < nchunks) {
-                cbeg = (int)c * kChunk4;
-                cend = (int)(cbeg + kChunk4 < total ? cbeg + kChunk4 : total);
+                cbeg = (int)c * chunk;
+                cend = (int)(cbeg + chunk < total ? cbeg + chunk : total);
                 cursor = cbeg;
                 if constexpr (WALK) {
                     // stage the chunk's keys and queries: items are in query order, each
@@ -571,8 +629,17 @@ dtw4_kernel(DtwArgs a) {
                         const int mid = (lo + hi) >> 1;
                         if (a.item_off[mid] <= cbeg) lo = mid; else hi = mid;
                     }
+                    if constexpr (YG) {
+                        if (lo != staged_q) {  // restage: lanes still on the old row read it from global
+                            if (ysm) { ybase = a.ysh + (int64_t)reinterpret_cast<const int *>(slot)[SL - 2] * a.LP; ysm = false; }
+                            __syncwarp();
+                            const float *src = a.ysh + (int64_t)lo * a.LP;
+                            for (int u = lane; u < a.LP; u += 32) wrow[u] = __ldg(src + u);
+                            staged_q = lo;
+                        }
+                    }
                     int q = lo;
-                    for (int t = 0; t < kChunk4 / 32; ++t) {
+                    for (int t = 0; t < chunk / 32; ++t) {
                         const int it = cbeg + lane + 32 * t;
                         if (it < cend) {
                             while (it >= a.item_off[q + 1]) ++q;
@@ -617,10 +684,16 @@ dtw4_kernel(DtwArgs a) {
                 }
                 xr = a.db + c * n;
                 yr = a.ysh + (int64_t)sh * a.ysh_stride_s + qy * a.LP;
+                if constexpr (YG) {
+                    ysm = WALK && qy == staged_q;
+                    ybase = ysm ? wrow : a.ysh + qy * a.LP;  // (shift-0 copy: no alignment needed)
+                }
                 // Y[d] = ypad[-w + kYPadL + d]; the copy `sh` makes base (kYPadL - w - sh) aligned
                 const float *ys = yr + (kYPadL - w - sh);
+                if constexpr (!YG) {
 #pragma unroll
-                for (int d = 0; d < NY; d += 4) cp_async16(slot + d, ys + d, 16);
+                    for (int d = 0; d < NY; d += 4) cp_async16(slot + d, ys + d, 16);
+                }
                 stage_rows8(slot + XA, xr, 0, n);
                 if (casc) {
                     stage_rows8(slot + XA + 8, ur, 0, n);
@@ -692,14 +765,19 @@ dtw4_kernel(DtwArgs a) {
             for (int blk = 0; blk < 2; ++blk) {
                 if (i + 4 > n) break;
                 const float x4[4] = {xv[0], xv[1], xv[2], xv[3]};
-                four_rows<WB, P, EXACT>(B, Y, x4, w2);
-                i += 4;
+                if constexpr (YG) {
+                    four_rows_g<WB, P, EXACT>(B, ybase + (kYPadL - w) + i, x4, w2);
+                    i += 4;
 #pragma unroll
-                for (int t = 0; t < 4; ++t) xv[t] = xv[t + 4];
-                // shift the y window by four and append y[i + w + 1 .. i + w + 4] (next block)
+                    for (int t = 0; t < 4; ++t) xv[t] = xv[t + 4];
+                } else {
+                    four_rows<WB, P, EXACT>(B, Y, x4, w2);
+                    i += 4;
 #pragma unroll
-                for (int d = 0; d + 4 < NY; ++d) Y[d] = Y[d + 4];
-                {
+                    for (int t = 0; t < 4; ++t) xv[t] = xv[t + 4];
+                    // shift the y window by four and append y[i + w + 1 .. i + w + 4] (next block)
+#pragma unroll
+                    for (int d = 0; d + 4 < NY; ++d) Y[d] = Y[d + 4];
                     const float4 v = __ldg(reinterpret_cast<const float4 *>(yr + (kYPadL - w - sh) + i + NY - 4));
                     Y[NY - 4] = v.x; Y[NY - 3] = v.y; Y[NY - 2] = v.z; Y[NY - 1] = v.w;
                 }
@@ -709,15 +787,18 @@ dtw4_kernel(DtwArgs a) {
                     float prev = kInf;
 #pragma unroll
                     for (int d = 0; d < NB; ++d) {
-                        float c = cell<P>(min3f(B[d], B[d + 1], prev), __ldg(xr + i) - Y[d]);
+                        const float yd = YG ? ybase[(kYPadL - w) + i + d] : Y[YG ? 0 : d];
+                        float c = cell<P>(min3f(B[d], B[d + 1], prev), __ldg(xr + i) - yd);
                         if (!EXACT && d > w2) c = kInf;
                         B[d] = c;
                         prev = c;
                     }
                     ++i;
+                    if constexpr (!YG) {
 #pragma unroll
-                    for (int d = 0; d + 1 < NY; ++d) Y[d] = Y[d + 1];
-                    Y[NY - 1] = __ldg(yr + (kYPadL - w - sh) + i + NY - 1);
+                        for (int d = 0; d + 1 < NY; ++d) Y[d] = Y[d + 1];
+                        Y[NY - 1] = __ldg(yr + (kYPadL - w - sh) + i + NY - 1);
+                    }
                 }
             }
             rows_done += (unsigned)(i - i0);
@@ -847,14 +928,14 @@ __global__ void dtw_generic_kernel(DtwArgs a, const float *__restrict__ yraw, fl
     }
 }
 
-template <int WB, int P, bool EXACT, bool WALK>
+template <int WB, int P, bool EXACT, bool WALK, bool YG>
 int launch_dtw4_t(const DtwArgs &a, cudaStream_t st) {
     DTWLB_CUDA(cudaMemsetAsync(a.queue, 0, sizeof(unsigned), st));
     const int64_t chunks = ceil_div(a.total, kChunk4);
     int64_t warps = std::min<int64_t>(chunks, (int64_t)148 * 48);  // persistent-ish: <= 48 warps per SM
     const int64_t grid = ceil_div(warps * 32, NT);
-    constexpr size_t smem = Dtw4Cfg<WB>::smem;
-    auto k = dtw4_kernel<WB, P, EXACT, WALK>;
+    const size_t smem = Dtw4Cfg<WB, YG>::smem + (YG ? (size_t)(NT / 32) * a.LP * sizeof(float) : 0);
+    auto k = dtw4_kernel<WB, P, EXACT, WALK, YG>;
     DTWLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<(unsigned)grid, NT, smem, st>>>(a);
     DTWLB_LAUNCH_CHECK();
@@ -863,8 +944,16 @@ int launch_dtw4_t(const DtwArgs &a, cudaStream_t st) {
 
 template <int WB, int P, bool EXACT, bool WALK>
 int launch_dtw_t(const DtwArgs &a, cudaStream_t st) {
-    if constexpr (WB <= 32) {
-        if (a.queue) return launch_dtw4_t<WB, P, EXACT, WALK>(a, st);
+    // w <= 32: y window in registers (or, DTWLB_DTW_YG=1, read through L1); 32 < w <= 64:
+    // the y window read through L1 (the band alone needs 2w+2 registers)
+    static const bool env_yg = [] { const char *e = getenv("DTWLB_DTW_YG"); return e && atoi(e); }();
+    if (a.queue) {
+        if constexpr (WB <= 32) {
+            if (env_yg) return launch_dtw4_t<WB, P, EXACT, WALK, true>(a, st);
+            return launch_dtw4_t<WB, P, EXACT, WALK, false>(a, st);
+        } else {
+            return launch_dtw4_t<WB, P, EXACT, WALK, true>(a, st);
+        }
     }
     const int ipw = kDtwIpw;
     const int64_t warps = WALK ? a.nchunks : ceil_div(a.total, ipw);

@@ -739,10 +739,10 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
             // ---- a5: DTW walk ----
             start_walk_kernel<<<(unsigned)ceil_div(qn, 256), 256, 0, st>>>(s, (int)qn);
             DTWLB_LAUNCH_CHECK();
-            // The w <= 32 DTW kernel reads each round's item count from device memory (written by
+            // The w <= 64 DTW kernels read each round's item count from device memory (written by
             // the plan kernel), so rounds are queued in batches of kRoundBatch with one host
-            // check per batch; the other DTW kernels size their grids from it (one check per round).
-            const bool dev_rounds = !generic_dtw && w <= 32;
+            // check per batch; the generic kernel sizes its grid from it (one check per round).
+            const bool dev_rounds = !generic_dtw;  // (w <= 64: the dtw4 kernels)
             const int batch = dev_rounds ? kRoundBatch : 1;
             for (bool walking = true; walking;) {
                 for (int b = 0; b < batch && walking; ++b) {
