@@ -319,7 +319,7 @@ __global__ void start_walk_kernel(QState s, int Qb) {
 // Two exclusive scans: item_off (results layout) and chunk_off (warp -> query).
 constexpr int kD0 = 128, kDMax = 65536;
 constexpr int kSeedCap = 2048;   // cap of the best-first seed range size S (nn_search)
-constexpr int kRoundBatch = 4;  // walk rounds queued per host check (w <= 32 DTW kernel)
+constexpr int kRoundBatch = 8;  // walk rounds queued per host check (w <= 64 DTW kernels)
 __device__ __forceinline__ int2 block_scan2(int2 v, int2 *warp_sums, int2 &total) {
     // inclusive block-wide scan of two ints; returns the inclusive value, sets total
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
