@@ -871,7 +871,9 @@ dtw4_kernel(DtwArgs a) {
 
 // Generic fallback for w > 64: one thread per pair, band kept in global scratch.
 template <int P, bool WALK>
-__global__ void dtw_generic_kernel(DtwArgs a, const float *__restrict__ yraw, float *__restrict__ scratch) {
+__global__ void dtw_generic_kernel(DtwArgs a, const float *__restrict__ yraw, float *__restrict__ scratch,
+                                   int smem_pitch) {
+    extern __shared__ float gband[];  // smem_pitch > 0: each thread's band in shared memory
     const int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (item >= a.total) return;
     const int n = a.n, w = a.w, nb = 2 * w + 1;
@@ -895,7 +897,7 @@ __global__ void dtw_generic_kernel(DtwArgs a, const float *__restrict__ yraw, fl
         xr = a.db + item * n;
         yr = yraw + item * n;
     }
-    float *B = scratch + item * (int64_t)(nb + 1);
+    float *B = smem_pitch > 0 ? gband + threadIdx.x * smem_pitch : scratch + item * (int64_t)(nb + 1);
     for (int d = 0; d <= nb; ++d) B[d] = kInf;
     B[w] = 0.f;
     for (int i = 0; i < n; ++i) {
@@ -1033,18 +1035,30 @@ int launch_dtw_generic(const DtwArgs &a, const float *yraw, float *scratch, int 
                        cudaStream_t st) {
     if (a.total == 0) return DTWLB_OK;
     const int64_t grid = ceil_div(a.total, 128);
+    // the band (2w+2 floats per pair) in shared memory when 128 of them fit (odd pitch: the
+    // threads' same-index cells fall in different banks), else in the global scratch
+    int pitch = (2 * a.w + 2) | 1;
+    size_t smem = (size_t)128 * pitch * sizeof(float);
+    if (smem > 200 * 1024) { pitch = 0; smem = 0; }
+    if (smem > 48 * 1024) {
+        DTWLB_CUDA(cudaFuncSetAttribute(dtw_generic_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        DTWLB_CUDA(cudaFuncSetAttribute(dtw_generic_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        DTWLB_CUDA(cudaFuncSetAttribute(dtw_generic_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        DTWLB_CUDA(cudaFuncSetAttribute(dtw_generic_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        DTWLB_CUDA(cudaFuncSetAttribute(dtw_generic_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    }
     if (p == 0) {
         if (walk) {
             set_error(DTWLB_EUNSUPPORTED, "nn_search: p = infinity unsupported");
             return DTWLB_EUNSUPPORTED;
         }
-        dtw_generic_kernel<0, false><<<(unsigned)grid, 128, 0, st>>>(a, yraw, scratch);
+        dtw_generic_kernel<0, false><<<(unsigned)grid, 128, smem, st>>>(a, yraw, scratch, pitch);
     } else if (p == 1) {
-        if (walk) dtw_generic_kernel<1, true><<<(unsigned)grid, 128, 0, st>>>(a, yraw, scratch);
-        else dtw_generic_kernel<1, false><<<(unsigned)grid, 128, 0, st>>>(a, yraw, scratch);
+        if (walk) dtw_generic_kernel<1, true><<<(unsigned)grid, 128, smem, st>>>(a, yraw, scratch, pitch);
+        else dtw_generic_kernel<1, false><<<(unsigned)grid, 128, smem, st>>>(a, yraw, scratch, pitch);
     } else {
-        if (walk) dtw_generic_kernel<2, true><<<(unsigned)grid, 128, 0, st>>>(a, yraw, scratch);
-        else dtw_generic_kernel<2, false><<<(unsigned)grid, 128, 0, st>>>(a, yraw, scratch);
+        if (walk) dtw_generic_kernel<2, true><<<(unsigned)grid, 128, smem, st>>>(a, yraw, scratch, pitch);
+        else dtw_generic_kernel<2, false><<<(unsigned)grid, 128, smem, st>>>(a, yraw, scratch, pitch);
     }
     DTWLB_LAUNCH_CHECK();
     return DTWLB_OK;
