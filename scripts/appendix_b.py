@@ -1,0 +1,65 @@
+"""Appendix B workload: triangle-inequality statistics of unconstrained DTW_p.
+
+For T triples (x, y, z) of 100-sample series -- white noise x_i = N(0,1) and random walks
+x_1 = 0, x_i = x_{i-1} + N(0,1) -- compute C(x,y,z) = DTW_p(x,z) / (DTW_p(x,y) + DTW_p(y,z))
+without a time constraint (w = n - 1) through the `dtw_band` C-ABI call, and report the
+fraction of violations C > 1 (the paper: none for white noise; 20 % (p=1) and 15 % (p=2)
+for random walks) and the DTW throughput.  A sample of triples is checked against the fp64
+oracle.  usage: python scripts/appendix_b.py [T=100000] [--no-oracle]
+"""
+import json
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, "/root/repo")
+import datagen  # noqa: E402
+from paper_0811_3301_b200 import dtw_band  # noqa: E402
+
+N_SAMPLES = 100
+
+
+def series(kind: str, rows: int, seed: int) -> np.ndarray:
+    if kind == "rw":
+        return datagen.random_walks(rows, N_SAMPLES, seed=seed, znorm=False)
+    g = np.random.default_rng(seed)
+    return g.standard_normal((rows, N_SAMPLES)).astype(np.float32)
+
+
+def run(T: int, check_oracle: bool = True):
+    out = {}
+    for kind, seed in (("white_noise", 11), ("random_walk", 12)):
+        x, y, z = (series("rw" if kind == "random_walk" else "wn", T, seed + 100 * t) for t in range(3))
+        xd, yd, zd = (torch.from_numpy(a).cuda() for a in (x, y, z))
+        for p in (1, 2):
+            w = N_SAMPLES - 1  # unconstrained
+            a = torch.cat([xd, xd, yd]).contiguous()
+            b = torch.cat([zd, yd, zd]).contiguous()
+            dtw_band(a[:64], b[:64], w, p)  # warm-up
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            d = dtw_band(a, b, w, p)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            dxz, dxy, dyz = d[:T].double(), d[T:2 * T].double(), d[2 * T:].double()
+            C = dxz / (dxy + dyz)
+            viol = float((C > 1).double().mean())
+            pairs = 3 * T
+            res = {"violation_frac": viol, "C_max": float(C.max()), "pairs": pairs, "seconds": dt,
+                   "pairs_per_s": pairs / dt, "cells_per_s": pairs * N_SAMPLES * N_SAMPLES / dt}
+            if check_oracle:
+                import oracle
+                S = 50
+                o = np.array([oracle.dtw(a[j].cpu().numpy(), b[j].cpu().numpy(), w, p)
+                              for j in list(range(S)) + list(range(T, T + S)) + list(range(2 * T, 2 * T + S))])
+                g = np.concatenate([d[:S].cpu().numpy(), d[T:T + S].cpu().numpy(), d[2 * T:2 * T + S].cpu().numpy()])
+                res["oracle_max_rel_err"] = float(np.max(np.abs(g - o) / np.maximum(o, 1e-30)))
+            out[f"{kind}_p{p}"] = res
+    return out
+
+
+if __name__ == "__main__":
+    T = int(sys.argv[1]) if len(sys.argv) > 1 and not sys.argv[1].startswith("-") else 100_000
+    print(json.dumps(run(T, "--no-oracle" not in sys.argv), indent=1))
