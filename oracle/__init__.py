@@ -61,6 +61,8 @@ def _load():
             lib.oracle_lb_keogh.restype = d
             lib.oracle_lb_piecewise.argtypes = [_dp, _dp, i, i, i, i]
             lib.oracle_lb_piecewise.restype = d
+            lib.oracle_lb_piecewise_paper.argtypes = [_dp, _dp, i, i, i, i]
+            lib.oracle_lb_piecewise_paper.restype = d
             lib.oracle_lb_improved.argtypes = [_dp, _dp, i, i, i]
             lib.oracle_lb_improved.restype = d
             lib.oracle_dtw.argtypes = [_dp, _dp, i, i, i]
@@ -128,10 +130,21 @@ def lb_keogh(x, y, w, p):
 
 
 def lb_piecewise(x, y, w, p, s=8):
-    """Piecewise-sum bound (p = 2 per reading c18), rooted; segment length s."""
+    """Piecewise-sum bound (p = 2 per reading c18), rooted, over the builder's
+    fixed-length cover (intervals of s samples, the last one shorter; reading c18)
+    that the GPU pre-filter uses."""
     x, xp = _d(x)
     y, yp = _d(y)
     return _load().oracle_lb_piecewise(xp, yp, x.shape[-1], int(w), int(s), int(p))
+
+
+def lb_piecewise_paper(x, y, w, p, d=8):
+    """Piecewise-sum bound over the paper's own cover (d intervals of floor(n/d),
+    the last one longer; d = 8 in the experiments), rooted; p = 2 divides each
+    interval's squared distance by its length (reading c18)."""
+    x, xp = _d(x)
+    y, yp = _d(y)
+    return _load().oracle_lb_piecewise_paper(xp, yp, x.shape[-1], int(w), int(d), int(p))
 
 
 def lb_improved(x, y, w, p):
@@ -209,7 +222,8 @@ def nn_twopass(queries, db, w, p, k, keogh_only=False, threads=1):
 
 
 def prune_counts(queries, db, w, p, tau, threads=1):
-    """Order-independent counts vs the final k-th distance tau[q] (parity unpinned)."""
+    """Order-independent counts vs the final k-th distance tau[q]: (#{LB_Keogh^p > tau^p},
+    #{LB_Keogh^p <= tau^p < LB_Improved^p}) per query (pinned: test_prune_counts_pinned)."""
     queries, qp = _f(queries)
     db, dbp = _f(db)
     Q, n = queries.shape

@@ -168,9 +168,14 @@ double oracle_lb_keogh(const double *x, const double *y, int n, int w, int p)
 }
 
 /* Piecewise-sum lower bound (section "Using a multidimensional
- * indexing structure"): with the cover C_j = [j*s, min((j+1)*s, n)) (the
- * paper's equal-length cover P:662-665, last interval shorter) and
- * P(v)_j = sum_{i in C_j} v_i,
+ * indexing structure"): with the cover C_j = [j*s, min((j+1)*s, n)) and
+ * P(v)_j = sum_{i in C_j} v_i.  This fixed-length cover (intervals of s
+ * samples, the LAST one SHORTER when s does not divide n) is the builder's
+ * choice for the GPU pre-filter (reading c18), NOT the cover the
+ * paper's experiments used: P:661-665 takes d intervals of floor(n/d) with
+ * the last one LONGER (oracle_lb_piecewise_paper below).  Any disjoint cover
+ * gives a valid bound, so both are lower bounds of LB_Keogh;
+ * they coincide when s divides n and d = n/s.
  *   p = 1:  sum_j d(P(x)_j, [P(L)_j, P(U)_j])          (the paper)
  *   p = 2:  sum_j d(P(x)_j, [P(L)_j, P(U)_j])^2 / s    (reading c18: Cauchy-Schwarz
  *           per interval, sum_{C_j} d_i^2 >= (sum_{C_j} d_i)^2 / |C_j|, |C_j| <= s)
@@ -200,6 +205,44 @@ double oracle_lb_piecewise(const double *x, const double *y, int n, int w, int s
     double *L = (double *)malloc(sizeof(double) * (size_t)n);
     oracle_envelope_naive(y, n, w, U, L);
     double v = oracle_lb_piecewise_pow(x, U, L, n, s, p);
+    free(U);
+    free(L);
+    return root_p(v, p);
+}
+
+/* The paper's own cover: d intervals C_j = [1+(j-1)floor(n/d),
+ * j floor(n/d)] for j < d and C_d = [1+(d-1)floor(n/d), n] (1-based; the last
+ * interval takes the remainder, so it is the LONGEST), requiring 1 <= d <= n.
+ *   p = 1: sum_j d(P_d(x)_j, [P_d(L)_j, P_d(U)_j])
+ *   p = 2: sum_j d(...)^2 / |C_j|  (reading c18, Cauchy-Schwarz per interval)
+ * Returns the p-th-power (unrooted) value; NAN if d is outside [1, n]. */
+double oracle_lb_piecewise_paper_pow(const double *x, const double *U, const double *L, int n, int d, int p)
+{
+    if (d < 1 || d > n) return NAN;
+    const int len = n / d; /* floor(n/d) */
+    double total = 0.0;
+    for (int j = 0; j < d; ++j) {
+        int j0 = j * len, j1 = (j == d - 1) ? n : (j + 1) * len; /* C_{j+1}, 0-based [j0, j1) */
+        double px = 0.0, pu = 0.0, pl = 0.0;
+        for (int i = j0; i < j1; ++i) {
+            px += x[i];
+            pu += U[i];
+            pl += L[i];
+        }
+        double dd = 0.0;
+        if (px > pu) dd = px - pu;
+        else if (px < pl) dd = pl - px;
+        total += p == 1 ? dd : dd * dd / (double)(j1 - j0);
+    }
+    return total;
+}
+
+double oracle_lb_piecewise_paper(const double *x, const double *y, int n, int w, int d, int p)
+{
+    double *U = (double *)malloc(sizeof(double) * (size_t)n);
+    double *L = (double *)malloc(sizeof(double) * (size_t)n);
+    oracle_envelope_naive(y, n, w, U, L);
+    double v = oracle_lb_piecewise_paper_pow(x, U, L, n, d, p);
     free(U);
     free(L);
     return root_p(v, p);
@@ -408,9 +451,12 @@ void oracle_nn_twopass(const float *queries, int64_t q0, int64_t q1, const float
 }
 
 /* Order-independent prune counts against a FINAL threshold (SURVEY 8(c)
- * "Prune rates" row, parity unpinned): for each query q with final k-th
+ * "Prune rates" row): for each query q with final k-th
  * distance tau_q (rooted), counts #{c : LB_Keogh^p > tau^p} and
- * #{c : LB_Keogh^p <= tau^p < LB_Improved^p}. */
+ * #{c : LB_Keogh^p <= tau^p < LB_Improved^p}.  Pinned in
+ * tests/test_oracle_pins.py::test_prune_counts_pinned against numpy bounds and
+ * the Alg. 3 counter invariants (the paper's pruning curves are stripped,
+ * P:767-856, so no printed value exists). */
 void oracle_prune_counts(const float *queries, int64_t q0, int64_t q1, const float *db, int64_t N,
                          int n, int w, int p, const double *tau, int64_t *out_keogh,
                          int64_t *out_improved)

@@ -349,3 +349,115 @@ def test_piecewise_chain_and_special_cases():
             one = max(sx - su, sl - sx, 0.0)
             expect = one if p == 1 else one * one / n
             assert oracle.lb_piecewise(x, y, w, p, n) ** p == pytest.approx(expect, rel=1e-9, abs=1e-9)
+
+
+# ---------------------------------------------------------------- the paper's own cover
+@pytest.mark.parametrize("case", GOLDEN["piecewise_paper_cover"], ids=lambda c: c["cite"][:30])
+def test_piecewise_paper_cover_golden(case):
+    """Hand-derived values over the paper's cover P:661-665 (d intervals of floor(n/d), the
+    last one longer)."""
+    v = oracle.lb_piecewise_paper(case["x"], case["y"], case["w"], case["p"], case["d"]) ** case["p"]
+    assert v == pytest.approx(case["value_pow"], abs=1e-12)
+
+
+def test_piecewise_paper_cover_special_cases():
+    """The paper's cover: d = n is LB_Keogh (one sample per interval); d = 1 is one
+    interval, d(sum x, [sum L, sum U]) with numpy's sliding-window envelope (library routine);
+    when d divides n it equals the builder's fixed-length cover with s = n/d; always
+    <= LB_Keogh <= DTW; d outside [1, n] is rejected (NaN)."""
+    from numpy.lib.stride_tricks import sliding_window_view as swv
+    for _ in range(800):
+        n = int(RNG.integers(1, 16))
+        integer = RNG.random() < 0.5
+        x = rand_int_series(n) if integer else RNG.standard_normal(n)
+        y = rand_int_series(n) if integer else RNG.standard_normal(n)
+        w = int(RNG.integers(0, n + 1))
+        for p in (1, 2):
+            kb = oracle.lb_keogh(x, y, w, p)
+            dd = oracle.dtw(x, y, w, p)
+            tol = 1e-12 * (1 + dd)
+            assert oracle.lb_piecewise_paper(x, y, w, p, n) == pytest.approx(kb, rel=1e-12, abs=1e-12)
+            for d in range(1, n + 1):
+                v = oracle.lb_piecewise_paper(x, y, w, p, d)
+                assert v <= kb + tol and v <= dd + tol
+                if n % d == 0:
+                    assert v == pytest.approx(oracle.lb_piecewise(x, y, w, p, n // d), rel=1e-12, abs=1e-12)
+            we = min(w, n - 1)
+            yp = np.pad(np.asarray(y, float), (we, we), mode="edge")
+            U, L = swv(yp, 2 * we + 1).max(axis=1), swv(yp, 2 * we + 1).min(axis=1)
+            sx = float(np.sum(x))
+            one = max(sx - float(U.sum()), float(L.sum()) - sx, 0.0)
+            expect = one if p == 1 else one * one / n
+            assert oracle.lb_piecewise_paper(x, y, w, p, 1) ** p == pytest.approx(expect, rel=1e-9, abs=1e-9)
+    assert math.isnan(oracle.lb_piecewise_paper([1.0, 2.0], [0.0, 0.0], 1, 1, 3))
+    assert math.isnan(oracle.lb_piecewise_paper([1.0, 2.0], [0.0, 0.0], 1, 1, 0))
+
+
+# ---------------------------------------------------------------- order-independent prune counts
+def _numpy_bounds_pow(x, y, w, p):
+    """LB_Keogh^p and LB_Improved^p by numpy (independent of the oracle's C code): sliding-window
+    envelopes (library routine), the projection H = clip(x, L, U) of Eq. (1), the
+    envelope of H, and the point-to-interval distances."""
+    from numpy.lib.stride_tricks import sliding_window_view as swv
+    n = len(y)
+    we = min(w, n - 1)
+
+    def env(v):
+        vp = np.pad(np.asarray(v, float), (we, we), mode="edge")
+        return swv(vp, 2 * we + 1).max(axis=1), swv(vp, 2 * we + 1).min(axis=1)
+
+    x, y = np.asarray(x, float), np.asarray(y, float)
+    U, L = env(y)
+    H = np.clip(x, L, U)
+    b1 = float(np.sum(np.abs(x - H) ** p))
+    U2, L2 = env(H)
+    b2 = float(np.sum(np.maximum(np.maximum(y - U2, L2 - y), 0.0) ** p))
+    return b1, b1 + b2
+
+
+@pytest.mark.parametrize("p,k", [(1, 1), (2, 1), (2, 3)])
+def test_prune_counts_pinned(p, k):
+    """oracle_prune_counts (SURVEY 8(c) "Prune rates" row), pinned against (1) the same counts
+    from numpy bounds (independent code; candidates whose bound is within 1e-9 relative of tau
+    may fall either way) and (2) the invariants that tie them to the paper's Alg. 3
+    (P:578-620): Alg. 3 compares each bound with its CURRENT k-th best, which is never below the
+    final tau, so the sequential scan evaluates LB_Improved on >= N - #keogh and DTW on
+    >= N - #keogh - #improved candidates; and every candidate with DTW <= tau survives both
+    bounds, so N - #keogh - #improved >= #{DTW <= tau} >= k."""
+    rng = np.random.default_rng(77 + p + k)
+    Q, N, n, w = 6, 60, 24, 3
+    walk = lambda m: np.cumsum(rng.standard_normal((m, n)), axis=1).astype(np.float32)
+    qs, db = walk(Q), walk(N)
+    idx, dist = oracle.nn_brute(qs, db, w, p, k)
+    tau = dist[:, k - 1]
+    ck, ci = oracle.prune_counts(qs, db, w, p, tau)
+    seen_keogh_evals = 0
+    for q in range(Q):
+        tp = float(tau[q]) ** p
+        lo, hi = tp * (1 - 1e-9), tp * (1 + 1e-9)
+        nk_lo = nk_hi = ni_lo = ni_hi = 0
+        n_le = 0
+        for c in range(N):
+            b1, bi = _numpy_bounds_pow(db[c].astype(float), qs[q].astype(float), w, p)
+            if b1 > hi:
+                nk_lo += 1; nk_hi += 1
+                continue
+            if b1 > lo:  # ambiguous at the tolerance: may be counted by either
+                nk_hi += 1
+            if bi > hi:
+                ni_lo += 1; ni_hi += 1
+            elif bi > lo:
+                ni_hi += 1
+            if oracle.dtw_pow(db[c], qs[q], w, p) <= hi:
+                n_le += 1
+        assert nk_lo <= ck[q] <= nk_hi
+        assert ni_lo - (nk_hi - nk_lo) <= ci[q] <= ni_hi + (nk_hi - nk_lo)
+        assert N - ck[q] - ci[q] >= n_le >= k
+        # sequential Alg. 3 on this query alone
+        _, _, cnt = oracle.nn_twopass(qs[q:q + 1], db, w, p, k)
+        seen, pk, pi, ndtw = (int(v) for v in cnt)
+        assert seen == N and pk + pi + ndtw == N
+        assert seen - pk >= N - ck[q]
+        assert ndtw >= N - ck[q] - ci[q]
+        seen_keogh_evals += seen - pk
+    assert seen_keogh_evals > 0
