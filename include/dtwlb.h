@@ -13,7 +13,11 @@
  * - Pointers are CUDA DEVICE pointers unless a function says otherwise;
  *   nn_search additionally accepts host pointers (see there).
  * - The caller owns all memory.  The library never frees a caller pointer and
- *   keeps none after return (it may cache its own device workspace).
+ *   keeps none after return (it caches its own device workspace, one per CUDA
+ *   device ordinal: calls on different devices never share scratch memory; calls
+ *   are serialised by a process-wide lock).
+ * - Calls run on the CUDA device current on the calling thread, which must be an
+ *   sm_100 device (checked once per device).
  * - `stream` is a cudaStream_t (NULL = legacy default stream).  The per-kernel
  *   entry points are stream-ordered and asynchronous; nn_search returns when
  *   its outputs are complete.
@@ -97,7 +101,9 @@ int lb_piecewise_sym(const float *q, const float *q_env, const float *db, int64_
  * projection H, both with locality constraint w.  q: device [Q][n] queries;
  * q_env: device [2][Q][n] envelope of q with the same w; db: device [N][n];
  * out: device [Q][N].  Dense form; nn_search evaluates it only on LB_Keogh
- * survivors.  Errors: as lb_keogh, plus EINVAL for w < 0. */
+ * survivors.  Errors: as lb_keogh, plus EINVAL for w < 0, EUNSUPPORTED for
+ * n > 1024 (the survivor kernel keeps a pair's n samples in one warp's registers,
+ * at most 32 per lane). */
 int lb_improved(const float *q, const float *q_env, const float *db, int64_t Q, int64_t N,
                 int32_t n, int32_t w, int32_t p, float *out, void *stream);
 
@@ -174,9 +180,10 @@ typedef struct nn_stats {
  *            (host buffers are staged to the device inside the call);
  *   out_idx: [Q][k] int64 (index_base + row), out_dist: [Q][k] float32 rooted
  *            DTW_p, ascending -- device or host pointers.
- * Errors: EINVAL (n < 1, w < 0, k < 1, Q < 0, N < 1, k > N, NULL pointers),
- * EUNSUPPORTED (p not 1 or 2, k > DTWLB_MAX_K), ENOMEM, ECUDA.  Q == 0 is a
- * no-op.  Synchronous with respect to `stream`. */
+ * Errors: EINVAL (n < 1, w < 0, k < 1, Q < 0, N < 1, k > N, N > 2^32 - 1, NULL
+ * pointers, an output overlapping an input or the other output), EUNSUPPORTED
+ * (p not 1 or 2, k > DTWLB_MAX_K, n > 1024 -- see lb_improved), ENOMEM, ECUDA.
+ * Q == 0 is a no-op.  Synchronous with respect to `stream`. */
 int nn_search(const float *queries, int64_t Q, const float *db, int64_t N, int32_t n, int32_t w,
               int32_t p, int32_t k, int64_t *out_idx, float *out_dist, const nn_opts *opts,
               nn_stats *stats, void *stream);

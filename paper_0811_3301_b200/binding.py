@@ -72,8 +72,8 @@ class NnStats(ctypes.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
-EXPORTS = ["lb_envelope", "lb_keogh", "lb_piecewise", "lb_improved", "dtw_band", "nn_search", "nn_merge",
-           "dtwlb_last_error", "dtwlb_release_workspace"]
+EXPORTS = ["lb_envelope", "lb_keogh", "lb_piecewise", "lb_piecewise_sym", "lb_improved", "dtw_band", "nn_search",
+           "nn_merge", "dtwlb_last_error", "dtwlb_release_workspace"]
 
 _lib = None
 

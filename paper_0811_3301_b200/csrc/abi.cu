@@ -34,27 +34,33 @@ int cuda_fail(cudaError_t e, const char *what, const char *file, int line) {
 }
 
 int require_device() {
-    static int state = -1;  // -1 unknown, 0 ok, else status
-    static char msg[512];
-    if (state < 0) {
-        int dev = 0;
-        cudaError_t e = cudaGetDevice(&dev);
+    // checked once per device ordinal (the current device of the calling thread)
+    constexpr int kMaxDev = 64;
+    static int state[kMaxDev + 1];  // 0 unknown, 1 ok, else 1 + status
+    static char msg[kMaxDev + 1][256];
+    static std::mutex m;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    const int slot = (e != cudaSuccess || dev < 0 || dev >= kMaxDev) ? kMaxDev : dev;
+    std::lock_guard<std::mutex> lock(m);
+    if (state[slot] == 0) {
         cudaDeviceProp prop;
         if (e == cudaSuccess) e = cudaGetDeviceProperties(&prop, dev);
         if (e != cudaSuccess) {
             cudaGetLastError();
-            snprintf(msg, sizeof(msg), "no usable CUDA device: %s", cudaGetErrorString(e));
-            state = DTWLB_ECUDA;
+            snprintf(msg[slot], sizeof(msg[slot]), "no usable CUDA device: %s", cudaGetErrorString(e));
+            state[slot] = 1 + DTWLB_ECUDA;
         } else if (prop.major != 10) {
-            snprintf(msg, sizeof(msg), "device %s is sm_%d%d; libdtwlb is built for sm_100a only", prop.name,
-                     prop.major, prop.minor);
-            state = DTWLB_ECUDA;
+            snprintf(msg[slot], sizeof(msg[slot]), "device %s is sm_%d%d; libdtwlb is built for sm_100a only",
+                     prop.name, prop.major, prop.minor);
+            state[slot] = 1 + DTWLB_ECUDA;
         } else {
-            state = DTWLB_OK;
+            state[slot] = 1;
         }
     }
-    if (state != DTWLB_OK) set_error(state, "%s", msg);
-    return state;
+    const int st = state[slot] - 1;
+    if (st != DTWLB_OK) set_error(st, "%s", msg[slot]);
+    return st;
 }
 
 }  // namespace dtwlb
@@ -240,8 +246,9 @@ int dtw_band(const float *x, const float *y, int32_t n, int32_t w, int32_t p, fl
     a.total = count;
     a.res = out;
     if (w > 64) {
-        float *scratch;
-        DTWLB_TRY(ws_get_bytes(4, sizeof(float) * count * (2 * w + 2), (void **)&scratch));
+        float *scratch = nullptr;
+        if (dtw_generic_needs_scratch(w))
+            DTWLB_TRY(ws_get_bytes(4, sizeof(float) * count * (2 * w + 2), (void **)&scratch));
         DTWLB_TRY(launch_dtw_generic(a, y, scratch, p, false, st));
     } else {
         const int LP = dtw_padded_len(n);
@@ -278,6 +285,17 @@ int nn_search(const float *queries, int64_t Q, const float *db, int64_t N, int32
     }
     if (Q == 0) return DTWLB_OK;
     CHECK_ARG(queries && db && out_idx && out_dist, "nn_search: NULL pointer");
+    {   // outputs may not overlap an input or each other (byte ranges)
+        auto ov = [](const void *a, size_t na, const void *b, size_t nb) {
+            const char *x = static_cast<const char *>(a), *y = static_cast<const char *>(b);
+            return x < y + nb && y < x + na;
+        };
+        const size_t bq = sizeof(float) * (size_t)Q * n, bd = sizeof(float) * (size_t)N * n;
+        const size_t bi = sizeof(int64_t) * (size_t)Q * k, bo = sizeof(float) * (size_t)Q * k;
+        CHECK_ARG(!ov(out_idx, bi, queries, bq) && !ov(out_idx, bi, db, bd) && !ov(out_dist, bo, queries, bq) &&
+                      !ov(out_dist, bo, db, bd) && !ov(out_idx, bi, out_dist, bo),
+                  "nn_search: an output aliases an input or the other output");
+    }
     CHECK_ARG(opts == nullptr || opts->eps >= 0.f, "nn_search: eps < 0");
     DTWLB_TRY(require_device());
     return nn_search_impl(queries, Q, db, N, n, w, p, k, out_idx, out_dist, opts, stats, as_stream(stream));

@@ -5,20 +5,18 @@
 //   D(i,j) = |x_i - y_j|^p + min(D(i-1,j), D(i,j-1), D(i-1,j-1)),  |i-j| <= w,
 //   D(-1,-1) = 0, everything else outside the band = +inf;  DTW_p^p = D(n-1,n-1).
 //
-// B200 design: thread-per-pair with the 2w+1-wide band held in REGISTERS
-// (template WB >= w, exact instantiations for the configs' w), so each cell is
-// the minimal 3-op SASS sequence FADD (x-y), FMNMX3, FADD|abs| / FFMA.  Two rows
-// are advanced per pass in an interleaved order (row i cell d, then row i+1 cell
-// d-1), giving two independent dependency chains per thread and letting both
-// cells share one y value.  The query row is read as 128-bit vectors from four
-// pre-shifted, +inf-padded copies (out-of-range columns cost +inf, so no column
-// tests), i.e. one 16-byte L1-resident load per 8 cells.
-// Early abandoning (not in the paper, reading c15): every path crosses
-// every row and costs are >= 0, so once a row's minimum exceeds the threshold
-// tau^p(1+eps) the pair cannot enter the top-k and is scored +inf.  Lanes are
-// desynchronised: a lane whose pair finishes or is abandoned immediately takes
-// the next pair of its warp's queue (ballot-based refill), so one long pair
-// does not idle the other 31 lanes.
+// B200 design (w <= 64, dtw4_kernel): thread-per-pair with the 2w+1-wide band held
+// in REGISTERS (template WB >= w, exact instantiations for the configs' w), so each
+// cell is the minimal 3-op SASS sequence FADD (x-y), FMNMX3, FADD|abs| / FFMA.  Four
+// rows are advanced per pass, skewed by two cells, so every step holds four
+// independent dependency chains; the query window lives in registers (w <= 32) or
+// is read from shared memory / L1 (32 < w <= 64).  Early abandoning (not in the
+// paper, readings c15, c19): every path crosses every row and costs are
+// >= 0, so once a row's minimum plus the LB_Keogh terms of the rows not yet computed
+// exceeds tau^p(1+eps) the pair cannot enter the top-k.  Lanes are desynchronised
+// and refilled from a work queue through a cp.async pipeline, so one long pair does
+// not idle the other 31 lanes.  w > 64: dtw_generic_kernel (one thread per pair,
+// band in shared memory).
 #include "kernels.cuh"
 
 namespace dtwlb {
@@ -34,83 +32,6 @@ __device__ __forceinline__ float cell(float m, float t) {
     if constexpr (P == 1) return m + fabsf(t);
     else if constexpr (P == 0) return fmaxf(m, fabsf(t));  // DTW_inf: max, exact
     else return fmaf(t, t, m);
-}
-
-// y window loads: shared memory (WALK: the warp's query is staged) or read-only global
-template <bool SMEM>
-__device__ __forceinline__ float4 ld4(const float *p) {
-    if constexpr (SMEM) return *reinterpret_cast<const float4 *>(p);
-    else return __ldg(reinterpret_cast<const float4 *>(p));
-}
-
-__device__ __forceinline__ float f4get(const float4 &v, int k) {
-    return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
-}
-
-// B holds row i-1; computes rows i (x = xa) and i+1 (x = xb); B <- row i+1.
-// ys: aligned pointer with ys[d] = y[i + d - w] (padded), d = 0..2WB+1.
-// Skewed by two cells: at step d row i computes band cell d and row i+1 band cell
-// d-2, whose up (row i, cell d-1) and diagonal (row i, cell d-2) neighbours were
-// produced one and two steps earlier -- the two cells of a step are independent
-// (two dependency chains per thread); row i+1 uses the previous step's y value.
-template <int WB, int P, bool EXACT, bool SMEM>
-__device__ __forceinline__ void two_rows(float (&B)[2 * WB + 2], float xa, float xb,
-                                         const float *__restrict__ ys, int w2) {
-    constexpr int NB = 2 * WB + 1;
-    float a1 = kInf, a2 = kInf, bl = kInf, yp = 0.f;
-    float4 yv4;
-#pragma unroll
-    for (int d = 0; d <= NB + 1; ++d) {
-        float yv = 0.f;
-        if (d <= NB) {
-            if ((d & 3) == 0) yv4 = ld4<SMEM>(ys + d);
-            yv = f4get(yv4, d & 3);
-        }
-        float a = kInf;
-        if (d < NB) {
-            a = cell<P>(min3f(B[d], B[d + 1], a1), xa - yv);
-            if (!EXACT && d > w2) a = kInf;
-        }
-        if (d >= 2) {
-            const int e = d - 2;  // row i+1: up = row i cell e+1 (a1), diag = row i cell e (a2)
-            float b = cell<P>(min3f(a2, a1, bl), xb - yp);
-            if (!EXACT && e > w2) b = kInf;
-            B[e] = b;
-            bl = b;
-        }
-        a2 = a1;
-        a1 = a;
-        yp = yv;
-    }
-}
-
-template <int WB, int P, bool EXACT, bool SMEM>
-__device__ __forceinline__ void one_row(float (&B)[2 * WB + 2], float xa, const float *__restrict__ ys,
-                                        int w2) {
-    constexpr int NB = 2 * WB + 1;
-    float a_prev = kInf;
-    float4 yv4;
-#pragma unroll
-    for (int d = 0; d < NB; ++d) {
-        if ((d & 3) == 0) yv4 = ld4<SMEM>(ys + d);
-        float a = cell<P>(min3f(B[d], B[d + 1], a_prev), xa - f4get(yv4, d & 3));
-        if (!EXACT && d > w2) a = kInf;
-        B[d] = a;
-        a_prev = a;
-    }
-}
-
-// x[i0 .. i0+7] of a candidate row (0 beyond n); vector loads when the row allows it
-__device__ __forceinline__ void load_x8(float (&xv)[8], const float *__restrict__ xr, int i0, int n) {
-    if (((n & 3) == 0) && i0 + 8 <= n) {
-        const float4 a = __ldg(reinterpret_cast<const float4 *>(xr + i0));
-        const float4 b = __ldg(reinterpret_cast<const float4 *>(xr + i0 + 4));
-        xv[0] = a.x; xv[1] = a.y; xv[2] = a.z; xv[3] = a.w;
-        xv[4] = b.x; xv[5] = b.y; xv[6] = b.z; xv[7] = b.w;
-    } else {
-#pragma unroll
-        for (int t = 0; t < 8; ++t) xv[t] = i0 + t < n ? __ldg(xr + i0 + t) : 0.f;
-    }
 }
 
 // LB_Keogh term of row i: d(x_i, [L(y)_i, U(y)_i])^p.  Every banded path visits row i
@@ -228,185 +149,6 @@ __global__ void __launch_bounds__(256) topk_merge_kernel(DtwArgs a) {
     const unsigned cnt = *a.rcount;
     for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x)
         walk_result(a, a.rq[t], a.rkey[t]);
-}
-
-template <int WB, int P, bool EXACT, bool WALK>
-__global__ void __launch_bounds__(NT)
-dtw_kernel(DtwArgs a, int ipw) {
-    constexpr int NB = 2 * WB + 1;
-    const int lane = threadIdx.x & 31;
-    const int64_t gw = ((int64_t)blockIdx.x * NT + threadIdx.x) >> 5;
-    const int n = a.n, w = EXACT ? WB : a.w, w2 = 2 * w;
-    int64_t a0, a1;
-    // WALK: the warp's chunk belongs to one query q (found once per warp)
-    int q = 0;
-    int64_t item_base = 0, lpos = 0;
-    const float *yq = nullptr;
-    float thr_q = kInf;
-    if constexpr (WALK) {
-        if (gw >= a.nchunks) return;
-        int lo = 0, hi = a.Qb;  // chunk_off[lo] <= gw < chunk_off[hi]
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (a.chunk_off[mid] <= gw) lo = mid; else hi = mid;
-        }
-        q = lo;
-        item_base = a.item_off[q];
-        const int64_t cnt = a.item_off[q + 1] - item_base;
-        const int64_t k0 = (gw - a.chunk_off[q]) * (int64_t)ipw;
-        a0 = item_base + k0;
-        a1 = item_base + (cnt < k0 + ipw ? cnt : k0 + ipw);
-        lpos = a.pos[q];
-        // stage the query's four shifted copies in this warp's shared-memory slice:
-        // desynchronised lanes then read 16-byte chunks from shared memory (~4-8
-        // wavefronts per warp load) instead of scattered L1 lines (~32)
-        extern __shared__ __align__(16) float ysm[];
-        float *mine = ysm + (size_t)(threadIdx.x >> 5) * 4 * a.LP;
-        const float *src = a.ysh + (int64_t)q * a.LP;
-        for (int s = 0; s < 4; ++s)
-            for (int t = lane * 4; t < a.LP; t += 128)
-                *reinterpret_cast<float4 *>(mine + s * a.LP + t) =
-                    __ldg(reinterpret_cast<const float4 *>(src + (int64_t)s * a.ysh_stride_s + t));
-        __syncwarp();
-        yq = mine;
-        thr_q = a.thr[q];
-        DCHECK(k0 < cnt, "dtw chunk gw=%lld q=%d k0=%lld cnt=%lld", (long long)gw, q, (long long)k0, (long long)cnt);
-    } else {
-        a0 = gw * ipw;
-        if (a0 >= a.total) return;
-        a1 = (a.total < a0 + ipw) ? a.total : a0 + ipw;
-    }
-
-    int64_t cursor = a0;
-    bool has = false;
-    uint32_t cand = 0;  // WALK: candidate of the lane's pair
-    int64_t item = 0;
-    const float *xr = nullptr, *yb = nullptr;
-    const int64_t ystride = WALK ? a.LP : a.ysh_stride_s;  // elements between shifted copies
-    float thr = kInf;
-    int i = 0;
-    float B[NB + 1];
-    float xv[8];  // x of the current 8-row block
-    // cascading abandon: rest = LB_Keogh^p terms of the rows not yet computed
-    const bool casc = WALK && (a.b1 != nullptr || a.b1h != nullptr);
-    float rest = 0.f;
-    const float *ur = nullptr, *lr = nullptr;
-    unsigned long long rows_done = 0, n_abandon = 0, n_started = 0;
-
-    while (true) {
-        // ---- refill lanes without a pair ----
-        const unsigned need = __ballot_sync(0xffffffffu, !has);
-        if (need) {
-            const int64_t mine = cursor + __popc(need & ((1u << lane) - 1));
-            cursor += __popc(need);
-            if (!has && mine < a1) {
-                item = mine;
-                float beta = 0.f;
-                if constexpr (WALK) {
-                    const int64_t j = lpos + (item - item_base);
-                    DCHECK(j >= 0 && j < a.cap, "dtw item %lld q=%d j=%lld", (long long)item, q, (long long)j);
-                    const unsigned long long key = a.list[(int64_t)q * a.cap + j];
-                    const uint32_t c = (uint32_t)(key & 0xffffffffu);
-                    cand = c;
-                    DCHECK((int64_t)c < a.Ndb, "dtw key c=%u N=%lld q=%d j=%lld key=%llx", c, (long long)a.Ndb, q,
-                           (long long)j, key);
-                    beta = __uint_as_float((uint32_t)(key >> 32));
-                    thr = *reinterpret_cast<volatile float *>(a.thr + q);  // tightened by walk_result
-                    xr = a.db + (int64_t)c * n;
-                    yb = yq;
-                    if (casc) {
-                        rest = fabsf(b1_at(a, (int64_t)q * a.ldb + c));  // beta1 = sum of all row terms
-                        ur = a.Uq + (int64_t)q * n;
-                        lr = a.Lq + (int64_t)q * n;
-                    }
-                } else {
-                    thr = kInf;
-                    xr = a.db + item * n;
-                    yb = a.ysh + item * a.LP;
-                }
-                DCHECK(item < a.total, "dtw item %lld total %lld", (long long)item, (long long)a.total);
-                if (beta > thr) {
-                    if constexpr (!WALK) a.res[item] = kInf;  // (WALK: pruned by its bound, nothing to record)
-                } else {
-                    has = true;
-                    ++n_started;
-                    i = 0;
-                    load_x8(xv, xr, 0, n);
-#pragma unroll
-                    for (int d = 0; d <= NB; ++d) B[d] = kInf;
-#pragma unroll
-                    for (int d = 0; d < NB; ++d)
-                        if (d == w) B[d] = 0.f;  // virtual D(-1,-1) = 0 sits on the diagonal
-                }
-            }
-        }
-        if (!__any_sync(0xffffffffu, has) && cursor >= a1) break;
-
-        bool has_res = false;
-        float res_v = 0.f;
-        if (has) {
-            // ---- advance this lane's pair by up to 8 rows ----
-            // x of this block was loaded with the previous block (or at setup); issue the
-            // loads of the next block now so their latency hides behind this block's cells
-            const int i0 = i, iend = min(n, i + 8);
-            float xn[8];
-            load_x8(xn, xr, iend, n);
-            if (casc) {
-#pragma unroll
-                for (int t = 0; t < 8; ++t)
-                    if (i0 + t < iend) rest -= row_lb<P>(xv[t], __ldg(ur + i0 + t), __ldg(lr + i0 + t));
-            }
-            while (i + 1 < iend) {
-                const int s0 = i - w + kYPadL;
-                const float *ys = yb + (int64_t)(s0 & 3) * ystride + (s0 & ~3);
-                two_rows<WB, P, EXACT, WALK>(B, xv[0], xv[1], ys, w2);
-#pragma unroll
-                for (int t = 0; t < 6; ++t) xv[t] = xv[t + 2];
-                i += 2;
-            }
-            if (i < iend) {
-                const int s0 = i - w + kYPadL;
-                const float *ys = yb + (int64_t)(s0 & 3) * ystride + (s0 & ~3);
-                one_row<WB, P, EXACT, WALK>(B, xv[0], ys, w2);
-                i += 1;
-            }
-#pragma unroll
-            for (int t = 0; t < 8; ++t) xv[t] = xn[t];
-            rows_done += (unsigned long long)(i - i0);
-            if (i >= n) {
-                float r = B[WB];
-                if constexpr (!EXACT) {
-#pragma unroll
-                    for (int d = 0; d < NB; ++d)
-                        if (d == w) r = B[d];
-                }
-                if constexpr (WALK) { has_res = r <= thr; res_v = r; }
-                else a.res[item] = rootp<P>(r);
-                has = false;
-            } else if (band_min<WB>(B) + rest > thr) {
-                if constexpr (!WALK) a.res[item] = kInf;
-                ++n_abandon;  // early abandon (readings c15, c19)
-                has = false;
-            }
-        }
-        if constexpr (WALK) walk_results_warp(a, has_res, q, cand, res_v, lane);
-    }
-    if (a.cells) {
-        unsigned long long cells = rows_done * (unsigned long long)(2 * w + 1);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) cells += __shfl_xor_sync(0xffffffffu, cells, o);
-        if (lane == 0) atomicAdd(a.cells, cells);
-    }
-    if (a.started) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) n_started += __shfl_xor_sync(0xffffffffu, n_started, o);
-        if (lane == 0 && n_started) atomicAdd(a.started, n_started);
-    }
-    if (a.abandoned) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) n_abandon += __shfl_xor_sync(0xffffffffu, n_abandon, o);
-        if (lane == 0 && n_abandon) atomicAdd(a.abandoned, n_abandon);
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -949,24 +691,16 @@ int launch_dtw_t(const DtwArgs &a, cudaStream_t st) {
     // w <= 32: y window in registers (or, DTWLB_DTW_YG=1, read through L1); 32 < w <= 64:
     // the y window read through L1 (the band alone needs 2w+2 registers)
     static const bool env_yg = [] { const char *e = getenv("DTWLB_DTW_YG"); return e && atoi(e); }();
-    if (a.queue) {
-        if constexpr (WB <= 32) {
-            if (env_yg) return launch_dtw4_t<WB, P, EXACT, WALK, true>(a, st);
-            return launch_dtw4_t<WB, P, EXACT, WALK, false>(a, st);
-        } else {
-            return launch_dtw4_t<WB, P, EXACT, WALK, true>(a, st);
-        }
+    if (!a.queue) {
+        set_error(DTWLB_EINVAL, "internal: the DTW kernel needs its work-queue counter");
+        return DTWLB_EINVAL;
     }
-    const int ipw = kDtwIpw;
-    const int64_t warps = WALK ? a.nchunks : ceil_div(a.total, ipw);
-    const int64_t grid = ceil_div(warps * 32, NT);
-    const size_t smem = WALK ? (size_t)(NT / 32) * 4 * a.LP * sizeof(float) : 0;
-    if (smem > 48 * 1024)
-        DTWLB_CUDA(cudaFuncSetAttribute(dtw_kernel<WB, P, EXACT, WALK>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    dtw_kernel<WB, P, EXACT, WALK><<<(unsigned)grid, NT, smem, st>>>(a, ipw);
-    DTWLB_LAUNCH_CHECK();
-    return DTWLB_OK;
+    if constexpr (WB <= 32) {
+        if (env_yg) return launch_dtw4_t<WB, P, EXACT, WALK, true>(a, st);
+        return launch_dtw4_t<WB, P, EXACT, WALK, false>(a, st);
+    } else {
+        return launch_dtw4_t<WB, P, EXACT, WALK, true>(a, st);
+    }
 }
 
 template <int P, bool WALK>
@@ -1031,6 +765,8 @@ int launch_dtw(const DtwArgs &a, int p, bool walk, cudaStream_t st) {
     return walk ? launch_dtw_p<2, true>(a, st) : launch_dtw_p<2, false>(a, st);
 }
 
+bool dtw_generic_needs_scratch(int w) { return (size_t)128 * ((2 * w + 2) | 1) * sizeof(float) > 200 * 1024; }
+
 int launch_dtw_generic(const DtwArgs &a, const float *yraw, float *scratch, int p, bool walk,
                        cudaStream_t st) {
     if (a.total == 0) return DTWLB_OK;
@@ -1039,7 +775,7 @@ int launch_dtw_generic(const DtwArgs &a, const float *yraw, float *scratch, int 
     // threads' same-index cells fall in different banks), else in the global scratch
     int pitch = (2 * a.w + 2) | 1;
     size_t smem = (size_t)128 * pitch * sizeof(float);
-    if (smem > 200 * 1024) { pitch = 0; smem = 0; }
+    if (dtw_generic_needs_scratch(a.w)) { pitch = 0; smem = 0; }
     if (smem > 48 * 1024) {
         DTWLB_CUDA(cudaFuncSetAttribute(dtw_generic_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         DTWLB_CUDA(cudaFuncSetAttribute(dtw_generic_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

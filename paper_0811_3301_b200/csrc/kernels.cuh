@@ -140,6 +140,8 @@ constexpr int kYPadL = 64;
 constexpr int kDtwIpw = 64;  // items per warp chunk of the DTW walk  // left padding of query rows (>= largest register band)
 int dtw_padded_len(int n);
 int launch_dtw(const DtwArgs &a, int p, bool walk, cudaStream_t st);
+// w > 64: does the generic kernel need a global band scratch of (2w+2) floats per item?
+bool dtw_generic_needs_scratch(int w);
 // Build the 4 shifted, +inf-padded copies of `rows` query rows.
 int launch_build_ysh(const float *y, int64_t rows, int n, float *ysh, int LP, cudaStream_t st);
 

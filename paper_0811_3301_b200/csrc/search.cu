@@ -37,13 +37,21 @@ int launch_dtw_generic(const DtwArgs &a, const float *yraw, float *scratch, int 
 // ------------------------------------------------------------------ workspace
 namespace {
 
+// One workspace per CUDA device ordinal: a process may call the library on several devices
+// (each call uses the workspace of the device current on the calling thread).
 struct Workspace {
+    int device = -1;  // owner ordinal (set on first allocation)
     std::vector<void *> ptr;
     std::vector<size_t> size;
     ~Workspace() { release(); }
     void release() {
+        if (ptr.empty()) return;
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (device >= 0 && device != cur) cudaSetDevice(device);
         for (void *p : ptr)
             if (p) cudaFree(p);
+        if (device >= 0 && device != cur) cudaSetDevice(cur);
         ptr.clear();
         size.clear();
     }
@@ -53,6 +61,7 @@ struct Workspace {
         bytes = std::max<size_t>(bytes, 256);
         if (size[slot] < bytes) {
             if (ptr[slot]) { cudaDeviceSynchronize(); cudaFree(ptr[slot]); ptr[slot] = nullptr; size[slot] = 0; }
+            if (device < 0) cudaGetDevice(&device);
             cudaError_t e = cudaMalloc(&ptr[slot], bytes);
             if (e != cudaSuccess) {
                 cudaGetLastError();
@@ -67,9 +76,15 @@ struct Workspace {
     }
 };
 
-Workspace &ws() {
-    static Workspace w;
+constexpr int kMaxDevices = 64;
+Workspace *ws_all() {
+    static Workspace w[kMaxDevices];
     return w;
+}
+Workspace &ws() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) { cudaGetLastError(); d = 0; }
+    return ws_all()[d];
 }
 std::mutex &ws_mutex() {
     static std::mutex m;
@@ -564,10 +579,18 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     // the block-sized slots this call would reuse count as free: the block size (hence the
     // pipeline) is then the same on every call of a given problem, not smaller after the first
     for (int sl : {S_BETA1, S_LIST, S_RES, S_MASK}) free_b += ws().cur_size(sl);
-    const size_t per_q = (size_t)N * (prefilter ? 10 : 12) + 4096;  // gate (2 or 4 B) + list (8 B) per pair
+    // per query of the block: gate bound (2 B fp16 with the pre-filter, else 4 B) + key list (8 B)
+    // per pair, a walk round's completed-pair slots (12 B per item, <= min(N, kDMax) items),
+    // the survivor pass's (query, mask) entries (12 B per 64-candidate tile) and the sort's runs
+    const size_t gate_elem = prefilter ? 2 : 4;
+    const int64_t round_items = std::min<int64_t>(N, kDMax);
+    const size_t per_q = (size_t)N * (gate_elem + 8) + (size_t)round_items * 12 + (size_t)ceil_div(N, 64) * 12 +
+                         (size_t)ceil_div(N, kRun) * 8 + 4096;
     static const double env_mem = [] { const char *e = getenv("DTWLB_BLOCK_MEM_FRAC"); return e ? atof(e) : 0.0; }();
     const double mem_frac = env_mem > 0 ? env_mem : 0.45;
     int64_t Qb = opts && opts->query_block > 0 ? opts->query_block : (int64_t)(free_b * mem_frac / per_q);
+    // a walk round holds <= Qb * min(N, kDMax) items, counted in int32 (plan_kernel, dtw4_kernel)
+    Qb = std::min<int64_t>(Qb, (int64_t)(0x7fffffff - 1024) / round_items);
     Qb = std::max<int64_t>(1, std::min<int64_t>(Qb, Q));
     if (Qb >= 64) Qb = Qb / 64 * 64;
     if (!(opts && opts->query_block > 0) && Qb >= 64) {  // balance the blocks (e.g. 2 x 4096, not 7168 + 1024)
@@ -579,9 +602,13 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
 
     float *beta1;
     unsigned long long *list;
-    DTWLB_TRY(wsget(S_BETA1, (size_t)Qb * ldb, &beta1));  // float (or __half with the pre-filter)
+    {   // float, or __half with the pre-filter
+        void *g = nullptr;
+        DTWLB_TRY(ws().get(S_BETA1, (size_t)Qb * ldb * gate_elem, &g));
+        beta1 = static_cast<float *>(g);
+    }
     DTWLB_TRY(wsget(S_LIST, (size_t)Qb * cap, &list));
-    const int64_t res_cap = std::min<int64_t>(Qb * cap, Qb * (int64_t)kDMax);  // items of one walk round
+    const int64_t res_cap = Qb * round_items;  // items of one walk round (< 2^31, see Qb)
     char *rbuf;  // completed pairs of a round: keys [res_cap] u64 + queries [res_cap] int
     DTWLB_TRY(wsget(S_RES, (size_t)res_cap * 12 + 64, &rbuf));
     char *imp_scratch;
@@ -609,8 +636,6 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         s.chunk_off = reinterpret_cast<int *>(take((Qb + 1) * 4));
     }
     DTWLB_TRY(wsget(S_TOPK, (size_t)Qb * k, &s.topk));
-    float *scratch = nullptr;
-    if (generic_dtw) DTWLB_TRY(wsget(S_SCRATCH, (size_t)res_cap * (2 * w + 2), &scratch));
     DTWLB_CUDA(cudaMemsetAsync(s.stat, 0, 8 * 8, st));
 
     // target size of the first (best-first) range: ~kSeedCap candidates per query.  Measured at
@@ -803,6 +828,11 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                         }
                     }
                     if (generic_dtw) {
+                        // global band scratch only when 128 bands do not fit in shared memory,
+                        // sized by this round's item count
+                        float *scratch = nullptr;
+                        if (dtw_generic_needs_scratch(w))
+                            DTWLB_TRY(wsget(S_SCRATCH, (size_t)tot2[0] * (2 * w + 2), &scratch));
                         const cudaEvent_t d0 = stats ? rec() : nullptr;
                         DTWLB_TRY(launch_dtw_generic(da, queries + qb0 * n, scratch, p, true, st));
                         if (stats) span(d0, rec(), &ms_dtw_kernel);
@@ -921,7 +951,7 @@ std::mutex &api_mutex() { return ws_mutex(); }
 void release_workspace() {
     std::lock_guard<std::mutex> lock(ws_mutex());
     cudaDeviceSynchronize();
-    ws().release();
+    for (int d = 0; d < kMaxDevices; ++d) ws_all()[d].release();
 }
 
 }  // namespace dtwlb

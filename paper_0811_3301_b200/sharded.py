@@ -66,7 +66,16 @@ def sharded_nn_search(queries: torch.Tensor, db_shard: torch.Tensor, shard_lo: i
     if world > 1:
         # all ranks use the same blocking; thresholds are min-reduced after each block's first range
         kw["query_block"] = query_block or common_query_block(db_shard.shape[0], group, dev)
-        kw["exchange"] = lambda thr: dist.all_reduce(thr, op=dist.ReduceOp.MIN, group=group)
+        if kk >= k:
+            kw["exchange"] = lambda thr: dist.all_reduce(thr, op=dist.ReduceOp.MIN, group=group)
+        else:
+            # a shard with fewer than k rows: its kk-th best is NOT an upper bound on the global
+            # k-th best, so it contributes +inf and only receives the other shards' minimum
+            def _ex_small(thr):
+                t = torch.full_like(thr, float("inf"))
+                dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+                torch.minimum(thr, t, out=thr)
+            kw["exchange"] = _ex_small
     if kk > 0:
         if out_local is not None and kk == k:
             idx, dst = search(queries, db_shard, w, p, k, index_base=shard_lo, out=out_local, **kw)
@@ -96,17 +105,3 @@ def sharded_nn_search(queries: torch.Tensor, db_shard: torch.Tensor, shard_lo: i
     dist.all_gather_into_tensor(g_dst, dst.contiguous(), group=group)
     return merge(g_idx.view(world, Q, k), g_dst.view(world, Q, k))
 
-
-def merge_reference(g_idx: torch.Tensor, g_dst: torch.Tensor):
-    """Host reference of nn_merge (tests): k smallest by (dist, idx), ignoring idx < 0."""
-    G, Q, k = g_idx.shape
-    out_i = torch.full((Q, k), -1, dtype=torch.int64)
-    out_d = torch.full((Q, k), float("inf"), dtype=torch.float32)
-    for q in range(Q):
-        cand = [(float(g_dst[g, q, j]), int(g_idx[g, q, j])) for g in range(G) for j in range(k)
-                if int(g_idx[g, q, j]) >= 0]
-        cand.sort()
-        for r, (d, i) in enumerate(cand[:k]):
-            out_i[q, r] = i
-            out_d[q, r] = d
-    return out_i, out_d

@@ -30,6 +30,11 @@ def test_header_declares_the_boundary():
         assert f in fns, fns
 
 
+def test_binding_exports_match_header():
+    from paper_0811_3301_b200 import binding
+    assert sorted(binding.EXPORTS) == _header_functions()
+
+
 def test_library_exports_every_declared_symbol(lib):
     so = ctypes.CDLL(os.path.join(ROOT, "paper_0811_3301_b200", "libdtwlb.so"))
     for f in _header_functions():

@@ -208,3 +208,21 @@ def test_full_size_sampled(cuda_ok, name, sample):
     # properties at any size: ascending, finite, distinct, in range
     assert np.all(np.diff(dist, axis=1) >= 0) and np.all(np.isfinite(dist))
     assert idx.min() >= 0 and idx.max() < c.N
+
+
+def test_output_aliasing_rejected(cuda_ok):
+    """nn_search rejects outputs that overlap an input or each other (EINVAL, include/dtwlb.h)."""
+    from paper_0811_3301_b200 import DtwlbError, nn_search
+    qs, db = datagen.make("C2p1", Q=4, N=500)
+    q_t, db_t = dev(qs), dev(db)
+    idx = torch.empty((4, 2), dtype=torch.int64, device="cuda")
+    dst = torch.empty((4, 2), dtype=torch.float32, device="cuda")
+    with pytest.raises(DtwlbError, match="EINVAL"):
+        nn_search(q_t, db_t, 25, 1, 2, out=(idx, q_t[0, :8]))            # dist over the queries
+    with pytest.raises(DtwlbError, match="EINVAL"):
+        nn_search(q_t, db_t, 25, 1, 2, out=(db_t.view(torch.int64)[:4, :2], dst))  # idx over the db
+    buf = torch.empty(64, dtype=torch.int64, device="cuda")
+    with pytest.raises(DtwlbError, match="EINVAL"):
+        nn_search(q_t, db_t, 25, 1, 2, out=(buf[:8].view(4, 2), buf.view(torch.float32)[4:12].view(4, 2)))
+    i2, d2 = nn_search(q_t, db_t, 25, 1, 2, out=(idx, dst))  # disjoint: fine
+    assert i2.data_ptr() == idx.data_ptr()

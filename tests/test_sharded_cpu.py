@@ -75,7 +75,8 @@ def _worker_exchange(rank, world, port, N, k, result_q):
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        from paper_0811_3301_b200.sharded import merge_reference, shard_range, sharded_nn_search
+        from paper_0811_3301_b200.sharded import shard_range, sharded_nn_search
+        from shard_ref import merge_reference
         cfg = datagen.CONFIGS["C2p2"]
         lo, hi = shard_range(N, world, rank)
         qs, _ = datagen.make(cfg, Q=4, N=0)
@@ -144,7 +145,8 @@ def _worker_body(rank, world, port, N, k, result_q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_0811_3301_b200.sharded import merge_reference, shard_range, sharded_nn_search
+    from paper_0811_3301_b200.sharded import shard_range, sharded_nn_search
+    from shard_ref import merge_reference
     cfg = datagen.CONFIGS["C2p2"]
     lo, hi = shard_range(N, world, rank)
     qs, _ = datagen.make(cfg, Q=5, N=0)
@@ -194,3 +196,72 @@ def test_shard_ranges_partition():
             assert all(r[i][1] == r[i + 1][0] for i in range(G - 1))
             sizes = [b - a for a, b in r]
             assert max(sizes) - min(sizes) <= 1
+
+
+def _worker_unbalanced(rank, world, port, bounds, k, result_q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_0811_3301_b200.sharded import sharded_nn_search
+        from shard_ref import merge_reference
+        cfg = datagen.CONFIGS["C2p2"]
+        lo, hi = bounds[rank], bounds[rank + 1]
+        qs, _ = datagen.make(cfg, Q=4, N=0)
+        qs = np.ascontiguousarray(qs[:, :32])
+        shard = np.ascontiguousarray(
+            datagen.series(cfg.family, hi - lo, cfg.n, cfg.seed, datagen.ROLE_DB, cfg.znorm, start=lo)[:, :32])
+        if rank == 0:  # rank 0's two rows are query 0's nearest: its 2nd best is far below the global 5th
+            shard[0] = qs[0]
+            shard[1] = qs[0] * np.float32(0.999)
+        sent = []
+
+        def search(queries, db, w, p, kk, index_base=0, out=None, query_block=None, exchange=None):
+            def ex(t):
+                exchange(t)
+                sent.append(t.numpy().copy())
+            return _cascade_search(queries, db, w, p, kk, index_base, out, query_block, ex)
+
+        idx, dst = sharded_nn_search(torch.from_numpy(qs), torch.from_numpy(shard), lo, 3, cfg.p, k,
+                                     search=search, merge=merge_reference, query_block=4)
+        result_q.put((rank, idx.numpy(), dst.numpy(), sent))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:
+        result_q.put((rank, None, repr(e), None))
+        raise
+
+
+def test_unbalanced_shard_smaller_than_k():
+    """a shard with fewer than k rows must not contribute its own kk-th best to the
+    threshold exchange (it is no upper bound on the global k-th best).  Rank 0 holds 2 rows,
+    rank 1 holds 38, k = 5: every rank must still return the brute-force k-NN of all 40 rows,
+    and the threshold rank 1 receives is its own k-th best (rank 0 sends +inf)."""
+    world, k = 2, 5
+    bounds = [0, 2, 40]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_unbalanced, args=(r, world, port, bounds, k, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    res.sort(key=lambda r: r[0])
+    for r in res:
+        assert r[1] is not None, r[2]
+    cfg = datagen.CONFIGS["C2p2"]
+    qs, db = datagen.make(cfg, Q=4, N=40)
+    qs, db = np.ascontiguousarray(qs[:, :32]), np.ascontiguousarray(db[:, :32])
+    db[0] = qs[0]
+    db[1] = qs[0] * np.float32(0.999)
+    o_idx, o_dst = oracle.nn_brute(qs, db, 3, cfg.p, k)
+    for rank, idx, dst, sent in res:
+        assert np.array_equal(idx, o_idx)
+        assert np.allclose(dst, o_dst, rtol=1e-6)
+    # rank 1's thresholds after the exchange are bounded below by the global k-th best
+    kth = (o_dst[:, k - 1].astype(np.float64) ** cfg.p)
+    for t in res[1][3]:
+        assert np.all(t >= kth * (1 - 1e-6))
