@@ -123,7 +123,20 @@ def oracle_sample(cfg, qs, db, budget_s=15.0, threads=None):
     dt = time.perf_counter() - t0
     return {"value": nq * len(db) / dt, "unit": "pairs/s", "cores": min(threads, nq), "kind": "oracle",
             "sample": f"{nq} of {cfg.Q} queries x all {len(db)} database series (Alg. 3 fp64 scan, "
-                      f"{min(threads, nq)} threads, {dt:.1f} s)", "seconds": dt}
+                      f"{min(threads, nq)} threads, {dt:.1f} s)", "seconds": dt,
+            "single_thread": {"value": len(db) / per_q, "unit": "pairs/s",
+                              "sample": f"query 0 x all {len(db)} series, 1 thread, {per_q:.2f} s"},
+            "cpu_model": _cpu_model(), "host_threads": os.cpu_count()}
+
+
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 def run_reference(args, cfg):
@@ -187,10 +200,24 @@ def run_ours(args, cfg):
     gbufs = (torch.empty((ws * cfg.Q, k), dtype=torch.int64, device=dev),
              torch.empty((ws * cfg.Q, k), dtype=torch.float32, device=dev))
     last = {}
+    # few queries (Q <= 8, n % 4 == 0): nn_search's streaming bound pass (no pre-filter)
+    stream_mode = cfg.Q <= 8 and cfg.n % 4 == 0 and not args.no_stream
+    pf = not args.no_prefilter and not stream_mode  # the piecewise-sum pre-filter runs
+    db_env, index_ms = None, None
+    if args.db_index:  # the database index (envelopes of the rows), built once outside the timed region
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        U_, L_ = B.lb_envelope(db, cfg.w)
+        db_env = torch.stack([U_, L_]).contiguous()
+        e1.record(st)
+        torch.cuda.synchronize()
+        index_ms = e0.elapsed_time(e1)
+        del U_, L_
 
     def search(q_, d_, w_, p_, k_, index_base=0, out=None, **kw):  # kw: query_block, exchange (N > 1)
         i_, d2, st_ = B.nn_search(q_, d_, w_, p_, k_, index_base=index_base, out=out, return_stats=True,
-                                  prefilter=not args.no_prefilter, keogh_only=args.keogh_only, **kw)
+                                  prefilter=not args.no_prefilter, keogh_only=args.keogh_only,
+                                  stream=not args.no_stream, db_env=db_env, **kw)
         last["st"] = st_
         return i_, d2
 
@@ -235,7 +262,7 @@ def run_ours(args, cfg):
     def e2e_step():
         if ws == 1:  # the C-ABI host-pointer path: the library stages H2D / D2H itself
             B.nn_search(qs_pin, db_pin, cfg.w, cfg.p, k, index_base=lo, out=(h_idx, h_dst),
-                        prefilter=not args.no_prefilter, keogh_only=args.keogh_only)
+                        prefilter=not args.no_prefilter, keogh_only=args.keogh_only, stream=not args.no_stream)
         else:  # H2D of the shard + queries, sharded search (exchange, all-gather, merge), D2H
             q_dev.copy_(qs_pin, non_blocking=True)
             d_dev.copy_(db_pin, non_blocking=True)
@@ -284,45 +311,51 @@ def run_ours(args, cfg):
     if rank == 0:
         pk = _peaks()
         sm_clock = 1965.0 if not pk else float(pk.get("sm_max_mhz", 1965.0))
+        hbm_peak = 6533.5 if not pk else float(pk.get("hbm_gbs", 6533.5))
         n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-        # FP32/ALU issue peak: SMs x 128 FP32 lanes x max SM clock (guide unit counts)
+        # ALU issue peak: SMs x 4 schedulers x 32 lanes (one warp-instruction per scheduler per
+        # clock = 128 lane-slots per SM per clock) x the max SM clock (guide unit counts)
         peak = n_sm * 128 * sm_clock * 1e6 / 1e12
-        # dense gate pass: 4 SASS lane-ops (FADD, FADD, FMNMX3, FADD|FFMA) per pair-element over
-        # Dp = round_up(ceil(n/8), 4) segment sums (pre-filter) or n samples (LB_Keogh)
-        # (the pre-filter is symmetric: a forward and a reverse launch, Dp elements each)
-        elems = 2 * (((cfg.n + 7) // 8 + 3) // 4 * 4) if not args.no_prefilter else cfg.n
-        gate_ops = 4.0 * (cfg.Q * (cfg.N // ws)) * elems
-        # survivor kernel (dominant with the pre-filter): algorithmic lane-ops = 4 n per in-kernel
-        # LB_Keogh evaluation (FADD, FADD, FMNMX3, FFMA) + 6 n per LB_Improved evaluation
-        # (FMNMX, FMNMX, FADD, FADD, FMNMX3, FFMA), counted by the kernel itself
-        k_in_kernel = keogh_eval if not args.no_prefilter else 0.0
-        surv_ops = 4.0 * cfg.n * k_in_kernel + 6.0 * cfg.n * improved
-        # the dominant single kernel by device time per step: the survivor kernel, the DTW
-        # kernel (all walk-round launches) or one gate launch (each about half the symmetric gate
-        # pass; the LB_Keogh pass without the pre-filter is one launch)
-        gate_kernel_ms = keogh_ms / 2 if not args.no_prefilter else keogh_ms
-        cand = [("gate", gate_kernel_ms), ("dtw", dtw_kernel_ms)]
-        if not args.no_prefilter:
-            cand.append(("surv", surv_ms))
-        dom = max(cand, key=lambda t: t[1])[0]
-        if dom == "surv":
-            rk = {"kernel": "improved_kernel (survivor pass: LB_Keogh + LB_Improved on sparse pairs)",
-                  "ms": surv_ms, "ops": surv_ops,
-                  "note": "4n lane-ops per LB_Keogh + 6n per LB_Improved evaluation (kernel counters)"}
-        elif dom == "dtw":
-            # banded DTW: FADD (x - y), FMNMX3 (min of three neighbours), FFMA|FADD (accumulate)
-            # = 3 lane-ops per computed cell (the kernel counts the cells it computes)
-            rk = {"kernel": "dtw4_kernel (banded DTW walk, w <= 32)" if cfg.w <= 32 else
-                            "dtw_kernel (banded DTW walk)",
-                  "ms": dtw_kernel_ms, "ops": 3.0 * cells_cmp,
-                  "note": "3 lane-ops per computed DTW cell (kernel counter), event time of all walk launches"}
+        Nr = cfg.N // ws  # rows per rank
+        kern = {}
+        # Minimal algorithmic issue slots per unit (sm_100a SASS):
+        #  bound element (LB_Keogh, piecewise-sum): FADD2 (two elements' two subtractions, so 1 per
+        #    element), FMNMX3 (max with 0), FFMA|FADD (accumulate)                   = 3
+        #  LB_Improved element: FMNMX, FMNMX (envelope of H), FADD2 (1), FMNMX3, FFMA  = 5
+        #  DTW cell (in the band |i-j| <= w, 0 <= j < n): FADD (x - y), FMNMX3, FADD|FFMA = 3
+        if stream_mode:
+            # HBM-bound: the database read once + beta1 written, per launch (one launch per step)
+            bytes_ = cfg.N * cfg.n * 4 + cfg.Q * cfg.N * 4 + 2 * cfg.Q * cfg.n * 4
+            kern["bound_pass"] = {"kernel": "keogh_stream_kernel (LB_Keogh, TMA-streamed database)",
+                                  "bound": "hbm", "ms": keogh_ms, "work": bytes_ / 1e9, "unit": "GB/s",
+                                  "peak": hbm_peak, "launches": 1,
+                                  "note": "N*n*4 database bytes + Q*N*4 bound bytes per launch"}
         else:
-            rk = {"kernel": "keogh_tile_kernel (dense gate pass: " +
-                            ("piecewise-sum bound" if not args.no_prefilter else "LB_Keogh") + ")",
-                  "ms": keogh_ms, "ops": gate_ops,
-                  "note": f"4 lane-ops per pair-element, {elems} elements per pair" +
-                          (" (forward + reverse)" if not args.no_prefilter else "")}
-        achieved = rk["ops"] / (rk["ms"] * 1e-3) / 1e12
+            elems = 2 * (((cfg.n + 7) // 8 + 3) // 4 * 4) if pf else cfg.n
+            kern["bound_pass"] = {"kernel": "keogh_tile_kernel (" + ("piecewise-sum gate, forward + reverse"
+                                                                      if pf else "LB_Keogh") + ")",
+                                  "bound": "alu", "ms": keogh_ms, "work": 3.0 * cfg.Q * Nr * elems / 1e12,
+                                  "unit": "Tlane-op/s", "peak": peak, "launches": 2 if pf else 1,
+                                  "note": f"3 slots per pair-element, {elems} elements per pair"}
+        if surv_ms > 0:
+            k_in_kernel = keogh_eval if pf else 0.0
+            kern["survivor_kernel"] = {"kernel": "improved_kernel (LB_Keogh + LB_Improved on sparse pairs)",
+                                       "bound": "alu", "ms": surv_ms,
+                                       "work": (3.0 * k_in_kernel + 5.0 * improved) * cfg.n / 1e12,
+                                       "unit": "Tlane-op/s", "peak": peak,
+                                       "note": "3n slots per LB_Keogh + 5n per LB_Improved evaluation (kernel counters)"}
+        if dtw_kernel_ms > 0:
+            kern["dtw_kernel"] = {"kernel": "dtw4_kernel (banded DTW walk)" if cfg.w <= 64 else
+                                  "dtw_generic_kernel (banded DTW walk, w > 64)",
+                                  "bound": "alu", "ms": dtw_kernel_ms, "work": 3.0 * cells_cmp / 1e12,
+                                  "unit": "Tlane-op/s", "peak": peak,
+                                  "note": "3 slots per in-band DTW cell actually computed (kernel counter, early "
+                                          "abandon), CUDA events around every walk-round launch"}
+        for v in kern.values():
+            v["achieved"] = v["work"] / (v["ms"] * 1e-3) if v["ms"] > 0 else 0.0
+            v["frac"] = v["achieved"] / v["peak"]
+        dom_name = max(kern, key=lambda kk: kern[kk]["ms"] / kern[kk].get("launches", 1))
+        rk = kern[dom_name]
         traffic, traffic_note = None, None
         tpath = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tpath):
@@ -349,13 +382,19 @@ def run_ours(args, cfg):
             "data": "synthetic",
             "config": {"workload": cfg.name, "Q": cfg.Q, "N": cfg.N, "n": cfg.n, "w": cfg.w, "p": cfg.p,
                        "k": cfg.k, "family": cfg.family, "parallelism": f"db-shard{ws}",
+                       "mode": ("stream" if stream_mode else ("prefilter" if pf else "alg3")) +
+                               ("+keogh_only" if args.keogh_only else ""),
+                       "db_index": ({"prebuilt": True, "build_ms": index_ms} if args.db_index else None),
                        "l2": f"inputs larger than L2 ({cfg.N * cfg.n * 4 / 1e9:.2f} GB database)"},
             "dtw_cells_per_s": cells_cmp / (ms_max * 1e-3),
             "dtw_cells_nominal_per_s": cells_nom / (ms_max * 1e-3),
+            "dtw_kernel_cells_per_s": ({"computed": cells_cmp / (dtw_kernel_ms * 1e-3),
+                                        "nominal": cells_nom / (dtw_kernel_ms * 1e-3)}
+                                       if dtw_kernel_ms > 0 else None),
             "walk": {k2: statistics.mean(s[k2] for s in stats_all)
                      for k2 in ("range1_improved", "range1_dtw", "range1_cells", "walk_rounds", "dtw_evaluated",
                                 "dtw_cells_computed")},
-            "prune": {"prefilter": not args.no_prefilter, "keogh_only": bool(args.keogh_only),
+            "prune": {"prefilter": pf, "stream_mode": stream_mode, "keogh_only": bool(args.keogh_only),
                       "keogh_evaluated_frac": keogh_eval / pairs,
                       "keogh_pruned_frac": 1 - improved / pairs,
                       "improved_evaluated_frac": improved / pairs,
@@ -364,19 +403,15 @@ def run_ours(args, cfg):
             "stage_ms": {k2: statistics.mean(s[k2] for s in stats_all)
                          for k2 in ("ms_envelope", "ms_keogh", "ms_select", "ms_improved", "ms_survivor_kernel", "ms_dtw_kernel",
                                     "ms_dtw", "ms_total")},
-            "roofline": {"kernel": rk["kernel"], "bound": "alu", "achieved": achieved, "peak": peak,
-                         "unit": "Tlane-op/s", "frac": achieved / peak, "traffic": traffic,
-                         "peak_note": f"{n_sm} SMs x 128 FP32 lanes x {sm_clock:.0f} MHz (guide unit counts, "
-                                      "MEASURED_PEAKS sm_max_mhz)",
+            "roofline": {"kernel": rk["kernel"], "bound": rk["bound"], "achieved": rk["achieved"],
+                         "peak": rk["peak"], "unit": rk["unit"], "frac": rk["frac"], "traffic": traffic,
+                         "peak_note": (f"{n_sm} SMs x 128 lane-slots/clk x {sm_clock:.0f} MHz (guide unit counts, "
+                                       "MEASURED_PEAKS sm_max_mhz)" if rk["bound"] == "alu" else
+                                       "MEASURED_PEAKS hbm_gbs (measured copy bandwidth)"),
                          "ops_note": rk["note"], "kernel_ms": rk["ms"], "traffic_note": traffic_note,
-                         "gate_pass": {"ms": keogh_ms, "achieved": gate_ops / (keogh_ms * 1e-3) / 1e12,
-                                       "frac": gate_ops / (keogh_ms * 1e-3) / 1e12 / peak},
-                         "survivor_kernel": ({"ms": surv_ms, "achieved": surv_ops / (surv_ms * 1e-3) / 1e12,
-                                              "frac": surv_ops / (surv_ms * 1e-3) / 1e12 / peak}
-                                             if surv_ms > 0 else None),
-                         "dtw_kernel": ({"ms": dtw_kernel_ms, "achieved": 3.0 * cells_cmp / (dtw_kernel_ms * 1e-3) / 1e12,
-                                         "frac": 3.0 * cells_cmp / (dtw_kernel_ms * 1e-3) / 1e12 / peak}
-                                        if dtw_kernel_ms > 0 else None)},
+                         "dominant": dom_name,
+                         **{kn: {x: v[x] for x in ("kernel", "bound", "ms", "achieved", "peak", "unit", "frac")}
+                            for kn, v in kern.items()}},
             "e2e": {"value": pairs / (e2e_ms * 1e-3), "unit": "pairs/s",
                     # whole job: every rank copies the queries and its shard in, its result out
                     "h2d_bytes_per_step": int(qs_h.nbytes * ws + cfg.N * cfg.n * 4),
@@ -404,6 +439,11 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--keogh-only", action="store_true",
                     help="Alg. 2 (LB_Keogh then DTW, no LB_Improved pass): the paper's comparison point")
+    ap.add_argument("--no-stream", action="store_true",
+                    help="Q <= 8: the tiled bound pass instead of the streaming one (DTWLB_NO_STREAM)")
+    ap.add_argument("--db-index", action="store_true",
+                    help="build the database index (row envelopes, nn_opts.db_env) once before the timed "
+                         "region and reuse it in every step")
     ap.add_argument("--no-prefilter", action="store_true",
                     help="LB_Keogh over every pair (Alg. 3 as printed) instead of the piecewise-sum pre-filter")
     ap.add_argument("--w", type=int, default=None,

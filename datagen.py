@@ -61,6 +61,12 @@ CONFIGS = {
     "C3": Config("C3", 1_000, 100_000, 1_000, 50, 2, 1, "rw", True, 3),
     "C4": Config("C4", 4_096, 200_000, 512, 51, 1, 1, "shape", True, 4),
     "C5": Config("C5", 8_192, 1_000_000, 256, 25, 2, 10, "rw", True, 5),
+    # C5-stream (SURVEY 8(d) added row): the first Q in {1, 2, 4, 8} C5 queries against the C5
+    # database -- the memory-bound regime of the bound pass (BASELINE "bound passes >= 60% HBM")
+    "C5s1": Config("C5s1", 1, 1_000_000, 256, 25, 2, 10, "rw", True, 5),
+    "C5s2": Config("C5s2", 2, 1_000_000, 256, 25, 2, 10, "rw", True, 5),
+    "C5s4": Config("C5s4", 4, 1_000_000, 256, 25, 2, 10, "rw", True, 5),
+    "C5s8": Config("C5s8", 8, 1_000_000, 256, 25, 2, 10, "rw", True, 5),
 }
 
 

@@ -65,7 +65,8 @@ int lb_envelope(const float *x, int32_t n, int32_t w, float *U, float *L, int64_
  * q_env: device [2][Q][n] (the U block of all Q queries, then the L block), as
  * written by lb_envelope into a contiguous buffer.  db: device [N][n].
  * out: device [Q][N] float32.  This is the dense (test / inspection) form of
- * the bound pass that nn_search fuses.
+ * the bound pass that nn_search fuses.  Q <= 8 (n % 4 == 0, 16-byte aligned db)
+ * runs the streaming kernel nn_search uses for few queries, else the tiled one.
  * Errors: EINVAL (sizes, NULL, n < 1), EUNSUPPORTED (p not 1 or 2). */
 int lb_keogh(const float *q_env, const float *db, int64_t Q, int64_t N, int32_t n, int32_t p,
              float *out, void *stream);
@@ -127,7 +128,7 @@ typedef struct nn_opts {
     int32_t flags;         /* DTWLB_KEOGH_ONLY: skip the LB_Improved pass (Alg. 2);
                               DTWLB_NO_PREFILTER: LB_Keogh over every pair (Alg. 3
                               literally) instead of the piecewise-sum pre-filter;
-                              DTWLB_NO_CASCADE: see below                           */
+                              DTWLB_NO_CASCADE, DTWLB_NO_STREAM: see below          */
     /* Database-sharded search: called once per query block after the
      * first (best-first) range, with thr = DEVICE pointer to the block's count
      * thresholds tau_q^p (1+eps) (+inf until k results), stream-ordered on `stream`.
@@ -137,12 +138,19 @@ typedef struct nn_opts {
      * query_block so that the calls match.  NULL = no exchange. */
     void (*exchange)(float *thr, int64_t count, void *user);
     void *exchange_user;
+    /* Optional database index (the query-independent part of the cascade, built once for
+     * a database that is searched many times -- the paper's setting): DEVICE
+     * [2][N][n], the envelope U(x) block then L(x) block of every database row with THIS
+     * call's w, exactly as lb_envelope(db, n, w, U, L, N) writes it.  NULL = computed
+     * inside the call.  A wrong index gives wrong bounds (not checked). */
+    const float *db_env;
     int32_t reserved[2];
 } nn_opts;
 
 #define DTWLB_KEOGH_ONLY 1
 #define DTWLB_NO_PREFILTER 2
 #define DTWLB_NO_CASCADE 4   /* DTW abandons on the row minimum alone (no LB_Keogh suffix) */
+#define DTWLB_NO_STREAM 8    /* Q <= 8: use the tiled bound pass instead of the streaming one */
 
 /* Counters of one nn_search call (host struct, filled on return). */
 typedef struct nn_stats {
@@ -175,7 +183,9 @@ typedef struct nn_stats {
  * LB_Keogh -> LB_Improved on survivors -> banded DTW on what remains, each gate
  * pruning only when the bound exceeds the current k-th best times (1+eps).
  * Without the pre-filter (DTWLB_NO_PREFILTER) LB_Keogh runs over the whole
- * database, as Alg. 3 is printed.
+ * database, as Alg. 3 is printed.  With few queries (Q <= 8, n % 4 == 0) the bound
+ * pass is memory-bound: LB_Keogh then runs as ONE streaming pass over the database
+ * for all Q queries (no pre-filter; DTWLB_NO_STREAM disables this mode).
  *   queries: [Q][n] float32, db: [N][n] float32 -- device OR host pointers
  *            (host buffers are staged to the device inside the call);
  *   out_idx: [Q][k] int64 (index_base + row), out_dist: [Q][k] float32 rooted

@@ -19,6 +19,7 @@ STATUS = {0: "OK", 1: "EINVAL", 2: "EUNSUPPORTED", 3: "ENOMEM", 4: "ECUDA", 5: "
 KEOGH_ONLY = 1
 NO_PREFILTER = 2
 NO_CASCADE = 4
+NO_STREAM = 8
 MAX_K = 1024
 
 
@@ -35,7 +36,7 @@ EXCHANGE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int64, ctypes.c_v
 class NnOpts(ctypes.Structure):
     _fields_ = [("eps", ctypes.c_float), ("index_base", ctypes.c_int64), ("query_block", ctypes.c_int32),
                 ("flags", ctypes.c_int32), ("exchange", EXCHANGE_FN), ("exchange_user", ctypes.c_void_p),
-                ("reserved", ctypes.c_int32 * 2)]
+                ("db_env", ctypes.c_void_p), ("reserved", ctypes.c_int32 * 2)]
 
 
 class _DeviceArray:
@@ -188,20 +189,23 @@ def dtw_band(x: torch.Tensor, y: torch.Tensor, w: int, p: int) -> torch.Tensor:
     return out
 
 
-def _opts(eps, index_base, query_block, keogh_only, prefilter=True, cascade=True, exchange=None):
+def _opts(eps, index_base, query_block, keogh_only, prefilter=True, cascade=True, exchange=None, stream=True,
+          db_env=None):
     o = NnOpts()
     if exchange is not None:
         o.exchange = exchange
     o.eps = eps
     o.index_base = index_base
     o.query_block = query_block
-    o.flags = (KEOGH_ONLY if keogh_only else 0) | (0 if prefilter else NO_PREFILTER) | (0 if cascade else NO_CASCADE)
+    o.flags = (KEOGH_ONLY if keogh_only else 0) | (0 if prefilter else NO_PREFILTER) | \
+        (0 if cascade else NO_CASCADE) | (0 if stream else NO_STREAM)
+    o.db_env = db_env.data_ptr() if db_env is not None else None
     return o
 
 
 def nn_search(queries, db, w: int, p: int, k: int, *, eps: float = 1e-3, index_base: int = 0,
               query_block: int = 0, keogh_only: bool = False, prefilter: bool = True, cascade: bool = True,
-              exchange=None, out=None,
+              stream: bool = True, db_env=None, exchange=None, out=None,
               return_stats: bool = False):
     """Exact k-NN under banded DTW_p.  Returns (idx int64 [Q][k], dist float32 [Q][k]).
 
@@ -210,7 +214,10 @@ def nn_search(queries, db, w: int, p: int, k: int, *, eps: float = 1e-3, index_b
     ``out`` optionally supplies (idx, dist) output tensors.  ``exchange(thr)`` (sharded
     search) is called once per query block after the first range with a float32 CUDA view
     of the block's thresholds, which it may lower in place (e.g. all-reduce MIN across
-    shards; every rank must then pass the same ``query_block``).
+    shards; every rank must then pass the same ``query_block``).  ``stream=False`` disables the
+    few-query streaming bound pass (DTWLB_NO_STREAM).  ``db_env`` optionally supplies the
+    database index: a [2][N][n] CUDA tensor holding lb_envelope(db, w) (U block, then L block),
+    reused instead of being computed in the call.
     """
     host = not (isinstance(queries, torch.Tensor) and queries.is_cuda)
     if host:
@@ -229,7 +236,11 @@ def nn_search(queries, db, w: int, p: int, k: int, *, eps: float = 1e-3, index_b
     else:
         idx, dist = out
     cb = _exchange_callback(exchange) if exchange is not None else None  # kept alive for the call
-    o = _opts(eps, index_base, query_block, keogh_only, prefilter, cascade, cb)
+    if db_env is not None:
+        db_env = _dev(db_env, "db_env")
+        if tuple(db_env.shape) != (2, N, n):
+            raise ValueError(f"db_env must be [2][N][n] = [2][{N}][{n}], got {tuple(db_env.shape)}")
+    o = _opts(eps, index_base, query_block, keogh_only, prefilter, cascade, cb, stream, db_env)
     st = NnStats()
     _check(load().nn_search(queries.data_ptr(), Q, db.data_ptr(), N, n, w, p, k, idx.data_ptr(),
                             dist.data_ptr(), ctypes.byref(o), ctypes.byref(st) if return_stats else None,

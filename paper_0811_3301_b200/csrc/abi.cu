@@ -110,6 +110,8 @@ int lb_keogh(const float *q_env, const float *db, int64_t Q, int64_t N, int32_t 
     if (Q == 0 || N == 0) return DTWLB_OK;
     CHECK_ARG(q_env && db && out, "lb_keogh: NULL pointer");
     DTWLB_TRY(require_device());
+    if (keogh_stream_ok(Q, n, db))  // few queries: one streaming pass over the database (stream.cu)
+        return launch_keogh_stream(q_env, q_env + Q * n, db, Q, N, n, p, true, out, N, as_stream(stream));
     return launch_keogh(q_env, q_env + Q * n, db, Q, N, n, p, true, out, N, as_stream(stream));
 }
 

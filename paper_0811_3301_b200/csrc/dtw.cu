@@ -44,6 +44,15 @@ __device__ __forceinline__ float b1_at(const DtwArgs &a, int64_t idx) {
     return a.b1 ? __ldg(a.b1 + idx) : __half2float(a.b1h[idx]);
 }
 
+// In-band cells of rows 0 .. r-1 of the n x n table: sum_i (min(n-1, i+w) - max(0, i-w) + 1)
+// = r(2w+1) - (left clip) - (right clip); band_cells(n, n, w) = n(2w+1) - w(w+1).  (w <= n-1)
+__device__ __forceinline__ unsigned long long band_cells(int r, int n, int w) {
+    const long long m = r < w ? r : w;                        // rows i < w lose w - i cells
+    const long long a = n - w;                                 // rows i >= n - w lose i + w - n + 1
+    const long long t = r > a ? r - a : 0;
+    return (unsigned long long)((long long)r * (2 * w + 1) - (m * w - m * (m - 1) / 2) - t * (t + 1) / 2);
+}
+
 template <int P>
 __device__ __forceinline__ float col_lb(float y, float ux, float lx, float lu, float ul) {
     // LB_Improved column term d(y_j, [L(H)_j, U(H)_j])^p by the closed form (improved.cu)
@@ -315,7 +324,8 @@ dtw4_kernel(DtwArgs a) {
     const bool casc2 = casc && a.col_c0 > 0 && a.b1h != nullptr;
     float rest = 0.f, rest_n = 0.f;
     const float *ur = nullptr, *lr = nullptr;
-    unsigned rows_done = 0, n_abandon = 0, n_started = 0;  // per-lane counters
+    unsigned long long cells_done = 0;  // in-band cells of this lane's finished / abandoned pairs
+    unsigned n_abandon = 0, n_started = 0;  // per-lane counters
 
     while (true) {
         // ---- (a) activate the lanes whose refill copies were issued one step ago ----
@@ -543,7 +553,6 @@ dtw4_kernel(DtwArgs a) {
                     }
                 }
             }
-            rows_done += (unsigned)(i - i0);
             cp_wait<0>();
             {
                 const float4 x0 = *reinterpret_cast<const float4 *>(slot + XA);
@@ -570,6 +579,7 @@ dtw4_kernel(DtwArgs a) {
             }
             // ---- (d) finished or abandoned lanes become free ----
             if (i >= n) {
+                cells_done += band_cells(n, n, w);
                 float r = B[WB];
                 if constexpr (!EXACT) {
 #pragma unroll
@@ -582,6 +592,7 @@ dtw4_kernel(DtwArgs a) {
             } else {
                 if (band_min<WB>(B) + rest > thr) {
                     if constexpr (!WALK) a.res[item] = kInf;
+                    cells_done += band_cells(i, n, w);
                     ++n_abandon;  // early abandon (readings c15, c19, c21)
                     st = kFree;
                 }
@@ -594,7 +605,7 @@ dtw4_kernel(DtwArgs a) {
         }
     }
     if (a.cells) {
-        unsigned long long cells = (unsigned long long)rows_done * (unsigned long long)(2 * w + 1);
+        unsigned long long cells = cells_done;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) cells += __shfl_xor_sync(0xffffffffu, cells, o);
         if (lane == 0) atomicAdd(a.cells, cells);
@@ -655,12 +666,12 @@ __global__ void dtw_generic_kernel(DtwArgs a, const float *__restrict__ yraw, fl
         }
         if (rmin > thr) {
             if constexpr (!WALK) a.res[item] = kInf;
-            if (a.cells) atomicAdd(a.cells, (unsigned long long)(i + 1) * (unsigned long long)nb);
+            if (a.cells) atomicAdd(a.cells, band_cells(i + 1, n, w));
             if (a.abandoned) atomicAdd(a.abandoned, 1ull);
             return;
         }
     }
-    if (a.cells) atomicAdd(a.cells, (unsigned long long)n * (unsigned long long)nb);
+    if (a.cells) atomicAdd(a.cells, band_cells(n, n, w));
     if constexpr (WALK) {
         if (B[w] <= thr) {
             const unsigned pos = atomicAdd(a.rcount, 1u);

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
 
 #include <cuda_fp16.h>
 
@@ -40,6 +41,14 @@ int launch_paa_bound(const float *Uhi, const float *Llo, const float *Xlo, const
 // envelope sums [N][Dp] (launch_paa_env_sums of U(x), L(x)).  Same out types as above.
 int launch_paa_bound_rev(const float *Ylo, const float *Yhi, const float *Uxhi, const float *Lxlo, int64_t Q,
                          int64_t N, int n, int p, bool rooted, void *out, int64_t ldo, cudaStream_t st);
+
+// LB_Keogh^p of Q <= kStreamMaxQ queries against every database row in ONE streaming pass
+// (stream.cu; TMA bulk copies, thread per candidate): out[q*ldo + c] = beta1 (rooted if `rooted`).
+// Requires n % 4 == 0 and a 16-byte aligned db (keogh_stream_ok).
+constexpr int kStreamMaxQ = 8;
+bool keogh_stream_ok(int64_t Q, int n, const void *db);
+int launch_keogh_stream(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n, int p,
+                        bool rooted, float *out, int64_t ldo, cudaStream_t st);
 
 // Arguments of the survivor passes (improved.cu).  Padded per-query arrays:
 //   yq, LUq, ULq: [Q][npadE] (npadE = 32 * epl), zero padded;

@@ -482,8 +482,9 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     const float eps = opts ? opts->eps : 1e-3f;
     const int64_t index_base = opts ? opts->index_base : 0;
     const bool keogh_only = opts && (opts->flags & DTWLB_KEOGH_ONLY);
-    // piecewise-sum pre-filter as the dense gate pass, LB_Keogh on its survivors
-    const bool prefilter = !(opts && (opts->flags & DTWLB_NO_PREFILTER));
+    // piecewise-sum pre-filter as the dense gate pass, LB_Keogh on its survivors;
+    // not with few queries (stream mode below: the LB_Keogh pass is then memory-bound)
+    bool prefilter = !(opts && (opts->flags & DTWLB_NO_PREFILTER));
     // DTW early abandon on rowmin + LB_Keogh terms of the remaining rows (reading c19)
     const bool cascade = !(opts && (opts->flags & DTWLB_NO_CASCADE));
     w = std::min(w, n - 1);
@@ -505,6 +506,10 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         DTWLB_CUDA(cudaMemcpyAsync(d, db_in, sizeof(float) * N * n, cudaMemcpyHostToDevice, st));
         db = d;
     }
+    // stream mode (Q <= kStreamMaxQ): LB_Keogh of all Q queries in one streaming pass over the
+    // database (stream.cu), no pre-filter
+    const bool stream_mode = !(opts && (opts->flags & DTWLB_NO_STREAM)) && keogh_stream_ok(Q, n, db);
+    if (stream_mode) prefilter = false;
     const bool out_dev = is_device_ptr(out_idx_in) && is_device_ptr(out_dist_in);
     int64_t *out_idx = out_idx_in;
     float *out_dist = out_dist_in;
@@ -559,9 +564,14 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         DTWLB_TRY(wsget(S_YSH, (size_t)4 * Q * LP, &ysh));
         DTWLB_TRY(launch_build_ysh(queries, Q, n, ysh, LP, st));
     }
-    float *dbenv;  // U(x), L(x): [2][N][n]
-    DTWLB_TRY(wsget(S_DBENV, (size_t)2 * N * n, &dbenv));
-    if (!keogh_only || prefilter) DTWLB_TRY(launch_envelope(db, n, w, dbenv, dbenv + (size_t)N * n, N, st));
+    // U(x), L(x): [2][N][n] -- the caller's database index (nn_opts.db_env) or computed here
+    const float *dbenv = opts ? opts->db_env : nullptr;
+    if (!dbenv && (!keogh_only || prefilter)) {
+        float *e;
+        DTWLB_TRY(wsget(S_DBENV, (size_t)2 * N * n, &e));
+        DTWLB_TRY(launch_envelope(db, n, w, e, e + (size_t)N * n, N, st));
+        dbenv = e;
+    }
     // symmetric gate (reading c20): reverse piecewise sums P(U(x)) up, P(L(x)) down [2][N][Dp]
     // and P(y) down / up [2][Q][Dp]
     float *rpaa = nullptr;
@@ -682,7 +692,9 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
             const float *yp = rpaa + (size_t)2 * N * Dp;
             DTWLB_TRY(launch_paa_bound_rev(yp + qb0 * Dp, yp + (size_t)Q * Dp + qb0 * Dp, rpaa,
                                            rpaa + (size_t)N * Dp, qn, N, n, p, false, beta1, ldb, st));
-        } else
+        } else if (stream_mode)
+            DTWLB_TRY(launch_keogh_stream(U + qb0 * n, L + qb0 * n, db, qn, N, n, p, false, beta1, ldb, st));
+        else
             DTWLB_TRY(launch_keogh(U + qb0 * n, L + qb0 * n, db, qn, N, n, p, false, beta1, ldb, st));
         if (stats) ev1 = rec();
         init_state_kernel<<<(unsigned)ceil_div(qn, 256), 256, 0, st>>>(s, (int)qn, k);
@@ -718,7 +730,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                     ia.n_eval_keogh = s.stat + 4;
                 }
                 ia.Ux = dbenv;
-                ia.Lx = dbenv + (size_t)N * n;
+                ia.Lx = dbenv ? dbenv + (size_t)N * n : nullptr;
                 ia.gate = beta1;
                 ia.ldb = ldb;
                 ia.Qb = qn;

@@ -1,0 +1,258 @@
+// stream.cu -- the LB_Keogh pass (a2) for a FEW queries: one streaming pass over the
+// database (SURVEY 8(d) "C5-stream": Q <= 8, the regime where the bound pass is
+// HBM-bound).  P:453-464, Alg. 2/3 lines P:507-514 / P:589-597:
+//
+//   beta1(q, c) = sum_i d(x_c,i, [L_q,i, U_q,i])^p,  d(v,[a,b]) = max(v - b, a - v, 0)
+//
+// This is the paper's own per-query scan shape -- Alg. 2/3 stream the whole database
+// for one query, (2N+3)n comparisons -- with up to QB = 8
+// queries sharing one read of the database.
+//
+// B200 design: thread = candidate.  A persistent CTA of 256 threads walks tiles of 256
+// database rows; each row is copied chunk by chunk (KCH floats) from HBM into the
+// thread's own shared-memory slot by a TMA bulk copy (cp.async.bulk, no tensor map:
+// a row chunk is contiguous) that completes on the thread's own mbarrier, D stages
+// deep, so ~D-1 chunks per row (~100 KB per SM) are in flight while the thread
+// computes on the oldest one.  Every thread reads only the slot it filled itself, so
+// there is no CTA-wide synchronisation in the loop.  The QB query envelopes sit in
+// shared memory and are read as 128-bit broadcasts (every lane the same address);
+// per pair-element the minimal FADD2 (two subtractions of two elements), FMNMX3,
+// FFMA|FADD (3 issue slots per element, the x value reused by all QB queries).
+// Per-chunk partial sums are folded into the total at each chunk end (two-level
+// summation, as the tile kernel).  Output beta1 (p-th power, fp32) [Q][ldo].
+// A cp.async (LDGSTS) variant of the same loop (COPY = 1: each warp copies its 32 rows
+// cooperatively, 128-byte coalesced segments) is kept for comparison.
+#include "kernels.cuh"
+
+namespace dtwlb {
+
+namespace {
+
+constexpr int kStreamNT = 256;  // threads (= candidate rows) per CTA
+constexpr int kKch = 32;        // floats per row chunk (128-byte copies)
+constexpr int kSlot = kKch + 4; // padded slot pitch (floats): conflict-free 128-bit reads
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// TMA bulk copy global -> shared (1D, bytes % 16 == 0, both addresses 16-byte aligned)
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+// order this thread's earlier generic-proxy reads of its slot before the next async write
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+template <int P>
+__device__ __forceinline__ float lb4(float acc, const float4 &x, const float4 &u, const float4 &l) {
+    // d = max(x - U, L - x, 0) on two elements at a time (packed f32x2 subtractions)
+    const float2 a0 = __fadd2_rn(make_float2(x.x, x.y), make_float2(-u.x, -u.y));
+    const float2 b0 = __fadd2_rn(make_float2(l.x, l.y), make_float2(-x.x, -x.y));
+    const float2 a1 = __fadd2_rn(make_float2(x.z, x.w), make_float2(-u.z, -u.w));
+    const float2 b1 = __fadd2_rn(make_float2(l.z, l.w), make_float2(-x.z, -x.w));
+    acc = accp<P>(acc, max3f(a0.x, b0.x, 0.f));
+    acc = accp<P>(acc, max3f(a0.y, b0.y, 0.f));
+    acc = accp<P>(acc, max3f(a1.x, b1.x, 0.f));
+    acc = accp<P>(acc, max3f(a1.y, b1.y, 0.f));
+    return acc;
+}
+
+// COPY: 0 = TMA bulk copies (per thread, own mbarrier), 1 = cp.async per warp.
+template <int P, int QB, int COPY>
+__global__ void __launch_bounds__(kStreamNT, 1)
+keogh_stream_kernel(const float *__restrict__ U, const float *__restrict__ L, const float *__restrict__ db,
+                    int64_t N, int n, int Q, int D, bool rooted, float *__restrict__ out, int64_t ldo) {
+    extern __shared__ __align__(128) unsigned char smraw[];
+    const int npad = (n + kKch - 1) / kKch * kKch;
+    const int nch = npad / kKch;
+    float *sU = reinterpret_cast<float *>(smraw);       // [QB][npad]
+    float *sL = sU + (size_t)QB * npad;                 // [QB][npad]
+    float *slots = sL + (size_t)QB * npad;              // [D][NT][kSlot]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(slots + (size_t)D * kStreamNT * kSlot);  // [D][NT]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    // query envelopes; pad columns (i >= n) and missing queries: U = +inf, L = -inf (d = 0)
+    for (int t = tid; t < QB * npad; t += kStreamNT) {
+        const int q = t / npad, i = t - q * npad;
+        const bool ok = q < Q && i < n;
+        sU[t] = ok ? U[(int64_t)q * n + i] : kInf;
+        sL[t] = ok ? L[(int64_t)q * n + i] : -kInf;
+    }
+    for (int t = tid; t < D * kStreamNT * kSlot; t += kStreamNT) slots[t] = 0.f;
+    if constexpr (COPY == 0) {
+        for (int s = 0; s < D; ++s) mbar_init(bars + s * kStreamNT + tid, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    const int64_t ntiles = (N + kStreamNT - 1) / kStreamNT;
+    const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t steps = my_tiles * nch;  // (tile, chunk) steps of this CTA, same for every thread
+
+    // issue the copy of step g into stage g % D
+    auto issue = [&](int64_t g) {
+        const int64_t ti = g / nch;
+        const int ch = (int)(g - ti * nch);
+        const int64_t tile = blockIdx.x + ti * gridDim.x;
+        const int s = (int)(g % D);
+        const int k0 = ch * kKch;
+        const int len = min(kKch, n - k0);  // floats (n % 4 == 0: a multiple of 4)
+        if constexpr (COPY == 0) {
+            const int64_t c = tile * kStreamNT + tid;
+            if (c < N) {
+                float *dst = slots + ((size_t)s * kStreamNT + tid) * kSlot;
+                fence_proxy_async();
+                mbar_expect_tx(bars + s * kStreamNT + tid, (unsigned)len * 4u);
+                bulk_g2s(dst, db + c * (int64_t)n + k0, (unsigned)len * 4u, bars + s * kStreamNT + tid);
+            }
+        } else {
+            // warp copies its 32 rows: each instruction moves 4 rows x 128 bytes (8 lanes per row)
+            const int sub = lane & 7, rr = lane >> 3;
+#pragma unroll
+            for (int r0 = 0; r0 < 32; r0 += 4) {
+                const int row = warp * 32 + r0 + rr;
+                const int64_t c = tile * kStreamNT + row;
+                const bool ok = c < N && 4 * sub < len;
+                float *dst = slots + ((size_t)s * kStreamNT + row) * kSlot + 4 * sub;
+                cp_async16(dst, ok ? db + c * (int64_t)n + k0 + 4 * sub : db, ok ? 16 : 0);
+            }
+            cp_commit();
+        }
+    };
+
+    float acc[QB];
+#pragma unroll
+    for (int q = 0; q < QB; ++q) acc[q] = 0.f;
+    const int64_t pro = steps < D - 1 ? steps : D - 1;
+    for (int64_t g = 0; g < pro; ++g) issue(g);
+    for (int64_t g = 0; g < steps; ++g) {
+        if (g + D - 1 < steps) issue(g + D - 1);
+        else if constexpr (COPY == 1) cp_commit();  // keep the group count uniform
+        const int64_t ti = g / nch;
+        const int ch = (int)(g - ti * nch);
+        const int64_t c = (blockIdx.x + ti * gridDim.x) * kStreamNT + tid;
+        const int s = (int)(g % D);
+        if constexpr (COPY == 0) {
+            if (c < N) mbar_wait(bars + s * kStreamNT + tid, (unsigned)((g / D) & 1));
+        } else {
+            switch (D - 1) {  // (wait_group takes an immediate)
+                case 1: cp_wait<1>(); break;
+                case 2: cp_wait<2>(); break;
+                case 3: cp_wait<3>(); break;
+                case 4: cp_wait<4>(); break;
+                case 5: cp_wait<5>(); break;
+                default: cp_wait<0>(); break;
+            }
+            __syncwarp();
+        }
+        const float *xs = slots + ((size_t)s * kStreamNT + tid) * kSlot;
+        const int k0 = ch * kKch;
+        float part[QB];
+#pragma unroll
+        for (int q = 0; q < QB; ++q) part[q] = 0.f;
+#pragma unroll 2
+        for (int e = 0; e < kKch; e += 4) {
+            const float4 xv = *reinterpret_cast<const float4 *>(xs + e);
+#pragma unroll
+            for (int q = 0; q < QB; ++q) {
+                const float4 u = *reinterpret_cast<const float4 *>(sU + (size_t)q * npad + k0 + e);
+                const float4 l = *reinterpret_cast<const float4 *>(sL + (size_t)q * npad + k0 + e);
+                part[q] = lb4<P>(part[q], xv, u, l);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < QB; ++q) acc[q] += part[q];
+        if (ch == nch - 1) {
+            if (c < N) {
+#pragma unroll
+                for (int q = 0; q < QB; ++q)
+                    if (q < Q) out[(int64_t)q * ldo + c] = rooted ? rootp<P>(acc[q]) : acc[q];
+            }
+#pragma unroll
+            for (int q = 0; q < QB; ++q) acc[q] = 0.f;
+        }
+        if constexpr (COPY == 1) __syncwarp();  // the slot is rewritten by the warp's next copy
+    }
+    if constexpr (COPY == 1) cp_wait<0>();
+}
+
+template <int P, int QB, int COPY>
+int launch_stream_t(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n, bool rooted,
+                    float *out, int64_t ldo, cudaStream_t st) {
+    const int npad = (n + kKch - 1) / kKch * kKch;
+    const size_t env = (size_t)2 * QB * npad * sizeof(float);
+    int dev = 0, smem_max = 0, nsm = 148;
+    DTWLB_CUDA(cudaGetDevice(&dev));
+    DTWLB_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    DTWLB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const size_t per_stage = (size_t)kStreamNT * (kSlot * sizeof(float) + sizeof(uint64_t));
+    static const int env_d = [] { const char *e = getenv("DTWLB_STREAM_STAGES"); return e ? atoi(e) : 0; }();
+    int D = env_d > 1 ? std::min(env_d, 6) : 5;
+    while (D > 2 && env + D * per_stage > (size_t)smem_max) --D;
+    const size_t smem = env + D * per_stage;
+    if (smem > (size_t)smem_max) {
+        set_error(DTWLB_EUNSUPPORTED, "stream LB_Keogh pass: n = %d too long for shared memory", n);
+        return DTWLB_EUNSUPPORTED;
+    }
+    auto k = keogh_stream_kernel<P, QB, COPY>;
+    DTWLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t ntiles = ceil_div(N, kStreamNT);
+    const int grid = (int)std::min<int64_t>(ntiles, nsm);  // persistent: one CTA per SM
+    k<<<grid, kStreamNT, smem, st>>>(U, L, db, N, n, (int)Q, D, rooted, out, ldo);
+    DTWLB_LAUNCH_CHECK();
+    return DTWLB_OK;
+}
+
+template <int P, int COPY>
+int launch_stream_p(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n, bool rooted,
+                    float *out, int64_t ldo, cudaStream_t st) {
+    if (Q <= 1) return launch_stream_t<P, 1, COPY>(U, L, db, Q, N, n, rooted, out, ldo, st);
+    if (Q <= 2) return launch_stream_t<P, 2, COPY>(U, L, db, Q, N, n, rooted, out, ldo, st);
+    if (Q <= 4) return launch_stream_t<P, 4, COPY>(U, L, db, Q, N, n, rooted, out, ldo, st);
+    return launch_stream_t<P, 8, COPY>(U, L, db, Q, N, n, rooted, out, ldo, st);
+}
+
+}  // namespace
+
+bool keogh_stream_ok(int64_t Q, int n, const void *db) {
+    return Q >= 1 && Q <= kStreamMaxQ && n % 4 == 0 && (reinterpret_cast<uintptr_t>(db) % 16) == 0;
+}
+
+int launch_keogh_stream(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n, int p,
+                        bool rooted, float *out, int64_t ldo, cudaStream_t st) {
+    if (Q == 0 || N == 0) return DTWLB_OK;
+    if (!keogh_stream_ok(Q, n, db)) {
+        set_error(DTWLB_EINVAL, "internal: stream LB_Keogh pass needs 1 <= Q <= %d, n %% 4 == 0, aligned rows",
+                  kStreamMaxQ);
+        return DTWLB_EINVAL;
+    }
+    static const int env_copy = [] { const char *e = getenv("DTWLB_STREAM_COPY"); return e ? atoi(e) : 0; }();
+    if (env_copy == 1)
+        return p == 1 ? launch_stream_p<1, 1>(U, L, db, Q, N, n, rooted, out, ldo, st)
+                      : launch_stream_p<2, 1>(U, L, db, Q, N, n, rooted, out, ldo, st);
+    return p == 1 ? launch_stream_p<1, 0>(U, L, db, Q, N, n, rooted, out, ldo, st)
+                  : launch_stream_p<2, 0>(U, L, db, Q, N, n, rooted, out, ldo, st);
+}
+
+}  // namespace dtwlb
