@@ -52,9 +52,43 @@ __device__ __forceinline__ void env_quad(const float *P, int i0, int w, float *m
     mn[3] = fminf(cmn, min3f(d, e, f));
 }
 
-// rows_per_cta rows per CTA; padded row length plen = n + 2w + 4.
+// env_quad with 128-bit shared-memory reads: P 16-byte aligned and i0 % 4 == 0, so the four
+// outputs' common window [i0+3, i0+2w] is read as aligned float4 vectors (a quarter-warp reads
+// 8 consecutive vectors: conflict-free) -- the scalar version's stride-4 reads were 4-way bank
+// conflicted.  Same comparisons, same (exact) result.
+__device__ __forceinline__ void env_quad4(const float *P, int i0, int w, float *mx, float *mn) {
+    const float4 h = *reinterpret_cast<const float4 *>(P + i0);  // P[i0 .. i0+3]
+    float cmx = h.w, cmn = h.w;                                  // P[i0+3]
+    const int te = i0 + 2 * w;                                   // last index of the common window
+    int t = i0 + 4;
+    for (; t + 3 <= te; t += 4) {
+        const float4 v = *reinterpret_cast<const float4 *>(P + t);
+        cmx = max3f(cmx, v.x, v.y);
+        cmx = max3f(cmx, v.z, v.w);
+        cmn = min3f(cmn, v.x, v.y);
+        cmn = min3f(cmn, v.z, v.w);
+    }
+    for (; t <= te; ++t) {
+        const float v = P[t];
+        cmx = fmaxf(cmx, v);
+        cmn = fminf(cmn, v);
+    }
+    const float a = h.x, b = h.y, c = h.z;
+    const float d = P[te + 1], e = P[te + 2], f = P[te + 3];
+    mx[0] = fmaxf(cmx, max3f(a, b, c));
+    mn[0] = fminf(cmn, min3f(a, b, c));
+    mx[1] = fmaxf(cmx, max3f(b, c, d));
+    mn[1] = fminf(cmn, min3f(b, c, d));
+    mx[2] = fmaxf(cmx, max3f(c, d, e));
+    mn[2] = fminf(cmn, min3f(c, d, e));
+    mx[3] = fmaxf(cmx, max3f(d, e, f));
+    mn[3] = fminf(cmn, min3f(d, e, f));
+}
+
+// rows_per_cta rows per CTA; padded row length plen >= n + 2w + 4 (a multiple of 4).
 __global__ void envelope_smem_kernel(const float *__restrict__ x, int n, int w, float *__restrict__ U,
-                                     float *__restrict__ L, int64_t count, int rows_per_cta, int plen) {
+                                     float *__restrict__ L, int64_t count, int rows_per_cta, int plen,
+                                     bool vec_out) {
     extern __shared__ float sm[];
     const int nq = (n + 3) >> 2;  // quads per row
     for (int64_t r0 = (int64_t)blockIdx.x * rows_per_cta; r0 < count;
@@ -70,11 +104,17 @@ __global__ void envelope_smem_kernel(const float *__restrict__ x, int n, int w, 
         for (int t = threadIdx.x; t < rows * nq; t += blockDim.x) {
             int r = t / nq, i0 = (t - r * nq) * 4;
             float mx[4], mn[4];
-            env_quad(sm + r * plen, i0, w, mx, mn);
             float *u = U + (r0 + r) * (int64_t)n, *l = L + (r0 + r) * (int64_t)n;
+            if (w >= 2 && (plen & 3) == 0) env_quad4(sm + r * plen, i0, w, mx, mn);
+            else env_quad(sm + r * plen, i0, w, mx, mn);
+            if ((n & 3) == 0 && vec_out) {  // 16-byte stores: a warp writes 512 contiguous bytes
+                *reinterpret_cast<float4 *>(u + i0) = make_float4(mx[0], mx[1], mx[2], mx[3]);
+                *reinterpret_cast<float4 *>(l + i0) = make_float4(mn[0], mn[1], mn[2], mn[3]);
+            } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (i0 + k < n) { u[i0 + k] = mx[k]; l[i0 + k] = mn[k]; }
+                for (int k = 0; k < 4; ++k)
+                    if (i0 + k < n) { u[i0 + k] = mx[k]; l[i0 + k] = mn[k]; }
+            }
         }
         __syncthreads();
     }
@@ -100,7 +140,7 @@ __global__ void envelope_global_kernel(const float *__restrict__ x, int n, int w
 int launch_envelope(const float *x, int n, int w, float *U, float *L, int64_t count, cudaStream_t st) {
     if (count == 0) return DTWLB_OK;
     w = w > n - 1 ? n - 1 : w;
-    const int plen = n + 2 * w + 4;
+    const int plen = (n + 2 * w + 4 + 3) & ~3;  // (a multiple of 4: 16-byte aligned rows)
     const size_t row_bytes = (size_t)plen * sizeof(float);
     const size_t max_smem = 160 * 1024;
     if (row_bytes <= max_smem) {
@@ -112,7 +152,8 @@ int launch_envelope(const float *x, int n, int w, float *U, float *L, int64_t co
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int64_t ctas = ceil_div(count, rows);
         int grid = (int)std::min<int64_t>(ctas, 148 * 64);
-        envelope_smem_kernel<<<grid, 256, smem, st>>>(x, n, w, U, L, count, rows, plen);
+        const bool vec_out = ((reinterpret_cast<uintptr_t>(U) | reinterpret_cast<uintptr_t>(L)) & 15) == 0;
+        envelope_smem_kernel<<<grid, 256, smem, st>>>(x, n, w, U, L, count, rows, plen, vec_out);
     } else {
         int64_t total = count * (int64_t)n;
         int grid = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 32);

@@ -383,9 +383,8 @@ __global__ void __launch_bounds__(1024) plan_kernel(QState s, int Qb, const unsi
             }
             s.pos[q] = pos;
             if (pos < len) {
-                int d = d0 << min(s.rnd[q], 11);
-                d = min(d, kDMax);
-                cnt = min(d, len - pos);
+                const long long d = min((long long)d0 << min(s.rnd[q], 11), (long long)kDMax);
+                cnt = (int)min(d, (long long)(len - pos));
             } else {
                 s.active[q] = 0;
             }
@@ -785,7 +784,12 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 for (int b = 0; b < batch && walking; ++b) {
                     ++walk_rounds;
                     static const int env_d0 = [] { const char *e = getenv("DTWLB_D0"); return e ? atoi(e) : 0; }();
-                    plan_kernel<<<1, 1024, 0, st>>>(s, (int)qn, list, cap, sorted, env_d0 > 0 ? env_d0 : kD0);
+                    // first batch per query: kD0 = 128 when many queries fill the GPU; with few
+                    // queries a round is latency-bound (one pair's DTW is a ~n-step chain), so the
+                    // batches start larger (2^15 / Qb items: fewer, fuller rounds)
+                    const int d0 = env_d0 > 0 ? env_d0
+                                              : (int)std::min<int64_t>(kDMax, std::max<int64_t>(kD0, (1 << 15) / qn));
+                    plan_kernel<<<1, 1024, 0, st>>>(s, (int)qn, list, cap, sorted, d0);
                     DTWLB_LAUNCH_CHECK();
                     int tot2[2] = {0, 0};
                     if (!dev_rounds) {

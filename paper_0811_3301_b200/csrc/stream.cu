@@ -22,6 +22,8 @@
 // summation, as the tile kernel).  Output beta1 (p-th power, fp32) [Q][ldo].
 // A cp.async (LDGSTS) variant of the same loop (COPY = 1: each warp copies its 32 rows
 // cooperatively, 128-byte coalesced segments) is kept for comparison.
+#include <cudaTypedefs.h>  // CUtensorMap, PFN_cuTensorMapEncodeTiled (driver entry point, no -lcuda)
+
 #include "kernels.cuh"
 
 namespace dtwlb {
@@ -197,6 +199,176 @@ keogh_stream_kernel(const float *__restrict__ U, const float *__restrict__ L, co
     if constexpr (COPY == 1) cp_wait<0>();
 }
 
+// ---------------------------------------------------------------------------------------
+// COPY = 2 (default): 2D TMA.  The database is a [N][n] fp32 tensor map; a warp owns tiles of
+// 32 rows and streams them through its own ring of D boxes of 32 rows x 64 floats (8 KB, one
+// cp.async.bulk.tensor per box issued by lane 0, completing on the warp's mbarrier of that
+// stage; out-of-range rows / columns are zero-filled by the TMA unit).  Lane t owns row t of
+// the box and visits its 64 columns in a lane-rotated order (column e + 4 (t & 7)), so the
+// 128-bit shared-memory reads of a quarter-warp hit 8 distinct bank groups for the row data
+// and 8 consecutive float4 of the query envelopes -- no bank conflicts without padding.
+constexpr int kBoxRows = 32, kBoxCols = 64, kTmaWarps = 8;
+
+template <int P, int QB>
+__global__ void __launch_bounds__(kTmaWarps * 32, 1)
+keogh_stream_tma_kernel(const __grid_constant__ CUtensorMap tmap, const float *__restrict__ U,
+                        const float *__restrict__ L, int64_t N, int n, int Q, int D, bool rooted,
+                        float *__restrict__ out, int64_t ldo) {
+    extern __shared__ __align__(1024) unsigned char smraw[];
+    const int npad = (n + kBoxCols - 1) / kBoxCols * kBoxCols;
+    const int nch = npad / kBoxCols;
+    constexpr int BOX = kBoxRows * kBoxCols;  // floats
+    float *boxes = reinterpret_cast<float *>(smraw);                // [warps][D][32][64]
+    float *sU = boxes + (size_t)kTmaWarps * D * BOX;                // [QB][npad]
+    float *sL = sU + (size_t)QB * npad;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sL + (size_t)QB * npad);  // [warps][D]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int t = tid; t < QB * npad; t += kTmaWarps * 32) {
+        const int q = t / npad, i = t - q * npad;
+        const bool ok = q < Q && i < n;
+        sU[t] = ok ? U[(int64_t)q * n + i] : kInf;
+        sL[t] = ok ? L[(int64_t)q * n + i] : -kInf;
+    }
+    if (lane == 0) {
+        for (int s = 0; s < D; ++s) mbar_init(bars + warp * D + s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    const int64_t ntiles = (N + kBoxRows - 1) / kBoxRows;
+    const int64_t gw = (int64_t)blockIdx.x * kTmaWarps + warp, GW = (int64_t)gridDim.x * kTmaWarps;
+    const int64_t my_tiles = gw < ntiles ? (ntiles - 1 - gw) / GW + 1 : 0;
+    const int64_t steps = my_tiles * nch;
+    float *mybox = boxes + (size_t)warp * D * BOX;
+    uint64_t *mybar = bars + warp * D;
+    auto issue = [&](int64_t g) {
+        if (lane == 0) {
+            const int64_t ti = g / nch;
+            const int ch = (int)(g - ti * nch);
+            const int64_t tile = gw + ti * GW;
+            const int s = (int)(g % D);
+            fence_proxy_async();
+            mbar_expect_tx(mybar + s, (unsigned)(BOX * sizeof(float)));
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                "[%4];\n" ::"r"(smem_u32(mybox + (size_t)s * BOX)),
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(ch * kBoxCols), "r"((int)(tile * kBoxRows)),
+                "r"(smem_u32(mybar + s))
+                : "memory");
+        }
+    };
+    const int pro = (int)(steps < D - 1 ? steps : D - 1);
+    for (int g = 0; g < pro; ++g) issue(g);
+    const int rot = 4 * (lane & 7);
+    float acc[QB];
+#pragma unroll
+    for (int q = 0; q < QB; ++q) acc[q] = 0.f;
+    for (int64_t g = 0; g < steps; ++g) {
+        if (g + D - 1 < steps) issue(g + D - 1);
+        const int64_t ti = g / nch;
+        const int ch = (int)(g - ti * nch);
+        const int s = (int)(g % D);
+        mbar_wait(mybar + s, (unsigned)((g / D) & 1));
+        const float *xr = mybox + (size_t)s * BOX + lane * kBoxCols;
+        const float *ub = sU + ch * kBoxCols, *lb = sL + ch * kBoxCols;
+        float part[QB];
+#pragma unroll
+        for (int q = 0; q < QB; ++q) part[q] = 0.f;
+#pragma unroll 4
+        for (int e = 0; e < kBoxCols; e += 4) {
+            const int col = (e + rot) & (kBoxCols - 1);
+            const float4 xv = *reinterpret_cast<const float4 *>(xr + col);
+#pragma unroll
+            for (int q = 0; q < QB; ++q) {
+                const float4 u = *reinterpret_cast<const float4 *>(ub + (size_t)q * npad + col);
+                const float4 l = *reinterpret_cast<const float4 *>(lb + (size_t)q * npad + col);
+                part[q] = lb4<P>(part[q], xv, u, l);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < QB; ++q) acc[q] += part[q];
+        if (ch == nch - 1) {
+            const int64_t c = (gw + ti * GW) * kBoxRows + lane;
+            if (c < N) {
+#pragma unroll
+                for (int q = 0; q < QB; ++q)
+                    if (q < Q) out[(int64_t)q * ldo + c] = rooted ? rootp<P>(acc[q]) : acc[q];
+            }
+#pragma unroll
+            for (int q = 0; q < QB; ++q) acc[q] = 0.f;
+        }
+        __syncwarp();  // every lane is done with box s before lane 0 refills it
+    }
+}
+
+using EncodeTiledFn = PFN_cuTensorMapEncodeTiled_v12000;
+EncodeTiledFn get_encode_tiled() {
+    static EncodeTiledFn fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+        }
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+template <int P, int QB>
+int launch_stream_tma_t(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n, bool rooted,
+                        float *out, int64_t ldo, cudaStream_t st) {
+    EncodeTiledFn enc = get_encode_tiled();
+    if (!enc) {
+        set_error(DTWLB_ECUDA, "stream LB_Keogh pass: cuTensorMapEncodeTiled unavailable");
+        return DTWLB_ECUDA;
+    }
+    CUtensorMap tmap;
+    const cuuint64_t gdim[2] = {(cuuint64_t)n, (cuuint64_t)N};
+    const cuuint64_t gstride[1] = {(cuuint64_t)n * sizeof(float)};
+    const cuuint32_t box[2] = {kBoxCols, kBoxRows};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(db), gdim, gstride, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error(DTWLB_ECUDA, "stream LB_Keogh pass: cuTensorMapEncodeTiled failed (%d)", (int)r);
+        return DTWLB_ECUDA;
+    }
+    const int npad = (n + kBoxCols - 1) / kBoxCols * kBoxCols;
+    const size_t env = (size_t)2 * QB * npad * sizeof(float);
+    int dev = 0, smem_max = 0, nsm = 148;
+    DTWLB_CUDA(cudaGetDevice(&dev));
+    DTWLB_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    DTWLB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const size_t per_stage = (size_t)kTmaWarps * (kBoxRows * kBoxCols * sizeof(float) + sizeof(uint64_t));
+    static const int env_d = [] { const char *e = getenv("DTWLB_STREAM_STAGES"); return e ? atoi(e) : 0; }();
+    int D = env_d > 1 ? std::min(env_d, 8) : 4;
+    while (D > 2 && env + D * per_stage + 1024 > (size_t)smem_max) --D;
+    const size_t smem = env + D * per_stage + 1024;
+    if (smem > (size_t)smem_max) {
+        set_error(DTWLB_EUNSUPPORTED, "stream LB_Keogh pass: n = %d too long for shared memory", n);
+        return DTWLB_EUNSUPPORTED;
+    }
+    auto k = keogh_stream_tma_kernel<P, QB>;
+    DTWLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t ntiles = ceil_div(N, kBoxRows);
+    const int grid = (int)std::min<int64_t>(ceil_div(ntiles, kTmaWarps), nsm);  // persistent
+    k<<<grid, kTmaWarps * 32, smem, st>>>(tmap, U, L, N, n, (int)Q, D, rooted, out, ldo);
+    DTWLB_LAUNCH_CHECK();
+    return DTWLB_OK;
+}
+
+template <int P>
+int launch_stream_tma_p(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n, bool rooted,
+                        float *out, int64_t ldo, cudaStream_t st) {
+    if (Q <= 1) return launch_stream_tma_t<P, 1>(U, L, db, Q, N, n, rooted, out, ldo, st);
+    if (Q <= 2) return launch_stream_tma_t<P, 2>(U, L, db, Q, N, n, rooted, out, ldo, st);
+    if (Q <= 4) return launch_stream_tma_t<P, 4>(U, L, db, Q, N, n, rooted, out, ldo, st);
+    return launch_stream_tma_t<P, 8>(U, L, db, Q, N, n, rooted, out, ldo, st);
+}
+
 template <int P, int QB, int COPY>
 int launch_stream_t(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n, bool rooted,
                     float *out, int64_t ldo, cudaStream_t st) {
@@ -247,8 +419,12 @@ int launch_keogh_stream(const float *U, const float *L, const float *db, int64_t
                   kStreamMaxQ);
         return DTWLB_EINVAL;
     }
-    static const int env_copy = [] { const char *e = getenv("DTWLB_STREAM_COPY"); return e ? atoi(e) : 0; }();
-    if (env_copy == 1)
+    // copy engine: 2 = 2D TMA boxes (default; n >= 64), 0 = per-row TMA bulk copies, 1 = cp.async
+    static const int env_copy = [] { const char *e = getenv("DTWLB_STREAM_COPY"); return e ? atoi(e) : 2; }();
+    if (env_copy == 2 && n >= kBoxCols)
+        return p == 1 ? launch_stream_tma_p<1>(U, L, db, Q, N, n, rooted, out, ldo, st)
+                      : launch_stream_tma_p<2>(U, L, db, Q, N, n, rooted, out, ldo, st);
+    if (env_copy != 0)
         return p == 1 ? launch_stream_p<1, 1>(U, L, db, Q, N, n, rooted, out, ldo, st)
                       : launch_stream_p<2, 1>(U, L, db, Q, N, n, rooted, out, ldo, st);
     return p == 1 ? launch_stream_p<1, 0>(U, L, db, Q, N, n, rooted, out, ldo, st)
