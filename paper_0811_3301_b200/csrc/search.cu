@@ -365,7 +365,7 @@ __device__ __forceinline__ int2 block_scan2(int2 v, int2 *warp_sums, int2 &total
 // into the top-k and tau directly): the walk advances past them and skips the rest of
 // a sorted run once its next bound exceeds tau (1+eps).
 __global__ void __launch_bounds__(1024) plan_kernel(QState s, int Qb, const unsigned long long *__restrict__ list,
-                                                    int64_t cap, bool sorted, int d0) {
+                                                    int64_t cap, bool sorted, int d0, int gs) {
     __shared__ int2 warp_sums[32];
     int2 carry = make_int2(0, 0);
     for (int base = 0; base < Qb; base += blockDim.x) {
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(QState s, int Qb, const unsi
             }
             s.pos[q] = pos;
             if (pos < len) {
-                const long long d = min((long long)d0 << min(s.rnd[q], 11), (long long)kDMax);
+                const long long d = min((long long)d0 << min(s.rnd[q] * gs, 11), (long long)kDMax);
                 cnt = (int)min(d, (long long)(len - pos));
             } else {
                 s.active[q] = 0;
@@ -784,12 +784,14 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 for (int b = 0; b < batch && walking; ++b) {
                     ++walk_rounds;
                     static const int env_d0 = [] { const char *e = getenv("DTWLB_D0"); return e ? atoi(e) : 0; }();
-                    // first batch per query: kD0 = 128 when many queries fill the GPU; with few
-                    // queries a round is latency-bound (one pair's DTW is a ~n-step chain), so the
-                    // batches start larger (2^15 / Qb items: fewer, fuller rounds)
-                    const int d0 = env_d0 > 0 ? env_d0
-                                              : (int)std::min<int64_t>(kDMax, std::max<int64_t>(kD0, (1 << 15) / qn));
-                    plan_kernel<<<1, 1024, 0, st>>>(s, (int)qn, list, cap, sorted, d0);
+                    // batch per query and round: kD0 << (round * gs).  The first round stays small (its
+                    // pairs run with tau = +inf: none is abandoned, and every completed pair is merged
+                    // into the query's top-k under its lock); with few queries a round is
+                    // latency-bound (one pair's DTW is a ~n-step chain), so later batches grow 8x per
+                    // round instead of 2x (fewer, fuller rounds)
+                    const int d0 = env_d0 > 0 ? env_d0 : kD0;
+                    const int gs = qn <= 64 ? 3 : 1;
+                    plan_kernel<<<1, 1024, 0, st>>>(s, (int)qn, list, cap, sorted, d0, gs);
                     DTWLB_LAUNCH_CHECK();
                     int tot2[2] = {0, 0};
                     if (!dev_rounds) {

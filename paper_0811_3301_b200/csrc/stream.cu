@@ -201,13 +201,15 @@ keogh_stream_kernel(const float *__restrict__ U, const float *__restrict__ L, co
 
 // ---------------------------------------------------------------------------------------
 // COPY = 2 (default): 2D TMA.  The database is a [N][n] fp32 tensor map; a warp owns tiles of
-// 32 rows and streams them through its own ring of D boxes of 32 rows x 64 floats (8 KB, one
+// 32 rows and streams them through its own ring of D boxes of 32 rows x 32 floats (4 KB, one
 // cp.async.bulk.tensor per box issued by lane 0, completing on the warp's mbarrier of that
-// stage; out-of-range rows / columns are zero-filled by the TMA unit).  Lane t owns row t of
-// the box and visits its 64 columns in a lane-rotated order (column e + 4 (t & 7)), so the
-// 128-bit shared-memory reads of a quarter-warp hit 8 distinct bank groups for the row data
-// and 8 consecutive float4 of the query envelopes -- no bank conflicts without padding.
-constexpr int kBoxRows = 32, kBoxCols = 64, kTmaWarps = 8;
+// stage; out-of-range rows / columns are zero-filled by the TMA unit).  The boxes are written
+// with the TMA 128-byte swizzle (16-byte chunk c of row r lands at chunk c ^ (r & 7)): lane t
+// owns row t and reads logical chunk k at physical chunk k ^ (t & 7), so the 8 lanes of a
+// quarter-warp hit 8 distinct bank groups, while every lane reads the SAME query-envelope
+// chunk -- a shared-memory broadcast.  (An unswizzled, lane-rotated layout measured 0.55 ms at
+// Q = 8, bound by the non-broadcast envelope reads.)
+constexpr int kBoxRows = 32, kBoxCols = 32, kTmaWarps = 8;
 
 template <int P, int QB>
 __global__ void __launch_bounds__(kTmaWarps * 32, 1)
@@ -217,8 +219,9 @@ keogh_stream_tma_kernel(const __grid_constant__ CUtensorMap tmap, const float *_
     extern __shared__ __align__(1024) unsigned char smraw[];
     const int npad = (n + kBoxCols - 1) / kBoxCols * kBoxCols;
     const int nch = npad / kBoxCols;
-    constexpr int BOX = kBoxRows * kBoxCols;  // floats
-    float *boxes = reinterpret_cast<float *>(smraw);                // [warps][D][32][64]
+    constexpr int BOX = kBoxRows * kBoxCols;  // floats (4 KB: a multiple of the 1 KB swizzle atom)
+    // (the dynamic shared-memory base is only guaranteed 16-byte aligned: round up to 1 KB)
+    float *boxes = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
     float *sU = boxes + (size_t)kTmaWarps * D * BOX;                // [QB][npad]
     float *sL = sU + (size_t)QB * npad;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sL + (size_t)QB * npad);  // [warps][D]
@@ -259,7 +262,7 @@ keogh_stream_tma_kernel(const __grid_constant__ CUtensorMap tmap, const float *_
     };
     const int pro = (int)(steps < D - 1 ? steps : D - 1);
     for (int g = 0; g < pro; ++g) issue(g);
-    const int rot = 4 * (lane & 7);
+    const int swz = lane & 7;
     float acc[QB];
 #pragma unroll
     for (int q = 0; q < QB; ++q) acc[q] = 0.f;
@@ -274,14 +277,13 @@ keogh_stream_tma_kernel(const __grid_constant__ CUtensorMap tmap, const float *_
         float part[QB];
 #pragma unroll
         for (int q = 0; q < QB; ++q) part[q] = 0.f;
-#pragma unroll 4
-        for (int e = 0; e < kBoxCols; e += 4) {
-            const int col = (e + rot) & (kBoxCols - 1);
-            const float4 xv = *reinterpret_cast<const float4 *>(xr + col);
+#pragma unroll
+        for (int k = 0; k < kBoxCols / 4; ++k) {
+            const float4 xv = *reinterpret_cast<const float4 *>(xr + 4 * (k ^ swz));
 #pragma unroll
             for (int q = 0; q < QB; ++q) {
-                const float4 u = *reinterpret_cast<const float4 *>(ub + (size_t)q * npad + col);
-                const float4 l = *reinterpret_cast<const float4 *>(lb + (size_t)q * npad + col);
+                const float4 u = *reinterpret_cast<const float4 *>(ub + (size_t)q * npad + 4 * k);
+                const float4 l = *reinterpret_cast<const float4 *>(lb + (size_t)q * npad + 4 * k);
                 part[q] = lb4<P>(part[q], xv, u, l);
             }
         }
@@ -330,7 +332,7 @@ int launch_stream_tma_t(const float *U, const float *L, const float *db, int64_t
     const cuuint32_t box[2] = {kBoxCols, kBoxRows};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(db), gdim, gstride, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         set_error(DTWLB_ECUDA, "stream LB_Keogh pass: cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -344,7 +346,7 @@ int launch_stream_tma_t(const float *U, const float *L, const float *db, int64_t
     DTWLB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     const size_t per_stage = (size_t)kTmaWarps * (kBoxRows * kBoxCols * sizeof(float) + sizeof(uint64_t));
     static const int env_d = [] { const char *e = getenv("DTWLB_STREAM_STAGES"); return e ? atoi(e) : 0; }();
-    int D = env_d > 1 ? std::min(env_d, 8) : 4;
+    int D = env_d > 1 ? std::min(env_d, 12) : 6;
     while (D > 2 && env + D * per_stage + 1024 > (size_t)smem_max) --D;
     const size_t smem = env + D * per_stage + 1024;
     if (smem > (size_t)smem_max) {
@@ -419,7 +421,7 @@ int launch_keogh_stream(const float *U, const float *L, const float *db, int64_t
                   kStreamMaxQ);
         return DTWLB_EINVAL;
     }
-    // copy engine: 2 = 2D TMA boxes (default; n >= 64), 0 = per-row TMA bulk copies, 1 = cp.async
+    // copy engine: 2 = 2D TMA boxes (default; n >= 32), 0 = per-row TMA bulk copies, 1 = cp.async
     static const int env_copy = [] { const char *e = getenv("DTWLB_STREAM_COPY"); return e ? atoi(e) : 2; }();
     if (env_copy == 2 && n >= kBoxCols)
         return p == 1 ? launch_stream_tma_p<1>(U, L, db, Q, N, n, rooted, out, ldo, st)
