@@ -19,7 +19,7 @@ CHECKED = os.environ.get("DTWLB_CHECKED") == "1"  # debug build with device boun
 LIB = os.path.join(HERE, "libdtwlb_checked.so" if CHECKED else "libdtwlb.so")
 OBJ = os.path.join(HERE, "_obj_checked" if CHECKED else "_obj")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
-SOURCES = ["abi.cu", "envelope.cu", "keogh.cu", "stream.cu", "improved.cu", "dtw.cu", "search.cu"]
+SOURCES = ["abi.cu", "envelope.cu", "keogh.cu", "stream.cu", "improved.cu", "dtw.cu", "dtw_wide.cu", "search.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-I", INCLUDE] + (["-DDTWLB_CHECKED"] if CHECKED else [])

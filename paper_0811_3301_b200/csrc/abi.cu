@@ -247,7 +247,19 @@ int dtw_band(const float *x, const float *y, int32_t n, int32_t w, int32_t p, fl
     a.w = w;
     a.total = count;
     a.res = out;
-    if (w > 64) {
+    int wS = 0;
+    const int wide = w > 64 ? dtw_wide_plan(n, w, &wS) : 0;
+    if (wide) {  // four lanes per pair, band (or the full row) in registers (dtw_wide.cu)
+        int padL = 0;
+        const int LPW = dtw_wide_padded(n, w, wS, &padL);
+        float *yp;
+        DTWLB_TRY(ws_get_bytes(5, sizeof(float) * count * LPW, (void **)&yp));
+        DTWLB_TRY(launch_build_ywide(y, count, n, yp, LPW, padL, st));
+        unsigned *queue;
+        DTWLB_TRY(ws_get_bytes(7, 64, (void **)&queue));
+        a.queue = queue;
+        DTWLB_TRY(launch_dtw_wide(a, yp, LPW, padL, p, false, st));
+    } else if (w > 64) {
         float *scratch = nullptr;
         if (dtw_generic_needs_scratch(w))
             DTWLB_TRY(ws_get_bytes(4, sizeof(float) * count * (2 * w + 2), (void **)&scratch));

@@ -1,0 +1,403 @@
+// dtw_wide.cu -- banded DTW_p for WIDE bands (w > 64: the band no longer fits one thread's
+// registers), the a5 step of the cascade.  Recursion of P:199-210 (section "Dynamic Time
+// Warping") in its forward (prefix) form, as dtw.cu:
+//
+//   D(i,j) = |x_i - y_j|^p + min(D(i-1,j), D(i,j-1), D(i-1,j-1)),  |i-j| <= w,
+//   D(-1,-1) = 0, everything else outside the band = +inf;  DTW_p^p = D(n-1,n-1).
+//
+// B200 design: ONE PAIR PER FOUR LANES.  The 2w+1-cell band of a row is split into four
+// segments of S cells held in the registers of four consecutive lanes (S = 51 for w = 100).
+// Lane t processes row r = s - t at step s (a skewed pipeline): the left neighbour of its
+// first cell is lane t-1's last cell of the same row, computed one step earlier, and the
+// up neighbour of its last cell is lane t+1's first cell of the previous row, computed
+// first in the same step -- two warp shuffles per row, every other cell dependency is in
+// registers, so a cell is the same 3-op FADD, FMNMX3, FFMA|FADD sequence as dtw4_kernel.
+// The query values of a lane's cells sit in a register window that shifts by four columns
+// every four rows (4 new values loaded one block ahead, like the row's x values).
+// UNCONSTRAINED DTW (w >= n-1, the Appendix B workload P:1079-1092) uses COLUMN coordinates
+// instead: lane t owns columns [tS, tS+S) of every row, its query values are constant, and
+// the only exchange is the last column to lane t+1 (one shuffle per row); columns beyond n
+// never feed a valid cell (dependencies point left and up only).
+// Eight pairs per warp advance in lockstep phases of 8 rows: pairs start at step multiples of
+// 8, the exact early abandon (reading c15: a row whose minimum exceeds tau^p(1+eps) ends the
+// pair; the four lanes record their segment minima of the checkpoint row and combine them
+// with two shuffles) and the refills of finished groups happen at the same phase for every
+// group, so the control flow stays warp-uniform.  Work items come from a global counter in
+// chunks of 32.
+#include "kernels.cuh"
+
+namespace dtwlb {
+
+namespace {
+
+constexpr int KW = 4;      // lanes per pair
+constexpr int NTW = 128;   // threads per CTA
+constexpr int kWChunk = 32;
+
+template <int P>
+__device__ __forceinline__ float wcell(float m, float t) {
+    if constexpr (P == 1) return m + fabsf(t);
+    else if constexpr (P == 0) return fmaxf(m, fabsf(t));  // DTW_inf
+    else return fmaf(t, t, m);
+}
+
+// in-band cells of rows 0 .. r-1 (see dtw.cu band_cells)
+__device__ __forceinline__ unsigned long long wband_cells(int r, int n, int w) {
+    const long long m = r < w ? r : w;
+    const long long a0 = n - w;
+    const long long tt = r > a0 ? r - a0 : 0;
+    return (unsigned long long)((long long)r * (2 * w + 1) - (m * w - m * (m - 1) / 2) - tt * (tt + 1) / 2);
+}
+
+// COL = false: band coordinates (cell e of lane t = band position d = tS + e, column r - w + d);
+//      true : column coordinates (cell e of lane t = column tS + e), w >= n - 1 only.
+// yp: padded query rows [rows][LPW], yp[u] = y[u - padL] (+inf outside [0, n)).
+template <int S>
+constexpr int wide_min_blocks() { return S <= 32 ? 3 : 2; }
+
+template <int S, int P, bool WALK, bool COL>
+__global__ void __launch_bounds__(NTW, wide_min_blocks<S>())
+dtw_wide_kernel(DtwArgs a, const float *__restrict__ yp, int LPW, int padL) {
+    constexpr int NY = COL ? S : S + 3;
+    const int lane = threadIdx.x & 31, t = lane & 3;
+    const unsigned FULL = 0xffffffffu;
+    const int n = a.n, w = a.w, NB = 2 * w + 1;
+    const int64_t total = (WALK && a.dev_total) ? (int64_t)*a.dev_total : a.total;
+    // band mode: lane 3 holds M = 4S - NB invalid cells at its top positions (0 <= M <= 3);
+    // they are reset to +inf after every row so they never feed a valid cell
+    const int M = COL ? 0 : 4 * S - NB;
+    const float mk0 = (!COL && t == 3 && M >= 3) ? kInf : -kInf;
+    const float mk1 = (!COL && t == 3 && M >= 2) ? kInf : -kInf;
+    const float mk2 = (!COL && t == 3 && M >= 1) ? kInf : -kInf;
+    // cell holding D(n-1, n-1): band position w, or column n-1
+    const int dfin = COL ? n - 1 : w;
+    const int tfin = dfin / S, efin = dfin - tfin * S;
+
+    bool busy = false;
+    int s0 = 0;
+    uint32_t cand = 0;
+    int qy = 0;
+    int64_t item = 0;
+    float thr = kInf;
+    const float *xr = nullptr, *yr = nullptr;
+    float B[S], Y[NY], xc[4], xn[4], yn[4];
+    float left_in = kInf, diag_in = kInf, segmin = kInf;
+    unsigned long long n_cells = 0;
+    unsigned n_started = 0, n_abandon = 0;
+    int64_t wcur = 0, wend = 0;
+    bool more_items = true;
+
+    for (int s = 0;; s += 4) {
+        // ---------------- refill (phase 0 of 8): free groups start new pairs at s0 = s
+        if ((s & 7) == 0) {
+            while (true) {
+                const unsigned needm = __ballot_sync(FULL, t == 0 && !busy) & 0x11111111u;
+                if (!needm || !more_items) break;
+                if (wcur >= wend) {
+                    int64_t base = 0;
+                    if (lane == 0) base = (int64_t)atomicAdd(a.queue, (unsigned)kWChunk);
+                    base = __shfl_sync(FULL, base, 0);
+                    if (base >= total) { more_items = false; break; }
+                    wcur = base;
+                    wend = base + kWChunk < total ? base + kWChunk : total;
+                }
+                const int rank = __popc(needm & ((1u << (lane & ~3)) - 1u));
+                const int take = __popc(needm);
+                const int64_t mine = wcur + rank;
+                const bool got = !busy && mine < wend;
+                wcur = wcur + take < wend ? wcur + take : wend;
+                if (got) {
+                    item = mine;
+                    float beta = 0.f;
+                    if constexpr (WALK) {
+                        int lo = 0, hi = a.Qb;  // item_off[lo] <= item < item_off[hi]
+                        while (hi - lo > 1) {
+                            const int mid = (lo + hi) >> 1;
+                            if (a.item_off[mid] <= item) lo = mid; else hi = mid;
+                        }
+                        qy = lo;
+                        const int64_t j = a.pos[qy] + (item - a.item_off[qy]);
+                        const unsigned long long key = a.list[(int64_t)qy * a.cap + j];
+                        cand = (uint32_t)(key & 0xffffffffu);
+                        beta = __uint_as_float((uint32_t)(key >> 32));
+                        thr = *reinterpret_cast<volatile float *>(a.thr + qy);
+                        xr = a.db + (int64_t)cand * n;
+                        yr = yp + (int64_t)qy * LPW;
+                    } else {
+                        cand = (uint32_t)item;
+                        thr = kInf;
+                        xr = a.db + item * n;
+                        yr = yp + item * LPW;
+                    }
+                    if (!(beta > thr)) {  // (WALK: else pruned by its bound before any cell)
+                        busy = true;
+                        s0 = s;
+                        ++n_started;
+                        // row -1: D(-1, -1) = 0 (band position w), everything else +inf
+#pragma unroll
+                        for (int e = 0; e < S; ++e) B[e] = (!COL && t * S + e == w) ? 0.f : kInf;
+                        left_in = kInf;
+                        diag_in = (COL && t == 0) ? 0.f : kInf;
+                        segmin = kInf;
+                        const int rb = -t;  // first block's first row of this lane
+                        if constexpr (COL) {
+#pragma unroll
+                            for (int e = 0; e < S; ++e) Y[e] = yr[padL + t * S + e];
+                        } else {
+                            // window of the block BEFORE the first (the block start shifts it)
+#pragma unroll
+                            for (int k = 4; k < NY; ++k) Y[k] = yr[padL + rb - 4 - w + t * S + k];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) yn[k] = yr[padL + rb - w + t * S + S - 1 + k];
+                        }
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) xn[k] = (rb + k >= 0 && rb + k < n) ? __ldg(xr + rb + k) : 0.f;
+                    } else if constexpr (!WALK) {
+                        a.res[item] = kInf;
+                    }
+                }
+            }
+            if (!__any_sync(FULL, busy)) {
+                if (!more_items) break;
+                continue;
+            }
+        }
+        // ---------------- block start: rows rb .. rb+3 of this lane
+        const int rb = s - s0 - t;
+        if (busy) {
+            if constexpr (!COL) {
+#pragma unroll
+                for (int k = 0; k < S - 1; ++k) Y[k] = Y[k + 4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) Y[S - 1 + k] = yn[k];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) yn[k] = yr[padL + rb + 4 - w + t * S + S - 1 + k];
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) xc[k] = xn[k];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) xn[k] = (rb + 4 + k >= 0 && rb + 4 + k < n) ? __ldg(xr + rb + 4 + k) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int r = rb + u;
+            const bool active = busy && r >= 0 && r < n;
+            if constexpr (COL) {
+                if (active) {
+                    float dg = diag_in, lf = left_in;
+#pragma unroll
+                    for (int e = 0; e < S; ++e) {
+                        const float up = B[e];
+                        const float v = wcell<P>(min3f(dg, up, lf), xc[u] - Y[e]);
+                        dg = up;
+                        lf = v;
+                        B[e] = v;
+                    }
+                    if (WALK && (r & 7) == 7) {
+                        float m = B[0];
+#pragma unroll
+                        for (int e = 1; e + 1 < S; e += 2) m = min3f(m, B[e], B[e + 1]);
+                        if ((S & 1) == 0) m = fminf(m, B[S - 1]);
+                        segmin = m;
+                    }
+                }
+                float recv = __shfl_up_sync(FULL, B[S - 1], 1, KW);
+                if (t == 0) recv = kInf;
+                diag_in = left_in;
+                left_in = recv;
+            } else {
+                float v0 = B[0];
+                if (active) {
+                    v0 = wcell<P>(min3f(B[0], B[1], left_in), xc[u] - Y[u]);
+                    B[0] = v0;
+                }
+                float upl = __shfl_down_sync(FULL, v0, 1, KW);
+                if (t == KW - 1) upl = kInf;
+                if (active) {
+                    float prev = v0;
+#pragma unroll
+                    for (int e = 1; e < S - 1; ++e) {
+                        const float v = wcell<P>(min3f(B[e], B[e + 1], prev), xc[u] - Y[e + u]);
+                        B[e] = v;
+                        prev = v;
+                    }
+                    B[S - 1] = wcell<P>(min3f(B[S - 1], upl, prev), xc[u] - Y[S - 1 + u]);
+                    B[S - 3] = fmaxf(B[S - 3], mk0);
+                    B[S - 2] = fmaxf(B[S - 2], mk1);
+                    B[S - 1] = fmaxf(B[S - 1], mk2);
+                    if (WALK && (r & 7) == 7) {
+                        float m = B[0];
+#pragma unroll
+                        for (int e = 1; e + 1 < S; e += 2) m = min3f(m, B[e], B[e + 1]);
+                        if ((S & 1) == 0) m = fminf(m, B[S - 1]);
+                        segmin = m;
+                    }
+                }
+                float recv = __shfl_up_sync(FULL, B[S - 1], 1, KW);
+                if (t == 0) recv = kInf;
+                left_in = recv;
+            }
+            const int ph = s + u - s0;  // group phase (uniform in the group)
+            // ---- completion: the last lane finished row n-1
+            if (busy && ph == n - 1 + KW - 1) {
+                float res = kInf;
+#pragma unroll
+                for (int e = 0; e < S; ++e)
+                    if (t == tfin && e == efin) res = B[e];
+                res = fminf(res, __shfl_xor_sync(FULL, res, 1, KW));
+                res = fminf(res, __shfl_xor_sync(FULL, res, 2, KW));
+                if (t == 0) {
+                    n_cells += wband_cells(n, n, w);
+                    if constexpr (WALK) {
+                        if (res <= thr) {
+                            const unsigned pos = atomicAdd(a.rcount, 1u);
+                            DCHECK(pos < a.rcap, "wide result buffer overflow pos=%u", pos);
+                            a.rkey[pos] = pack_key(res, cand);
+                            a.rq[pos] = qy;
+                        }
+                    } else {
+                        a.res[item] = rootp<P>(res);
+                    }
+                }
+                busy = false;
+            }
+            // ---- exact early abandon (reading c15): checkpoint row 8m+7 complete in all lanes
+            if constexpr (WALK) {
+                if (((s + u) & 7) == 2) {  // (uniform: every group's s0 is a multiple of 8)
+                    float m = segmin;
+                    m = fminf(m, __shfl_xor_sync(FULL, m, 1, KW));
+                    m = fminf(m, __shfl_xor_sync(FULL, m, 2, KW));
+                    if (busy && ph >= 10) {
+                        thr = fminf(thr, *reinterpret_cast<volatile float *>(a.thr + qy));
+                        if (m > thr) {
+                            if (t == 0) {
+                                ++n_abandon;
+                                n_cells += wband_cells(ph - KW + 2, n, w);  // rows 0 .. ph-3 done
+                            }
+                            busy = false;
+                        }
+                    }
+                }
+            }
+        }
+    }
+    if (a.cells) {
+        unsigned long long c = n_cells;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+        if (lane == 0 && c) atomicAdd(a.cells, c);
+    }
+    if (a.started) {
+        unsigned c = t == 0 ? n_started : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+        if (lane == 0 && c) atomicAdd(a.started, (unsigned long long)c);
+    }
+    if (a.abandoned) {
+        unsigned c = n_abandon;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+        if (lane == 0 && c) atomicAdd(a.abandoned, (unsigned long long)c);
+    }
+}
+
+__global__ void build_ywide_kernel(const float *__restrict__ y, int64_t rows, int n, float *__restrict__ yp,
+                                   int LPW, int padL) {
+    const int64_t total = rows * (int64_t)LPW;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = t / LPW;
+        const int j = (int)(t - r * LPW) - padL;
+        yp[t] = (j >= 0 && j < n) ? y[r * n + j] : kInf;
+    }
+}
+
+template <int S, int P, bool WALK, bool COL>
+int launch_wide_t(const DtwArgs &a, const float *yp, int LPW, int padL, cudaStream_t st) {
+    DTWLB_CUDA(cudaMemsetAsync(a.queue, 0, sizeof(unsigned), st));
+    int dev = 0, nsm = 148;
+    DTWLB_CUDA(cudaGetDevice(&dev));
+    DTWLB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    // enough warps to hold every pair of the round (8 per warp), at most 3 CTAs x 4 warps per SM
+    const int64_t warps = std::min<int64_t>(ceil_div(std::max<int64_t>(a.total, 1), 8), (int64_t)nsm * 12);
+    const int64_t grid = ceil_div(warps * 32, NTW);
+    dtw_wide_kernel<S, P, WALK, COL><<<(unsigned)grid, NTW, 0, st>>>(a, yp, LPW, padL);
+    DTWLB_LAUNCH_CHECK();
+    return DTWLB_OK;
+}
+
+template <int P, bool WALK>
+int launch_wide_p(const DtwArgs &a, const float *yp, int LPW, int padL, int mode, int S, cudaStream_t st) {
+    if (mode == 1) {  // column coordinates (w >= n - 1)
+        switch (S) {
+            case 16: return launch_wide_t<16, P, WALK, true>(a, yp, LPW, padL, st);
+            case 25: return launch_wide_t<25, P, WALK, true>(a, yp, LPW, padL, st);
+            case 32: return launch_wide_t<32, P, WALK, true>(a, yp, LPW, padL, st);
+            case 48: return launch_wide_t<48, P, WALK, true>(a, yp, LPW, padL, st);
+            case 64: return launch_wide_t<64, P, WALK, true>(a, yp, LPW, padL, st);
+        }
+    } else {
+        switch (S) {
+            case 51: return launch_wide_t<51, P, WALK, false>(a, yp, LPW, padL, st);
+        }
+    }
+    set_error(DTWLB_EINVAL, "internal: no wide DTW kernel for S = %d", S);
+    return DTWLB_EINVAL;
+}
+
+}  // namespace
+
+// Which wide kernel handles (n, w), if any: mode 1 = column coordinates (w >= n-1, n <= 256),
+// mode 2 = band coordinates (S = ceil((2w+1)/4) instantiated: w = 100, 101); 0 = none (generic).
+int dtw_wide_plan(int n, int w, int *S_out) {
+    if (w >= n - 1 && n <= 256) {
+        const int need = (n + KW - 1) / KW;
+        const int opts[] = {16, 25, 32, 48, 64};
+        for (int S : opts)
+            if (S >= need) { *S_out = S; return 1; }
+    }
+    const int S = (2 * w + 1 + KW - 1) / KW;
+    if (S == 51) { *S_out = S; return 2; }
+    return 0;
+}
+
+int dtw_wide_padded(int n, int w, int S, int *padL) {
+    *padL = (w + 8 + 3) / 4 * 4;
+    return (*padL + n + KW * S + 16 + 3) / 4 * 4;
+}
+
+int launch_build_ywide(const float *y, int64_t rows, int n, float *yp, int LPW, int padL, cudaStream_t st) {
+    if (rows == 0) return DTWLB_OK;
+    const int64_t total = rows * (int64_t)LPW;
+    const int grid = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
+    build_ywide_kernel<<<grid, 256, 0, st>>>(y, rows, n, yp, LPW, padL);
+    DTWLB_LAUNCH_CHECK();
+    return DTWLB_OK;
+}
+
+int launch_dtw_wide(const DtwArgs &a, const float *yp, int LPW, int padL, int p, bool walk, cudaStream_t st) {
+    int S = 0;
+    const int mode = dtw_wide_plan(a.n, a.w, &S);
+    if (mode == 0) {
+        set_error(DTWLB_EINVAL, "internal: no wide DTW kernel for n = %d, w = %d", a.n, a.w);
+        return DTWLB_EINVAL;
+    }
+    if (!a.queue) {
+        set_error(DTWLB_EINVAL, "internal: the wide DTW kernel needs its work-queue counter");
+        return DTWLB_EINVAL;
+    }
+    if (walk && !a.dev_total && a.total == 0) return DTWLB_OK;
+    if (p == 0) {
+        if (walk) {
+            set_error(DTWLB_EUNSUPPORTED, "nn_search: p = infinity unsupported");
+            return DTWLB_EUNSUPPORTED;
+        }
+        return launch_wide_p<0, false>(a, yp, LPW, padL, mode, S, st);
+    }
+    if (p == 1) return walk ? launch_wide_p<1, true>(a, yp, LPW, padL, mode, S, st)
+                            : launch_wide_p<1, false>(a, yp, LPW, padL, mode, S, st);
+    return walk ? launch_wide_p<2, true>(a, yp, LPW, padL, mode, S, st)
+                : launch_wide_p<2, false>(a, yp, LPW, padL, mode, S, st);
+}
+
+}  // namespace dtwlb

@@ -151,6 +151,13 @@ int dtw_padded_len(int n);
 int launch_dtw(const DtwArgs &a, int p, bool walk, cudaStream_t st);
 // w > 64: does the generic kernel need a global band scratch of (2w+2) floats per item?
 bool dtw_generic_needs_scratch(int w);
+// Wide bands (dtw_wide.cu, four lanes per pair): dtw_wide_plan returns 1 (column coordinates,
+// w >= n-1, n <= 256), 2 (band coordinates, instantiated S) or 0 (no wide kernel: generic);
+// the query rows are padded to LPW = dtw_wide_padded(n, w, S, &padL) floats (+inf outside).
+int dtw_wide_plan(int n, int w, int *S);
+int dtw_wide_padded(int n, int w, int S, int *padL);
+int launch_build_ywide(const float *y, int64_t rows, int n, float *yp, int LPW, int padL, cudaStream_t st);
+int launch_dtw_wide(const DtwArgs &a, const float *yp, int LPW, int padL, int p, bool walk, cudaStream_t st);
 // Build the 4 shifted, +inf-padded copies of `rows` query rows.
 int launch_build_ysh(const float *y, int64_t rows, int n, float *ysh, int LP, cudaStream_t st);
 

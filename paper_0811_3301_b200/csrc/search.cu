@@ -563,6 +563,15 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         DTWLB_TRY(wsget(S_YSH, (size_t)4 * Q * LP, &ysh));
         DTWLB_TRY(launch_build_ysh(queries, Q, n, ysh, LP, st));
     }
+    // w > 64: the four-lanes-per-pair kernel (dtw_wide.cu) where instantiated, else the generic one
+    int wide_S = 0, wide_padL = 0, wide_LPW = 0;
+    const int wide_mode = generic_dtw ? dtw_wide_plan(n, w, &wide_S) : 0;
+    float *ywide = nullptr;
+    if (wide_mode) {
+        wide_LPW = dtw_wide_padded(n, w, wide_S, &wide_padL);
+        DTWLB_TRY(wsget(S_YSH, (size_t)Q * wide_LPW, &ywide));
+        DTWLB_TRY(launch_build_ywide(queries, Q, n, ywide, wide_LPW, wide_padL, st));
+    }
     // U(x), L(x): [2][N][n] -- the caller's database index (nn_opts.db_env) or computed here
     const float *dbenv = opts ? opts->db_env : nullptr;
     if (!dbenv && (!keogh_only || prefilter)) {
@@ -845,7 +854,11 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                             da.Lxdb = dbenv + (size_t)N * n;
                         }
                     }
-                    if (generic_dtw) {
+                    if (wide_mode) {
+                        const cudaEvent_t d0 = stats ? rec() : nullptr;
+                        DTWLB_TRY(launch_dtw_wide(da, ywide + (size_t)qb0 * wide_LPW, wide_LPW, wide_padL, p, true, st));
+                        if (stats) span(d0, rec(), &ms_dtw_kernel);
+                    } else if (generic_dtw) {
                         // global band scratch only when 128 bands do not fit in shared memory,
                         // sized by this round's item count
                         float *scratch = nullptr;

@@ -209,24 +209,28 @@ keogh_stream_kernel(const float *__restrict__ U, const float *__restrict__ L, co
 // quarter-warp hit 8 distinct bank groups, while every lane reads the SAME query-envelope
 // chunk -- a shared-memory broadcast.  (An unswizzled, lane-rotated layout measured 0.55 ms at
 // Q = 8, bound by the non-broadcast envelope reads.)
-constexpr int kBoxRows = 32, kBoxCols = 32, kTmaWarps = 8;
+// R > 1: lane t owns rows t, t+32, .. of a 32R-row box, so every envelope chunk read from
+// shared memory serves R rows (a 128-bit read costs 4 shared-memory wavefronts, broadcast or
+// not: with R = 1 and Q >= 2 the envelope reads, not HBM, bounded the kernel).
+constexpr int kBoxCols = 32;
 
-template <int P, int QB>
-__global__ void __launch_bounds__(kTmaWarps * 32, 1)
+template <int P, int QB, int R, int W>
+__global__ void __launch_bounds__(W * 32, 1)
 keogh_stream_tma_kernel(const __grid_constant__ CUtensorMap tmap, const float *__restrict__ U,
                         const float *__restrict__ L, int64_t N, int n, int Q, int D, bool rooted,
                         float *__restrict__ out, int64_t ldo) {
     extern __shared__ __align__(1024) unsigned char smraw[];
+    constexpr int ROWS = 32 * R;
     const int npad = (n + kBoxCols - 1) / kBoxCols * kBoxCols;
     const int nch = npad / kBoxCols;
-    constexpr int BOX = kBoxRows * kBoxCols;  // floats (4 KB: a multiple of the 1 KB swizzle atom)
+    constexpr int BOX = ROWS * kBoxCols;  // floats (a multiple of the 1 KB swizzle atom)
     // (the dynamic shared-memory base is only guaranteed 16-byte aligned: round up to 1 KB)
     float *boxes = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-    float *sU = boxes + (size_t)kTmaWarps * D * BOX;                // [QB][npad]
+    float *sU = boxes + (size_t)W * D * BOX;  // [QB][npad]
     float *sL = sU + (size_t)QB * npad;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sL + (size_t)QB * npad);  // [warps][D]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sL + (size_t)QB * npad);  // [W][D]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int t = tid; t < QB * npad; t += kTmaWarps * 32) {
+    for (int t = tid; t < QB * npad; t += W * 32) {
         const int q = t / npad, i = t - q * npad;
         const bool ok = q < Q && i < n;
         sU[t] = ok ? U[(int64_t)q * n + i] : kInf;
@@ -238,8 +242,8 @@ keogh_stream_tma_kernel(const __grid_constant__ CUtensorMap tmap, const float *_
     }
     __syncthreads();
 
-    const int64_t ntiles = (N + kBoxRows - 1) / kBoxRows;
-    const int64_t gw = (int64_t)blockIdx.x * kTmaWarps + warp, GW = (int64_t)gridDim.x * kTmaWarps;
+    const int64_t ntiles = (N + ROWS - 1) / ROWS;
+    const int64_t gw = (int64_t)blockIdx.x * W + warp, GW = (int64_t)gridDim.x * W;
     const int64_t my_tiles = gw < ntiles ? (ntiles - 1 - gw) / GW + 1 : 0;
     const int64_t steps = my_tiles * nch;
     float *mybox = boxes + (size_t)warp * D * BOX;
@@ -255,17 +259,19 @@ keogh_stream_tma_kernel(const __grid_constant__ CUtensorMap tmap, const float *_
             asm volatile(
                 "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
                 "[%4];\n" ::"r"(smem_u32(mybox + (size_t)s * BOX)),
-                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(ch * kBoxCols), "r"((int)(tile * kBoxRows)),
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(ch * kBoxCols), "r"((int)(tile * ROWS)),
                 "r"(smem_u32(mybar + s))
                 : "memory");
         }
     };
     const int pro = (int)(steps < D - 1 ? steps : D - 1);
     for (int g = 0; g < pro; ++g) issue(g);
-    const int swz = lane & 7;
-    float acc[QB];
+    const int swz = lane & 7;  // (rows lane + 32 i share lane & 7)
+    float acc[QB][R];
 #pragma unroll
-    for (int q = 0; q < QB; ++q) acc[q] = 0.f;
+    for (int q = 0; q < QB; ++q)
+#pragma unroll
+        for (int i = 0; i < R; ++i) acc[q][i] = 0.f;
     for (int64_t g = 0; g < steps; ++g) {
         if (g + D - 1 < steps) issue(g + D - 1);
         const int64_t ti = g / nch;
@@ -274,30 +280,44 @@ keogh_stream_tma_kernel(const __grid_constant__ CUtensorMap tmap, const float *_
         mbar_wait(mybar + s, (unsigned)((g / D) & 1));
         const float *xr = mybox + (size_t)s * BOX + lane * kBoxCols;
         const float *ub = sU + ch * kBoxCols, *lb = sL + ch * kBoxCols;
-        float part[QB];
+        float part[QB][R];
 #pragma unroll
-        for (int q = 0; q < QB; ++q) part[q] = 0.f;
+        for (int q = 0; q < QB; ++q)
+#pragma unroll
+            for (int i = 0; i < R; ++i) part[q][i] = 0.f;
 #pragma unroll
         for (int k = 0; k < kBoxCols / 4; ++k) {
-            const float4 xv = *reinterpret_cast<const float4 *>(xr + 4 * (k ^ swz));
+            float4 xv[R];
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+                xv[i] = *reinterpret_cast<const float4 *>(xr + i * 32 * kBoxCols + 4 * (k ^ swz));
 #pragma unroll
             for (int q = 0; q < QB; ++q) {
                 const float4 u = *reinterpret_cast<const float4 *>(ub + (size_t)q * npad + 4 * k);
                 const float4 l = *reinterpret_cast<const float4 *>(lb + (size_t)q * npad + 4 * k);
-                part[q] = lb4<P>(part[q], xv, u, l);
+#pragma unroll
+                for (int i = 0; i < R; ++i) part[q][i] = lb4<P>(part[q][i], xv[i], u, l);
             }
         }
 #pragma unroll
-        for (int q = 0; q < QB; ++q) acc[q] += part[q];
-        if (ch == nch - 1) {
-            const int64_t c = (gw + ti * GW) * kBoxRows + lane;
-            if (c < N) {
+        for (int q = 0; q < QB; ++q)
 #pragma unroll
-                for (int q = 0; q < QB; ++q)
-                    if (q < Q) out[(int64_t)q * ldo + c] = rooted ? rootp<P>(acc[q]) : acc[q];
+            for (int i = 0; i < R; ++i) acc[q][i] += part[q][i];
+        if (ch == nch - 1) {
+            const int64_t c0 = (gw + ti * GW) * ROWS + lane;
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+                const int64_t c = c0 + 32 * i;
+                if (c < N) {
+#pragma unroll
+                    for (int q = 0; q < QB; ++q)
+                        if (q < Q) out[(int64_t)q * ldo + c] = rooted ? rootp<P>(acc[q][i]) : acc[q][i];
+                }
             }
 #pragma unroll
-            for (int q = 0; q < QB; ++q) acc[q] = 0.f;
+            for (int q = 0; q < QB; ++q)
+#pragma unroll
+                for (int i = 0; i < R; ++i) acc[q][i] = 0.f;
         }
         __syncwarp();  // every lane is done with box s before lane 0 refills it
     }
@@ -318,7 +338,7 @@ EncodeTiledFn get_encode_tiled() {
     return fn;
 }
 
-template <int P, int QB>
+template <int P, int QB, int R, int W>
 int launch_stream_tma_t(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n, bool rooted,
                         float *out, int64_t ldo, cudaStream_t st) {
     EncodeTiledFn enc = get_encode_tiled();
@@ -326,10 +346,11 @@ int launch_stream_tma_t(const float *U, const float *L, const float *db, int64_t
         set_error(DTWLB_ECUDA, "stream LB_Keogh pass: cuTensorMapEncodeTiled unavailable");
         return DTWLB_ECUDA;
     }
+    constexpr int ROWS = 32 * R;
     CUtensorMap tmap;
     const cuuint64_t gdim[2] = {(cuuint64_t)n, (cuuint64_t)N};
     const cuuint64_t gstride[1] = {(cuuint64_t)n * sizeof(float)};
-    const cuuint32_t box[2] = {kBoxCols, kBoxRows};
+    const cuuint32_t box[2] = {kBoxCols, ROWS};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(db), gdim, gstride, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -344,20 +365,21 @@ int launch_stream_tma_t(const float *U, const float *L, const float *db, int64_t
     DTWLB_CUDA(cudaGetDevice(&dev));
     DTWLB_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     DTWLB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    const size_t per_stage = (size_t)kTmaWarps * (kBoxRows * kBoxCols * sizeof(float) + sizeof(uint64_t));
+    const size_t per_stage = (size_t)W * (ROWS * kBoxCols * sizeof(float) + sizeof(uint64_t));
     static const int env_d = [] { const char *e = getenv("DTWLB_STREAM_STAGES"); return e ? atoi(e) : 0; }();
-    int D = env_d > 1 ? std::min(env_d, 12) : 6;
+    // ~192 KB of boxes per SM: D - 1 boxes per warp in flight while it computes on one
+    int D = env_d > 1 ? std::min(env_d, 12) : (int)std::max<size_t>(2, (192 * 1024) / per_stage);
     while (D > 2 && env + D * per_stage + 1024 > (size_t)smem_max) --D;
     const size_t smem = env + D * per_stage + 1024;
     if (smem > (size_t)smem_max) {
         set_error(DTWLB_EUNSUPPORTED, "stream LB_Keogh pass: n = %d too long for shared memory", n);
         return DTWLB_EUNSUPPORTED;
     }
-    auto k = keogh_stream_tma_kernel<P, QB>;
+    auto k = keogh_stream_tma_kernel<P, QB, R, W>;
     DTWLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t ntiles = ceil_div(N, kBoxRows);
-    const int grid = (int)std::min<int64_t>(ceil_div(ntiles, kTmaWarps), nsm);  // persistent
-    k<<<grid, kTmaWarps * 32, smem, st>>>(tmap, U, L, N, n, (int)Q, D, rooted, out, ldo);
+    const int64_t ntiles = ceil_div(N, ROWS);
+    const int grid = (int)std::min<int64_t>(ceil_div(ntiles, W), nsm);  // persistent
+    k<<<grid, W * 32, smem, st>>>(tmap, U, L, N, n, (int)Q, D, rooted, out, ldo);
     DTWLB_LAUNCH_CHECK();
     return DTWLB_OK;
 }
@@ -365,10 +387,11 @@ int launch_stream_tma_t(const float *U, const float *L, const float *db, int64_t
 template <int P>
 int launch_stream_tma_p(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n, bool rooted,
                         float *out, int64_t ldo, cudaStream_t st) {
-    if (Q <= 1) return launch_stream_tma_t<P, 1>(U, L, db, Q, N, n, rooted, out, ldo, st);
-    if (Q <= 2) return launch_stream_tma_t<P, 2>(U, L, db, Q, N, n, rooted, out, ldo, st);
-    if (Q <= 4) return launch_stream_tma_t<P, 4>(U, L, db, Q, N, n, rooted, out, ldo, st);
-    return launch_stream_tma_t<P, 8>(U, L, db, Q, N, n, rooted, out, ldo, st);
+    // rows per lane R grows with Q: each envelope read serves R rows (see the kernel)
+    if (Q <= 1) return launch_stream_tma_t<P, 1, 1, 8>(U, L, db, Q, N, n, rooted, out, ldo, st);
+    if (Q <= 2) return launch_stream_tma_t<P, 2, 2, 8>(U, L, db, Q, N, n, rooted, out, ldo, st);
+    if (Q <= 4) return launch_stream_tma_t<P, 4, 4, 4>(U, L, db, Q, N, n, rooted, out, ldo, st);
+    return launch_stream_tma_t<P, 8, 4, 4>(U, L, db, Q, N, n, rooted, out, ldo, st);
 }
 
 template <int P, int QB, int COPY>
