@@ -174,6 +174,30 @@ def test_dtw_band_paper_values(cuda_ok):
     assert dtw_band(x, y, 0, 1).item() == pytest.approx(3.0)
 
 
+# wide bands (w > 64, dtw_wide.cu): band coordinates (w = 100, 101: four lanes x S = 51 cells),
+# column coordinates for unconstrained DTW (w >= n - 1, n <= 256: S = 25/32/48/64 columns per
+# lane, ragged last lane), and the generic fallback (w = 150)
+WIDE_CASES = [(102, 100), (150, 100), (333, 101), (1000, 100), (66, 65), (100, 99), (101, 150), (128, 127),
+              (129, 128), (192, 191), (200, 199), (256, 255), (400, 150)]
+
+
+@pytest.mark.parametrize("n,w", WIDE_CASES)
+@pytest.mark.parametrize("p", [0, 1, 2])
+def test_dtw_band_wide(cuda_ok, n, w, p):
+    from paper_0811_3301_b200 import dtw_band
+    count = 300 if n <= 256 else 60  # > one warp's 8 pairs x several chunks of 32 pairs
+    x, y = series(count, n), series(count, n)
+    x[0] = y[0]
+    x[1] = y[1] + 5.0
+    out = dtw_band(dev(x), dev(y), w, p).cpu().numpy()
+    ref = np.array([oracle.dtw(x[r], y[r], w, p) for r in range(count)])
+    if p == 0:  # DTW_inf: only |x_i - y_j| rounds, exactly once
+        assert np.array_equal(out, ref.astype(np.float32))
+    else:
+        close(out, ref, 1e-4, 1e-6)
+    assert out[0] == 0.0
+
+
 @pytest.mark.parametrize("n,w", [(1, 0), (4, 3), (9, 2), (128, 12), (256, 25), (257, 25), (512, 51), (300, 64),
                                  (100, 99), (1000, 50)])
 def test_dtw_band_inf(cuda_ok, n, w):

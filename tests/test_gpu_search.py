@@ -226,3 +226,17 @@ def test_output_aliasing_rejected(cuda_ok):
         nn_search(q_t, db_t, 25, 1, 2, out=(buf[:8].view(4, 2), buf.view(torch.float32)[4:12].view(4, 2)))
     i2, d2 = nn_search(q_t, db_t, 25, 1, 2, out=(idx, dst))  # disjoint: fine
     assert i2.data_ptr() == idx.data_ptr()
+
+
+@pytest.mark.parametrize("name,Q,N,w", [("C3", 12, 8000, 100), ("C3", 3, 8000, 101), ("C2p1", 40, 4000, 255),
+                                        ("C2p2", 20, 4000, 300), ("C3", 6, 5000, 150)])
+def test_wide_band_walk(cuda_ok, name, Q, N, w):
+    """w > 64 through nn_search: the four-lanes-per-pair band kernel (w = 100, 101), the column
+    kernel for unconstrained DTW (C2 n = 256 with w >= n - 1), and the generic kernel (w = 150);
+    exact early abandon against the walk's thresholds, results equal to the oracle."""
+    c = datagen.CONFIGS[name]
+    qs, db = datagen.make(c, Q=Q, N=N)
+    k = 3
+    g_idx, g_dist = run(qs, db, w, c.p, k)
+    o_idx, o_dist, _ = oracle.nn_twopass(qs, db, w, c.p, k + EXTRA, threads=THREADS)
+    assert_knn_match(g_idx, g_dist, o_idx, o_dist, k)
