@@ -238,15 +238,17 @@ dtw_wide_kernel(DtwArgs a, const float *__restrict__ yp, int LPW, int padL) {
                 left_in = recv;
             }
             const int ph = s + u - s0;  // group phase (uniform in the group)
-            // ---- completion: the last lane finished row n-1
-            if (busy && ph == n - 1 + KW - 1) {
+            // ---- completion: the last lane finished row n-1 (the shuffles run warp-uniformly:
+            //      every lane enters when any group completes)
+            const bool done = busy && ph == n - 1 + KW - 1;
+            if (__any_sync(FULL, done)) {
                 float res = kInf;
 #pragma unroll
                 for (int e = 0; e < S; ++e)
                     if (t == tfin && e == efin) res = B[e];
                 res = fminf(res, __shfl_xor_sync(FULL, res, 1, KW));
                 res = fminf(res, __shfl_xor_sync(FULL, res, 2, KW));
-                if (t == 0) {
+                if (done && t == 0) {
                     n_cells += wband_cells(n, n, w);
                     if constexpr (WALK) {
                         if (res <= thr) {
@@ -259,7 +261,7 @@ dtw_wide_kernel(DtwArgs a, const float *__restrict__ yp, int LPW, int padL) {
                         a.res[item] = rootp<P>(res);
                     }
                 }
-                busy = false;
+                if (done) busy = false;
             }
             // ---- exact early abandon (reading c15): checkpoint row 8m+7 complete in all lanes
             if constexpr (WALK) {
