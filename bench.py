@@ -332,10 +332,13 @@ def run_ours(args, cfg):
                                   "note": "N*n*4 database bytes + Q*N*4 bound bytes per launch"}
         else:
             elems = 2 * (((cfg.n + 7) // 8 + 3) // 4 * 4) if pf else cfg.n
-            kern["bound_pass"] = {"kernel": "keogh_tile_kernel (" + ("piecewise-sum gate, forward + reverse"
-                                                                      if pf else "LB_Keogh") + ")",
+            split = os.environ.get("DTWLB_GATE_SPLIT") == "1"
+            kern["bound_pass"] = {"kernel": ("gate_sym_kernel (symmetric piecewise-sum gate, forward + reverse "
+                                             "in one pass)" if pf and not split else
+                                             "keogh_tile_kernel (" + ("piecewise-sum gate, two launches"
+                                                                      if pf else "LB_Keogh") + ")"),
                                   "bound": "alu", "ms": keogh_ms, "work": 3.0 * cfg.Q * Nr * elems / 1e12,
-                                  "unit": "Tlane-op/s", "peak": peak, "launches": 2 if pf else 1,
+                                  "unit": "Tlane-op/s", "peak": peak, "launches": 2 if pf and split else 1,
                                   "note": f"3 slots per pair-element, {elems} elements per pair"}
         if surv_ms > 0:
             k_in_kernel = keogh_eval if pf else 0.0

@@ -273,6 +273,148 @@ int launch_tile(const float *U, const float *L, const float *db, const float *db
 #undef DTWLB_K
 }
 
+// ---------------------------------------------------------------- fused symmetric gate
+// Both terms of the symmetric piecewise-sum gate (readings c18, c20) in ONE tile pass: per
+// (query, candidate) pair the forward term (candidate sums against the query's envelope sums)
+// and the reverse term (query sums against the candidate's envelope sums) accumulate in two
+// register tiles and the maximum is written once -- instead of a forward launch writing the
+// fp16 gate block and a reverse launch reading it back (a read-modify-write of the whole block
+// whose load stalled the reverse epilogue).  Same directed rounding, same per-term arithmetic
+// order, so the result equals max(forward launch, reverse launch) bit for bit.  With Dp <= 32
+// (n <= 256) the single chunk is staged once (one 110 KB stage: 2 CTAs per SM).
+struct SymStage {
+    float X[TC][KP], X2[TC][KP];    // candidate segment sums: lo, hi            (forward)
+    float XR[TC][KP], XR2[TC][KP];  // candidate envelope sums: P(U(x)) hi, P(L(x)) lo (reverse)
+    float U[TQ][KP], L[TQ][KP];     // query envelope sums: P(U(y)) hi, P(L(y)) lo   (forward)
+    float UR[TQ][KP], LR[TQ][KP];   // query sums: P(y) lo, hi                       (reverse)
+};
+
+template <int P, bool VEC, bool ROOTED>
+__global__ void __launch_bounds__(NT, 2)
+gate_sym_kernel(const float *__restrict__ Uhi, const float *__restrict__ Llo, const float *__restrict__ Ylo,
+                const float *__restrict__ Yhi, const float *__restrict__ Xlo, const float *__restrict__ Xhi,
+                const float *__restrict__ Uxhi, const float *__restrict__ Lxlo, int64_t Q, int64_t N, int n,
+                void *__restrict__ out, int64_t ldo, int nqt) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    SymStage *st = reinterpret_cast<SymStage *>(smraw);
+    const int64_t tile = blockIdx.x;
+    const int64_t q0 = (tile % nqt) * TQ;
+    const int64_t c0 = (tile / nqt) * TC;
+    const int tid = threadIdx.x;
+    const int cg = tid & 15, qg = tid >> 4;
+    float acc[4][8], accr[4][8];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { acc[r][j] = 0.f; accr[r][j] = 0.f; }
+    const int nchunks = (n + KC - 1) / KC;
+    const int nbuf = nchunks > 1 ? 2 : 1;
+    auto stage = [&](SymStage &S, int k0) {
+        stage_rows<TC, VEC>(S.X, Xlo, c0, N, n, k0);
+        stage_rows<TC, VEC>(S.X2, Xhi, c0, N, n, k0);
+        stage_rows<TC, VEC>(S.XR, Uxhi, c0, N, n, k0);
+        stage_rows<TC, VEC>(S.XR2, Lxlo, c0, N, n, k0);
+        stage_rows<TQ, VEC>(S.U, Uhi, q0, Q, n, k0);
+        stage_rows<TQ, VEC>(S.L, Llo, q0, Q, n, k0);
+        stage_rows<TQ, VEC>(S.UR, Ylo, q0, Q, n, k0);
+        stage_rows<TQ, VEC>(S.LR, Yhi, q0, Q, n, k0);
+    };
+    stage(st[0], 0);
+    cp_commit();
+    for (int ch = 0; ch < nchunks; ++ch) {
+        if (ch + 1 < nchunks) stage(st[(ch + 1) % nbuf], (ch + 1) * KC);
+        cp_commit();
+        cp_wait<1>();
+        __syncthreads();
+        const SymStage &S = st[ch % nbuf];
+#pragma unroll 2
+        for (int k = 0; k < KC; k += 4) {
+            {   // forward: d = max(Xlo - Uhi, Llo - Xhi, 0)
+                float4 uv[4], lv[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    uv[r] = *reinterpret_cast<const float4 *>(&S.U[4 * qg + r][k]);
+                    lv[r] = *reinterpret_cast<const float4 *>(&S.L[4 * qg + r][k]);
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float4 xv = *reinterpret_cast<const float4 *>(&S.X[cg + 16 * j][k]);
+                    const float4 xw = *reinterpret_cast<const float4 *>(&S.X2[cg + 16 * j][k]);
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        float t = acc[r][j];
+                        t = lb_elem2<P, true>(t, make_float2(xv.x, xv.y), make_float2(xw.x, xw.y),
+                                              make_float2(uv[r].x, uv[r].y), make_float2(lv[r].x, lv[r].y));
+                        t = lb_elem2<P, true>(t, make_float2(xv.z, xv.w), make_float2(xw.z, xw.w),
+                                              make_float2(uv[r].z, uv[r].w), make_float2(lv[r].z, lv[r].w));
+                        acc[r][j] = t;
+                    }
+                }
+            }
+            {   // reverse: d = max(Ylo - Uxhi, Lxlo - Yhi, 0)
+                float4 yl[4], yh[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    yl[r] = *reinterpret_cast<const float4 *>(&S.UR[4 * qg + r][k]);
+                    yh[r] = *reinterpret_cast<const float4 *>(&S.LR[4 * qg + r][k]);
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float4 ux = *reinterpret_cast<const float4 *>(&S.XR[cg + 16 * j][k]);
+                    const float4 lx = *reinterpret_cast<const float4 *>(&S.XR2[cg + 16 * j][k]);
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        float t = accr[r][j];
+                        t = lb_elem2<P, true>(t, make_float2(yl[r].x, yl[r].y), make_float2(yh[r].x, yh[r].y),
+                                              make_float2(ux.x, ux.y), make_float2(lx.x, lx.y));
+                        t = lb_elem2<P, true>(t, make_float2(yl[r].z, yl[r].w), make_float2(yh[r].z, yh[r].w),
+                                              make_float2(ux.z, ux.w), make_float2(lx.z, lx.w));
+                        accr[r][j] = t;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int64_t q = q0 + 4 * qg + r;
+        if (q >= Q) continue;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int64_t c = c0 + cg + 16 * j;
+            if (c >= N) continue;
+            float v = fmaxf(acc[r][j], accr[r][j]);  // max of two lower bounds (exact)
+            if constexpr (P == 2) v = __fmul_rd(v, 1.0f / kSeg);
+            if constexpr (ROOTED) {
+                if constexpr (P == 2) v = __fsqrt_rd(v);
+                reinterpret_cast<float *>(out)[q * ldo + c] = v;
+            } else {
+                reinterpret_cast<__half *>(out)[q * ldo + c] = __float2half_rd(v);
+            }
+        }
+    }
+}
+
+template <int P, bool VEC, bool ROOTED>
+int launch_sym_t(const float *Uhi, const float *Llo, const float *Ylo, const float *Yhi, const float *Xlo,
+                 const float *Xhi, const float *Uxhi, const float *Lxlo, int64_t Q, int64_t N, int Dp, void *out,
+                 int64_t ldo, cudaStream_t st) {
+    const int nchunks = (Dp + KC - 1) / KC;
+    const size_t smem = (nchunks > 1 ? 2 : 1) * sizeof(SymStage);
+    auto k = gate_sym_kernel<P, VEC, ROOTED>;
+    DTWLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t nqt = ceil_div(Q, TQ), nct = ceil_div(N, TC);
+    const int64_t tiles = nqt * nct;
+    if (tiles > 0x7fffffffLL) {
+        set_error(DTWLB_EINVAL, "bound pass: problem too large (%lld tiles)", (long long)tiles);
+        return DTWLB_EINVAL;
+    }
+    k<<<(unsigned)tiles, NT, smem, st>>>(Uhi, Llo, Ylo, Yhi, Xlo, Xhi, Uxhi, Lxlo, Q, N, Dp, out, ldo, (int)nqt);
+    DTWLB_LAUNCH_CHECK();
+    return DTWLB_OK;
+}
+
 // ---------------------------------------------------------------- piecewise sums
 // One thread per (row, segment): directed fp64 sums of the s samples, then a directed
 // conversion to fp32 (the interval [lo, hi] contains the exact sum).
@@ -334,6 +476,17 @@ int launch_paa_bound(const float *Uhi, const float *Llo, const float *Xlo, const
 int launch_paa_bound_rev(const float *Ylo, const float *Yhi, const float *Uxhi, const float *Lxlo, int64_t Q,
                          int64_t N, int n, int p, bool rooted, void *out, int64_t ldo, cudaStream_t st) {
     return launch_tile<true, true>(Ylo, Yhi, Uxhi, Lxlo, Q, N, paa_pitch(n), p, rooted, out, ldo, st);
+}
+
+int launch_paa_bound_sym(const float *Uhi, const float *Llo, const float *Ylo, const float *Yhi, const float *Xlo,
+                         const float *Xhi, const float *Uxhi, const float *Lxlo, int64_t Q, int64_t N, int n, int p,
+                         bool rooted, void *out, int64_t ldo, cudaStream_t st) {
+    if (Q == 0 || N == 0) return DTWLB_OK;
+    const int Dp = paa_pitch(n);  // a multiple of 4: 16-byte rows
+#define DTWLB_S(P_, R_) return launch_sym_t<P_, true, R_>(Uhi, Llo, Ylo, Yhi, Xlo, Xhi, Uxhi, Lxlo, Q, N, Dp, out, ldo, st)
+    if (p == 1) { if (rooted) DTWLB_S(1, true); else DTWLB_S(1, false); }
+    else { if (rooted) DTWLB_S(2, true); else DTWLB_S(2, false); }
+#undef DTWLB_S
 }
 
 int launch_keogh(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n, int p,

@@ -41,6 +41,10 @@ int launch_paa_bound(const float *Uhi, const float *Llo, const float *Xlo, const
 // envelope sums [N][Dp] (launch_paa_env_sums of U(x), L(x)).  Same out types as above.
 int launch_paa_bound_rev(const float *Ylo, const float *Yhi, const float *Uxhi, const float *Lxlo, int64_t Q,
                          int64_t N, int n, int p, bool rooted, void *out, int64_t ldo, cudaStream_t st);
+// Both terms in one pass: out[q][c] = max(forward, reverse) (same rounding as the two launches above).
+int launch_paa_bound_sym(const float *Uhi, const float *Llo, const float *Ylo, const float *Yhi, const float *Xlo,
+                         const float *Xhi, const float *Uxhi, const float *Lxlo, int64_t Q, int64_t N, int n, int p,
+                         bool rooted, void *out, int64_t ldo, cudaStream_t st);
 
 // LB_Keogh^p of Q <= kStreamMaxQ queries against every database row in ONE streaming pass
 // (stream.cu; TMA bulk copies, thread per candidate): out[q*ldo + c] = beta1 (rooted if `rooted`).

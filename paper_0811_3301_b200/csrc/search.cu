@@ -694,12 +694,20 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         //      LB_Keogh then runs on its survivors inside the survivor pass), or a2 itself ----
         if (stats) ev0 = rec();
         if (prefilter) {
-            DTWLB_TRY(launch_paa_bound(qpaa + qb0 * Dp, qpaa + (size_t)Q * Dp + qb0 * Dp, xpaa,
-                                       xpaa + (size_t)N * Dp, qn, N, n, p, false, beta1, ldb, st));
-            // symmetric gate: max with the reverse piecewise-sum bound (reading c20)
+            // symmetric gate: max of the forward and the reverse piecewise-sum bounds (readings c18,
+            // c20), one fused tile pass (DTWLB_GATE_SPLIT=1: two launches, the second max-combining)
+            static const bool gate_split = [] { const char *e = getenv("DTWLB_GATE_SPLIT"); return e && atoi(e); }();
             const float *yp = rpaa + (size_t)2 * N * Dp;
-            DTWLB_TRY(launch_paa_bound_rev(yp + qb0 * Dp, yp + (size_t)Q * Dp + qb0 * Dp, rpaa,
-                                           rpaa + (size_t)N * Dp, qn, N, n, p, false, beta1, ldb, st));
+            if (gate_split) {
+                DTWLB_TRY(launch_paa_bound(qpaa + qb0 * Dp, qpaa + (size_t)Q * Dp + qb0 * Dp, xpaa,
+                                           xpaa + (size_t)N * Dp, qn, N, n, p, false, beta1, ldb, st));
+                DTWLB_TRY(launch_paa_bound_rev(yp + qb0 * Dp, yp + (size_t)Q * Dp + qb0 * Dp, rpaa,
+                                               rpaa + (size_t)N * Dp, qn, N, n, p, false, beta1, ldb, st));
+            } else {
+                DTWLB_TRY(launch_paa_bound_sym(qpaa + qb0 * Dp, qpaa + (size_t)Q * Dp + qb0 * Dp, yp + qb0 * Dp,
+                                               yp + (size_t)Q * Dp + qb0 * Dp, xpaa, xpaa + (size_t)N * Dp, rpaa,
+                                               rpaa + (size_t)N * Dp, qn, N, n, p, false, beta1, ldb, st));
+            }
         } else if (stream_mode)
             DTWLB_TRY(launch_keogh_stream(U + qb0 * n, L + qb0 * n, db, qn, N, n, p, false, beta1, ldb, st));
         else
