@@ -111,11 +111,12 @@ int lb_improved(const float *q, const float *q_env, const float *db, int64_t Q, 
 /* Banded DTW_p of row pairs (section "Dynamic Time Warping"):
  *   out[r] = DTW_p(x[r], y[r]) with the band |i-j| <= w, rooted.
  * p = 0 encodes p = infinity: DTW_inf, the max instead of the sum along the path
- * (P:211-214); exact in fp32 (only |x_i - y_j| rounds).  w >= n-1 is the
- * unconstrained DTW (Appendix B workload).
+ * (P:211-214); exact in fp32 (only |x_i - y_j| rounds).  p = 4 is DTW_4, the third
+ * member of the Appendix C comparison.  w >= n-1 is the unconstrained DTW
+ * (Appendix B workload).
  * x, y: device [count][n]; out: device [count].
- * Errors: EINVAL (sizes, NULL, n < 1, w < 0, count > 2^31 - 1), EUNSUPPORTED (p not 0, 1
- * or 2). */
+ * Errors: EINVAL (sizes, NULL, n < 1, w < 0, count > 2^31 - 1), EUNSUPPORTED (p not 0, 1,
+ * 2 or 4). */
 int dtw_band(const float *x, const float *y, int32_t n, int32_t w, int32_t p, float *out,
              int64_t count, void *stream);
 

@@ -233,7 +233,8 @@ int dtw_band(const float *x, const float *y, int32_t n, int32_t w, int32_t p, fl
     CHECK_ARG(w >= 0, "dtw_band: w = %d < 0", w);
     CHECK_ARG(count >= 0, "dtw_band: count < 0");
     CHECK_ARG(count <= 0x7fffffffLL, "dtw_band: count = %lld > 2^31 - 1 (split the call)", (long long)count);
-    if (p != 0) DTWLB_TRY(check_p(p));  // p = 0 encodes DTW_inf, dtw_band only
+    if (p != 0 && p != 4) DTWLB_TRY(check_p(p));  // p = 0 encodes DTW_inf; p = 4: DTW_4
+                                                  // (Appendix C); both dtw_band only
     if (count == 0) return DTWLB_OK;
     CHECK_ARG(x && y && out, "dtw_band: NULL pointer");
     DTWLB_TRY(require_device());

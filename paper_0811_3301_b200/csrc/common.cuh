@@ -81,6 +81,7 @@ __device__ __forceinline__ float accp(float acc, float d) {
 template <int P>
 __device__ __forceinline__ float rootp(float v) {
     if constexpr (P == 2) return sqrtf(v);
+    else if constexpr (P == 4) return sqrtf(sqrtf(v));  // (dtw_band's DTW_4, Appendix C)
     else return v;  // p = 1, and p = 0 (DTW_inf, a max: no root)
 }
 

@@ -31,6 +31,7 @@ template <int P>
 __device__ __forceinline__ float cell(float m, float t) {
     if constexpr (P == 1) return m + fabsf(t);
     else if constexpr (P == 0) return fmaxf(m, fabsf(t));  // DTW_inf: max, exact
+    else if constexpr (P == 4) { const float t2 = t * t; return fmaf(t2, t2, m); }  // DTW_4
     else return fmaf(t, t, m);
 }
 
@@ -772,6 +773,13 @@ int launch_dtw(const DtwArgs &a, int p, bool walk, cudaStream_t st) {
         }
         return launch_dtw_p<0, false>(a, st);
     }
+    if (p == 4) {  // DTW_4: pairs mode only (dtw_band)
+        if (walk) {
+            set_error(DTWLB_EUNSUPPORTED, "nn_search: p = 4 unsupported");
+            return DTWLB_EUNSUPPORTED;
+        }
+        return launch_dtw_p<4, false>(a, st);
+    }
     if (p == 1) return walk ? launch_dtw_p<1, true>(a, st) : launch_dtw_p<1, false>(a, st);
     return walk ? launch_dtw_p<2, true>(a, st) : launch_dtw_p<2, false>(a, st);
 }
@@ -793,8 +801,15 @@ int launch_dtw_generic(const DtwArgs &a, const float *yraw, float *scratch, int 
         DTWLB_CUDA(cudaFuncSetAttribute(dtw_generic_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         DTWLB_CUDA(cudaFuncSetAttribute(dtw_generic_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         DTWLB_CUDA(cudaFuncSetAttribute(dtw_generic_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        DTWLB_CUDA(cudaFuncSetAttribute(dtw_generic_kernel<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
-    if (p == 0) {
+    if (p == 4) {
+        if (walk) {
+            set_error(DTWLB_EUNSUPPORTED, "nn_search: p = 4 unsupported");
+            return DTWLB_EUNSUPPORTED;
+        }
+        dtw_generic_kernel<4, false><<<(unsigned)grid, 128, smem, st>>>(a, yraw, scratch, pitch);
+    } else if (p == 0) {
         if (walk) {
             set_error(DTWLB_EUNSUPPORTED, "nn_search: p = infinity unsupported");
             return DTWLB_EUNSUPPORTED;

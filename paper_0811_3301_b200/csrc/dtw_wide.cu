@@ -38,6 +38,7 @@ template <int P>
 __device__ __forceinline__ float wcell(float m, float t) {
     if constexpr (P == 1) return m + fabsf(t);
     else if constexpr (P == 0) return fmaxf(m, fabsf(t));  // DTW_inf
+    else if constexpr (P == 4) { const float t2 = t * t; return fmaf(t2, t2, m); }  // DTW_4
     else return fmaf(t, t, m);
 }
 
@@ -395,6 +396,13 @@ int launch_dtw_wide(const DtwArgs &a, const float *yp, int LPW, int padL, int p,
             return DTWLB_EUNSUPPORTED;
         }
         return launch_wide_p<0, false>(a, yp, LPW, padL, mode, S, st);
+    }
+    if (p == 4) {
+        if (walk) {
+            set_error(DTWLB_EUNSUPPORTED, "nn_search: p = 4 unsupported");
+            return DTWLB_EUNSUPPORTED;
+        }
+        return launch_wide_p<4, false>(a, yp, LPW, padL, mode, S, st);
     }
     if (p == 1) return walk ? launch_wide_p<1, true>(a, yp, LPW, padL, mode, S, st)
                             : launch_wide_p<1, false>(a, yp, LPW, padL, mode, S, st);

@@ -53,6 +53,9 @@ def test_argument_validation_precedes_device(lib):
     assert lib.lb_piecewise_sym(null, null, null, 1, 1, 8, 1, 3, null, null) == 2   # p = 3 unsupported
     assert lib.lb_piecewise_sym(null, null, null, 1, 1, 8, -1, 1, null, null) == 1  # w < 0
     assert lib.dtw_band(null, null, 8, 2, 3, null, 1, null) == 2          # p = 3 unsupported
+    assert lib.dtw_band(null, null, 8, 2, 5, null, 1, null) == 2          # p = 5 unsupported
+    assert lib.dtw_band(null, null, 8, 2, 4, null, 1, null) == 1          # p = 4 (DTW_4) ok: NULL -> EINVAL
+    assert lib.nn_search(null, 1, null, 4, 8, 1, 4, 1, null, null, None, None, null) == 2   # p = 4: dtw_band only
     assert lib.dtw_band(null, null, 8, 2, 0, null, 1, null) == 1          # p = 0 (inf) ok, NULL pointers
     assert lib.nn_search(null, 1, null, 4, 8, 1, 0, 1, null, null, None, None, null) == 2   # p = inf
     assert lib.nn_search(null, 1, null, 0, 8, 1, 1, 1, null, null, None, None, null) == 1   # N = 0

@@ -243,3 +243,18 @@ def test_error_model_on_gpu(cuda_ok):
     with pytest.raises(DtwlbError) as e:
         dtw_band(dev(np.zeros((2, 4))), dev(np.zeros((2, 4))), -1, 1)
     assert e.value.name == "EINVAL"
+
+
+@pytest.mark.parametrize("n,w", [(4, 1), (128, 12), (256, 25), (300, 64), (150, 100), (100, 99), (400, 150)])
+def test_dtw_band_p4(cuda_ok, n, w):
+    """DTW_4 (Appendix C compares DTW_1, DTW_2, DTW_4 and DTW_inf) through dtw_band:
+    the register-band kernel (w <= 64), the four-lanes-per-pair kernels (w = 100; unconstrained
+    n = 100) and the generic one (w = 150) against the fp64 oracle (generic p)."""
+    from paper_0811_3301_b200 import dtw_band
+    count = 120
+    x, y = series(count, n), series(count, n)
+    x[0] = y[0]
+    out = dtw_band(dev(x), dev(y), w, 4).cpu().numpy()
+    ref = np.array([oracle.dtw(x[r], y[r], w, 4) for r in range(count)])
+    close(out, ref, 1e-4, 1e-6)
+    assert out[0] == 0.0
