@@ -188,7 +188,8 @@ def run_ours(args, cfg):
     dev = torch.device("cuda", local if ws > 1 else 0)
     torch.cuda.set_device(dev)
     st = torch.cuda.current_stream()
-    lo, hi = shard_range(cfg.N, ws, rank)
+    qshard = args.shard == "queries" and ws > 1  # comparison mode: replicated database, queries split
+    lo, hi = shard_range(cfg.N, ws, rank) if not qshard else (0, cfg.N)
     qs_h, _ = datagen.make(cfg, N=0)
     db_h = datagen.series(cfg.family, hi - lo, cfg.n, cfg.seed, datagen.ROLE_DB, cfg.znorm, start=lo)
     qs = torch.from_numpy(qs_h).to(dev)
@@ -221,9 +222,14 @@ def run_ours(args, cfg):
         last["st"] = st_
         return i_, d2
 
+    from paper_0811_3301_b200.sharded import query_sharded_nn_search
+
     def step(stats=False):
-        sharded_nn_search(qs, db, lo, cfg.w, cfg.p, k, search=search, merge=B.nn_merge, out_local=(idx, dst),
-                          gather_bufs=gbufs)
+        if qshard:
+            query_sharded_nn_search(qs, db, cfg.w, cfg.p, k, search=search)
+        else:
+            sharded_nn_search(qs, db, lo, cfg.w, cfg.p, k, search=search, merge=B.nn_merge, out_local=(idx, dst),
+                              gather_bufs=gbufs)
         return last["st"] if stats else None
 
     def barrier():
@@ -266,8 +272,11 @@ def run_ours(args, cfg):
         else:  # H2D of the shard + queries, sharded search (exchange, all-gather, merge), D2H
             q_dev.copy_(qs_pin, non_blocking=True)
             d_dev.copy_(db_pin, non_blocking=True)
-            gi, gd = sharded_nn_search(q_dev, d_dev, lo, cfg.w, cfg.p, k, search=search, merge=B.nn_merge,
-                                       out_local=(idx, dst), gather_bufs=gbufs)
+            if qshard:
+                gi, gd = query_sharded_nn_search(q_dev, d_dev, cfg.w, cfg.p, k, search=search)
+            else:
+                gi, gd = sharded_nn_search(q_dev, d_dev, lo, cfg.w, cfg.p, k, search=search, merge=B.nn_merge,
+                                           out_local=(idx, dst), gather_bufs=gbufs)
             h_idx.copy_(gi, non_blocking=True)
             h_dst.copy_(gd, non_blocking=True)
 
@@ -316,7 +325,7 @@ def run_ours(args, cfg):
         # ALU issue peak: SMs x 4 schedulers x 32 lanes (one warp-instruction per scheduler per
         # clock = 128 lane-slots per SM per clock) x the max SM clock (guide unit counts)
         peak = n_sm * 128 * sm_clock * 1e6 / 1e12
-        Nr = cfg.N // ws  # rows per rank
+        pairs_rank = cfg.Q * cfg.N / ws  # (query, candidate) pairs per rank, either sharding
         kern = {}
         # Minimal algorithmic issue slots per unit (sm_100a SASS):
         #  bound element (LB_Keogh, piecewise-sum): FADD2 (two elements' two subtractions, so 1 per
@@ -337,7 +346,7 @@ def run_ours(args, cfg):
                                              "in one pass)" if pf and not split else
                                              "keogh_tile_kernel (" + ("piecewise-sum gate, two launches"
                                                                       if pf else "LB_Keogh") + ")"),
-                                  "bound": "alu", "ms": keogh_ms, "work": 3.0 * cfg.Q * Nr * elems / 1e12,
+                                  "bound": "alu", "ms": keogh_ms, "work": 3.0 * pairs_rank * elems / 1e12,
                                   "unit": "Tlane-op/s", "peak": peak, "launches": 2 if pf and split else 1,
                                   "note": f"3 slots per pair-element, {elems} elements per pair"}
         if surv_ms > 0:
@@ -384,7 +393,8 @@ def run_ours(args, cfg):
             "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": cfg.name, "Q": cfg.Q, "N": cfg.N, "n": cfg.n, "w": cfg.w, "p": cfg.p,
-                       "k": cfg.k, "family": cfg.family, "parallelism": f"db-shard{ws}",
+                       "k": cfg.k, "family": cfg.family,
+                       "parallelism": f"query-shard{ws}" if qshard else f"db-shard{ws}",
                        "mode": ("stream" if stream_mode else ("prefilter" if pf else "alg3")) +
                                ("+keogh_only" if args.keogh_only else ""),
                        "db_index": ({"prebuilt": True, "build_ms": index_ms} if args.db_index else None),
@@ -417,7 +427,7 @@ def run_ours(args, cfg):
                             for kn, v in kern.items()}},
             "e2e": {"value": pairs / (e2e_ms * 1e-3), "unit": "pairs/s",
                     # whole job: every rank copies the queries and its shard in, its result out
-                    "h2d_bytes_per_step": int(qs_h.nbytes * ws + cfg.N * cfg.n * 4),
+                    "h2d_bytes_per_step": int(qs_h.nbytes * ws + cfg.N * cfg.n * 4 * (ws if qshard else 1)),
                     "d2h_bytes_per_step": int(cfg.Q * k * 12 * ws)},
             "gpu_launches": launches * args.steps + (0 if ws == 1 else args.steps),
             "clocks": clocks,
@@ -442,6 +452,9 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--keogh-only", action="store_true",
                     help="Alg. 2 (LB_Keogh then DTW, no LB_Improved pass): the paper's comparison point")
+    ap.add_argument("--shard", default="db", choices=["db", "queries"],
+                    help="N > 1: shard the database (default, SURVEY 8(e)) or the queries (comparison "
+                         "mode: replicated database, no collective during the search)")
     ap.add_argument("--no-stream", action="store_true",
                     help="Q <= 8: the tiled bound pass instead of the streaming one (DTWLB_NO_STREAM)")
     ap.add_argument("--db-index", action="store_true",

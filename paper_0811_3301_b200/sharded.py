@@ -105,3 +105,46 @@ def sharded_nn_search(queries: torch.Tensor, db_shard: torch.Tensor, shard_lo: i
     dist.all_gather_into_tensor(g_dst, dst.contiguous(), group=group)
     return merge(g_idx.view(world, Q, k), g_dst.view(world, Q, k))
 
+
+
+def query_shard_range(Q: int, world: int, rank: int):
+    """Contiguous, balanced queries [lo, hi) of rank `rank` in the query-sharded mode."""
+    return rank * Q // world, (rank + 1) * Q // world
+
+
+def query_sharded_nn_search(queries: torch.Tensor, db: torch.Tensor, w: int, p: int, k: int,
+                            group: Optional[dist.ProcessGroup] = None, search: Optional[Callable] = None,
+                            **kw):
+    """The comparison mode of SURVEY 8(e): the whole database is replicated on every rank and the
+    QUERIES are split; each rank searches its queries against all N rows with no collective during
+    the search, then the [Q][k] results are all-gathered so that every rank holds the full answer.
+    Exact for the same reason as the single-GPU search (every query sees the whole set S).
+    Per-rank work is Q/G queries x N rows, the same as the database-sharded mode's Q x N/G, but each
+    rank streams the full database (N n 4 bytes of HBM per query block) and needs it resident."""
+    if search is None:
+        from . import binding
+        search = binding.nn_search
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    Q = queries.shape[0]
+    lo, hi = query_shard_range(Q, world, rank)
+    dev = queries.device
+    idx, dst = search(queries[lo:hi], db, w, p, k, **kw)
+    if world == 1:
+        return idx, dst
+    # ranks may hold different query counts: pad to the largest, gather, then drop the padding
+    cnt = max(query_shard_range(Q, world, r)[1] - query_shard_range(Q, world, r)[0] for r in range(world))
+    pi = torch.full((cnt, k), -1, dtype=torch.int64, device=dev)
+    pd = torch.full((cnt, k), float("inf"), dtype=torch.float32, device=dev)
+    pi[:hi - lo] = idx
+    pd[:hi - lo] = dst
+    gi = torch.empty((world * cnt, k), dtype=torch.int64, device=dev)
+    gd = torch.empty((world * cnt, k), dtype=torch.float32, device=dev)
+    dist.all_gather_into_tensor(gi, pi, group=group)
+    dist.all_gather_into_tensor(gd, pd, group=group)
+    parts_i, parts_d = [], []
+    for r in range(world):
+        a, b = query_shard_range(Q, world, r)
+        parts_i.append(gi[r * cnt:r * cnt + (b - a)])
+        parts_d.append(gd[r * cnt:r * cnt + (b - a)])
+    return torch.cat(parts_i), torch.cat(parts_d)

@@ -265,3 +265,54 @@ def test_unbalanced_shard_smaller_than_k():
     kth = (o_dst[:, k - 1].astype(np.float64) ** cfg.p)
     for t in res[1][3]:
         assert np.all(t >= kth * (1 - 1e-6))
+
+
+def _worker_qshard(rank, world, port, Q, N, k, result_q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_0811_3301_b200.sharded import query_sharded_nn_search
+        cfg = datagen.CONFIGS["C2p1"]
+        qs, db = datagen.make(cfg, Q=Q, N=N)
+        calls = []
+
+        def search(queries, dbt, w, p, kk, **kw):
+            calls.append(queries.shape[0])
+            return _oracle_search(queries, dbt, w, p, kk)
+
+        idx, dst = query_sharded_nn_search(torch.from_numpy(qs), torch.from_numpy(db), cfg.w, cfg.p, k,
+                                           search=search)
+        result_q.put((rank, idx.numpy(), dst.numpy(), calls))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:
+        result_q.put((rank, None, repr(e), None))
+        raise
+
+
+@pytest.mark.parametrize("Q", [7, 2])
+def test_query_sharded_equals_global(Q):
+    """Query-sharded comparison mode: replicated database, queries split over the
+    ranks (7 = 3 + 4; 2 = 1 + 1), results all-gathered: every rank returns the brute-force k-NN."""
+    world, N, k = 2, 150, 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_qshard, args=(r, world, port, Q, N, k, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    res.sort(key=lambda r: r[0])
+    for r in res:
+        assert r[1] is not None, r[2]
+    cfg = datagen.CONFIGS["C2p1"]
+    qs, db = datagen.make(cfg, Q=Q, N=N)
+    o_idx, o_dst = oracle.nn_brute(qs, db, cfg.w, cfg.p, k)
+    for rank, idx, dst, calls in res:
+        assert np.array_equal(idx, o_idx)
+        assert np.allclose(dst, o_dst, rtol=1e-6)
+        assert calls == [Q // 2 if rank == 0 else Q - Q // 2]
