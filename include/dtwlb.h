@@ -174,6 +174,7 @@ typedef struct nn_stats {
                                     LB_Improved on sparse pairs), part of ms_improved   */
     double ms_dtw_kernel;        /* device time of the banded-DTW kernel launches of the
                                     walk, part of ms_dtw                                */
+    int64_t survivor_entries;    /* (query, 64-candidate tile) entries the survivor kernel walked */
 } nn_stats;
 
 /* Exact k-nearest-neighbour search under banded DTW_p: for each query y_q,

@@ -67,7 +67,7 @@ class NnStats(ctypes.Structure):
                 ("range1_dtw", ctypes.c_int64), ("range1_cells", ctypes.c_int64), ("walk_rounds", ctypes.c_int64),
                 ("prefilter_evaluated", ctypes.c_int64), ("prefilter_segment", ctypes.c_int32),
                 ("reserved_", ctypes.c_int32), ("ms_survivor_kernel", ctypes.c_double),
-                ("ms_dtw_kernel", ctypes.c_double)]
+                ("ms_dtw_kernel", ctypes.c_double), ("survivor_entries", ctypes.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -432,6 +432,7 @@ improved_kernel(ImprovedArgs a, int Ct) {
     if (c0 >= a.N) return;
     const int cnt = a.tile_cnt[tile];
     if (cnt == 0) return;
+    if (a.n_entries && sub == 0 && threadIdx.x == 0) atomicAdd(a.n_entries, (unsigned long long)cnt);
     const int ct = (int)((a.N - c0) < Ct ? (a.N - c0) : Ct);
     const int n = a.n;
     const unsigned long long ctmask = Ct == 64 ? ~0ull : ((1ull << Ct) - 1);

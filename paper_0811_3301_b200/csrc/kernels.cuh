@@ -83,6 +83,7 @@ struct ImprovedArgs {
     int64_t ldd;
     unsigned long long *n_eval;        // stats: LB_Improved (phase-2) evaluations (may be NULL)
     unsigned long long *n_eval_keogh;  // stats: in-kernel LB_Keogh evaluations (may be NULL)
+    unsigned long long *n_entries;     // stats: (query, 64-candidate tile) entries walked (may be NULL)
     // scratch: per 64-candidate tile, the list of (query, survivor mask) entries
     unsigned long long *tile_m;    // [ceil(N/64)][Qb]
     int *tile_q;                   // [ceil(N/64)][Qb]

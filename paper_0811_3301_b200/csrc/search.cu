@@ -760,6 +760,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 ia.cap = cap;
                 ia.list_len = s.len;
                 ia.n_eval = s.stat + 0;
+                ia.n_entries = s.stat + 5;
                 if (stats) { ev_s0 = new_ev(); ev_s1 = new_ev(); ia.ev0 = ev_s0; ia.ev1 = ev_s1; }
                 improved_scratch_bind(ia, imp_scratch);
                 DTWLB_TRY(launch_improved(ia, p, keogh_only, false, st));
@@ -970,6 +971,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         stats->range1_dtw = (int64_t)r1[1];
         stats->range1_cells = (int64_t)r1[2];
         stats->walk_rounds = walk_rounds;
+        stats->survivor_entries = (int64_t)h[5];
     }
     return DTWLB_OK;
 }
