@@ -292,6 +292,35 @@ def run_ours(args, cfg):
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
 
+    # ---- work efficiency (after the timed region, 1 GPU): the cascade's LB_Improved and DTW
+    # evaluations per query against their order-independent minima on a query sample, from the
+    # library's own dense bounds and this run's final k-th distances tau_q: #{LB_Keogh <= tau(1+eps)}
+    # (every such pair must reach LB_Improved) and #{LB_Improved <= tau(1+eps)} (must reach DTW)
+    work_eff = None
+    if ws == 1 and not args.keogh_only and not qshard:
+        try:
+            S = min(cfg.Q, 64)
+            rows = torch.linspace(0, cfg.Q - 1, S).round().long().to(dev)
+            qsamp = qs.index_select(0, rows).contiguous()
+            U_, L_ = B.lb_envelope(qsamp, cfg.w)
+            env_ = torch.stack([U_, L_]).contiguous()
+            tau = dst.index_select(0, rows)[:, k - 1:k].double() * (1.0 + 1e-3) ** (1.0 / cfg.p)
+            kb = B.lb_keogh(env_, db, cfg.p)
+            n_keogh = int((kb.double() <= tau).sum().item())
+            del kb
+            ib = B.lb_improved(qsamp, env_, db, cfg.w, cfg.p)
+            n_imp = int((ib.double() <= tau).sum().item())
+            del ib
+            st1 = stats_all[-1]
+            work_eff = {"sample_queries": S,
+                        "min_improved_per_query": n_keogh / S, "min_dtw_per_query": n_imp / S,
+                        "improved_per_query": st1["improved_evaluated"] / cfg.Q,
+                        "dtw_per_query": st1["dtw_evaluated"] / cfg.Q,
+                        "improved_ratio": (st1["improved_evaluated"] / cfg.Q) / max(n_keogh / S, 1e-9),
+                        "dtw_ratio": (st1["dtw_evaluated"] / cfg.Q) / max(n_imp / S, 1e-9)}
+        except Exception as e:  # (a reporting extra: never fails the bench)
+            work_eff = {"error": repr(e)[:200]}
+
     # ---- aggregate counters over ranks ----
     def tot(key):
         v = torch.tensor([float(sum(s[key] for s in stats_all) / len(stats_all))], device=dev,
@@ -441,6 +470,7 @@ def run_ours(args, cfg):
                     # whole job: every rank copies the queries and its shard in, its result out
                     "h2d_bytes_per_step": int(qs_h.nbytes * ws + cfg.N * cfg.n * 4 * (ws if qshard else 1)),
                     "d2h_bytes_per_step": int(cfg.Q * k * 12 * ws)},
+            "work_efficiency": work_eff,
             "gpu_launches": launches * args.steps + (0 if ws == 1 else args.steps),
             "clocks": clocks,
         }
