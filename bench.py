@@ -246,11 +246,16 @@ def run_ours(args, cfg):
         time.sleep(0.5)  # let nvidia-smi start polling before the timed region (its start-up stalls the GPU)
         barrier()
         ev0.record(st)
+        step_ev = []
         for _ in range(args.steps):
             stats_all.append(step(stats=True))
+            step_ev.append(torch.cuda.Event(enable_timing=True))
+            step_ev[-1].record(st)
         ev1.record(st)
         barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
+    # per-step device times (run-to-run diagnostics: one slow step shows up here)
+    step_ms = [round((step_ev[i - 1] if i else ev0).elapsed_time(step_ev[i]), 3) for i in range(args.steps)]
     ms_t = torch.tensor([ms], device=dev)
     if ws > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -473,6 +478,7 @@ def run_ours(args, cfg):
             "work_efficiency": work_eff,
             "gpu_launches": launches * args.steps + (0 if ws == 1 else args.steps),
             "clocks": clocks,
+            "step_ms": step_ms,
         }
         if ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = oracle_sample(cfg, qs_h, db_h, budget_s=args.cpu_budget)

@@ -114,6 +114,10 @@ __device__ __forceinline__ void walk_result(const DtwArgs &a, int64_t q, unsigne
     int *lock = a.topk_lock + q;
     bool done = false;
     while (!done) {
+        // re-test against the threshold while waiting: in a walk's first round (tau = +inf) a
+        // query's ~128 completed pairs contend for its lock, and once k of them are in, most
+        // of the rest can no longer enter -- they leave without taking the lock
+        if (!(__uint_as_float((uint32_t)(key >> 32)) <= *thr)) return;
         if (atomicCAS(lock, 0, 1) == 0) {
             __threadfence();
             if (key < tk[a.k - 1]) {

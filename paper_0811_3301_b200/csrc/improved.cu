@@ -516,6 +516,12 @@ improved_kernel(ImprovedArgs a, int Ct) {
     QRegs<NV, B1X, KO> cur, nxt;
     int64_t qe = eq[e];
     load_p1<EPL, B1X, KO>(cur, a, qe, c0t, lane);
+    // one CTA per tile: the (query, mask) of the entry after next is loaded one iteration
+    // ahead, so the next entry's query-row loads do not wait on its index load
+    constexpr bool IDX_AHEAD = ONE_CTA;
+    int q_ah = 0;
+    unsigned long long m_ah = 0;
+    if (IDX_AHEAD && e + NW < cnt) { q_ah = eq[e + NW]; m_ah = em[e + NW]; }
     while (true) {
         unsigned long long mn = 0;
         int en = e + NW;
@@ -523,8 +529,14 @@ improved_kernel(ImprovedArgs a, int Ct) {
         const bool more = en < cnt;
         int64_t qn = 0;
         if (more) {
-            qn = eq[en];
-            if (ONE_CTA || subs == 1) mn = em[en];
+            if constexpr (IDX_AHEAD) {
+                qn = q_ah;
+                mn = m_ah;
+                if (en + NW < cnt) { q_ah = eq[en + NW]; m_ah = em[en + NW]; }
+            } else {
+                qn = eq[en];
+                if (ONE_CTA || subs == 1) mn = em[en];
+            }
             if constexpr (PREFETCH) load_p1<EPL, B1X, KO>(nxt, a, qn, c0t, lane);
         }
         if (PREFETCH && mcur) load_p2<EPL, B1X, KO>(cur, a, qe, lane);  // in flight during phase 1

@@ -63,6 +63,13 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// 128-bit shared-memory load by 32-bit shared address (forces LDS: pointers derived from the
+// dynamic shared array through address arithmetic otherwise compile to generic loads)
+__device__ __forceinline__ float4 lds128(unsigned a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
 // order this thread's earlier generic-proxy reads of its slot before the next async write
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
@@ -219,13 +226,15 @@ __global__ void __launch_bounds__(W * 32, 1)
 keogh_stream_tma_kernel(const __grid_constant__ CUtensorMap tmap, const float *__restrict__ U,
                         const float *__restrict__ L, int64_t N, int n, int Q, int D, bool rooted,
                         float *__restrict__ out, int64_t ldo) {
-    extern __shared__ __align__(1024) unsigned char smraw[];
+    extern __shared__ __align__(128) unsigned char smraw[];
     constexpr int ROWS = 32 * R;
     const int npad = (n + kBoxCols - 1) / kBoxCols * kBoxCols;
     const int nch = npad / kBoxCols;
     constexpr int BOX = ROWS * kBoxCols;  // floats (a multiple of the 1 KB swizzle atom)
     // (the dynamic shared-memory base is only guaranteed 16-byte aligned: round up to 1 KB)
-    float *boxes = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    // (offset arithmetic on the shared array itself, not a uintptr_t round trip: the compiler
+    // then keeps the shared address space and emits LDS, not generic loads)
+    float *boxes = reinterpret_cast<float *>(smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u));
     float *sU = boxes + (size_t)W * D * BOX;  // [QB][npad]
     float *sL = sU + (size_t)QB * npad;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sL + (size_t)QB * npad);  // [W][D]
@@ -278,8 +287,8 @@ keogh_stream_tma_kernel(const __grid_constant__ CUtensorMap tmap, const float *_
         const int ch = (int)(g - ti * nch);
         const int s = (int)(g % D);
         mbar_wait(mybar + s, (unsigned)((g / D) & 1));
-        const float *xr = mybox + (size_t)s * BOX + lane * kBoxCols;
-        const float *ub = sU + ch * kBoxCols, *lb = sL + ch * kBoxCols;
+        const unsigned xr = smem_u32(mybox) + (unsigned)(s * BOX + lane * kBoxCols) * 4u;
+        const unsigned ub = smem_u32(sU) + (unsigned)(ch * kBoxCols) * 4u, lb = smem_u32(sL) + (unsigned)(ch * kBoxCols) * 4u;
         float part[QB][R];
 #pragma unroll
         for (int q = 0; q < QB; ++q)
@@ -289,12 +298,11 @@ keogh_stream_tma_kernel(const __grid_constant__ CUtensorMap tmap, const float *_
         for (int k = 0; k < kBoxCols / 4; ++k) {
             float4 xv[R];
 #pragma unroll
-            for (int i = 0; i < R; ++i)
-                xv[i] = *reinterpret_cast<const float4 *>(xr + i * 32 * kBoxCols + 4 * (k ^ swz));
+            for (int i = 0; i < R; ++i) xv[i] = lds128(xr + (unsigned)(i * 32 * kBoxCols + 4 * (k ^ swz)) * 4u);
 #pragma unroll
             for (int q = 0; q < QB; ++q) {
-                const float4 u = *reinterpret_cast<const float4 *>(ub + (size_t)q * npad + 4 * k);
-                const float4 l = *reinterpret_cast<const float4 *>(lb + (size_t)q * npad + 4 * k);
+                const float4 u = lds128(ub + (unsigned)(q * npad + 4 * k) * 4u);
+                const float4 l = lds128(lb + (unsigned)(q * npad + 4 * k) * 4u);
 #pragma unroll
                 for (int i = 0; i < R; ++i) part[q][i] = lb4<P>(part[q][i], xv[i], u, l);
             }
@@ -320,6 +328,170 @@ keogh_stream_tma_kernel(const __grid_constant__ CUtensorMap tmap, const float *_
                 for (int i = 0; i < R; ++i) acc[q][i] = 0.f;
         }
         __syncwarp();  // every lane is done with box s before lane 0 refills it
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// COPY = 3 (5 <= Q <= 8): split queries, shared boxes.  At Q = 8 the pass does 8 pair-elements
+// per database element, so the per-element issue cost, not HBM, decides: the R = 4, one-warp-
+// per-scheduler variant above reached 0.24 of HBM.  Here a CTA has G row groups x H query
+// groups of warps; the G rings of D boxes (32R rows x 16 floats, 64-byte TMA swizzle) are each
+// consumed by the H warps of the row group (QW = 4 queries each), so a box read from HBM once
+// serves all Q queries, each lane holds R = 8 rows (an envelope read from shared memory serves
+// 8 rows), and two warps per scheduler hide the shared-memory latency.  Ring protocol per row
+// group: full[s] completes on the TMA bytes, empty[s] on the H consumer warps' arrivals; lane 0
+// of the group's first warp refills a stage once both consumers released it.  Accumulation in
+// packed pairs (even / odd elements of a row: one FFMA2 per two pair-elements), so per
+// pair-element one FADD2 (two subtractions), one FMNMX3 and half an FFMA2: 2.5 issue slots.
+// Two-level summation (as the other bound kernels): the 16 terms of a box per (query, row) in
+// two packed partial sums, folded into the row total after every box.
+constexpr int kSqCols = 16;  // box columns (64-byte rows)
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int P>
+__device__ __forceinline__ float2 lb4x2(float2 acc, const float4 &x, const float4 &u, const float4 &l) {
+    const float2 a0 = __fadd2_rn(make_float2(x.x, x.y), make_float2(-u.x, -u.y));
+    const float2 b0 = __fadd2_rn(make_float2(l.x, l.y), make_float2(-x.x, -x.y));
+    const float2 a1 = __fadd2_rn(make_float2(x.z, x.w), make_float2(-u.z, -u.w));
+    const float2 b1 = __fadd2_rn(make_float2(l.z, l.w), make_float2(-x.z, -x.w));
+    const float2 d0 = make_float2(max3f(a0.x, b0.x, 0.f), max3f(a0.y, b0.y, 0.f));
+    const float2 d1 = make_float2(max3f(a1.x, b1.x, 0.f), max3f(a1.y, b1.y, 0.f));
+    if constexpr (P == 1) {
+        acc = __fadd2_rn(acc, d0);
+        return __fadd2_rn(acc, d1);
+    } else {
+        acc = __ffma2_rn(d0, d0, acc);
+        return __ffma2_rn(d1, d1, acc);
+    }
+}
+
+template <int P, int H, int G, int R>
+__global__ void __launch_bounds__(G * H * 32, 1)
+keogh_stream_sq_kernel(const __grid_constant__ CUtensorMap tmap, const float *__restrict__ U,
+                       const float *__restrict__ L, int64_t N, int n, int Q, int D, bool rooted,
+                       float *__restrict__ out, int64_t ldo) {
+    constexpr int QW = 4;  // queries per warp
+    constexpr int QB = QW * H;
+    constexpr int ROWS = 32 * R;
+    constexpr int BOX = ROWS * kSqCols;  // floats
+    extern __shared__ __align__(128) unsigned char smraw[];
+    const int npad = (n + kSqCols - 1) / kSqCols * kSqCols;
+    const int nch = npad / kSqCols;
+    // (offset arithmetic on the shared array itself, not a uintptr_t round trip: the compiler
+    // then keeps the shared address space and emits LDS, not generic loads)
+    float *boxes = reinterpret_cast<float *>(smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u));
+    float *sU = boxes + (size_t)G * D * BOX;  // [QB][npad]
+    float *sL = sU + (size_t)QB * npad;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sL + (size_t)QB * npad);  // [G][D]
+    uint64_t *empty = full + G * D;                                        // [G][D]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = warp / H, h = warp - g * H;  // row group, query group
+    for (int t = tid; t < QB * npad; t += G * H * 32) {
+        const int q = t / npad, i = t - q * npad;
+        const bool ok = q < Q && i < n;
+        sU[t] = ok ? U[(int64_t)q * n + i] : kInf;
+        sL[t] = ok ? L[(int64_t)q * n + i] : -kInf;
+    }
+    if (tid == 0) {
+        for (int s = 0; s < G * D; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, H);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    const int64_t ntiles = (N + ROWS - 1) / ROWS;
+    const int64_t gw = (int64_t)blockIdx.x * G + g, GW = (int64_t)gridDim.x * G;
+    const int64_t my_tiles = gw < ntiles ? (ntiles - 1 - gw) / GW + 1 : 0;
+    const int64_t steps = my_tiles * nch;
+    float *mybox = boxes + (size_t)g * D * BOX;
+    uint64_t *myfull = full + g * D, *myempty = empty + g * D;
+    const bool producer = h == 0 && lane == 0;
+    auto issue = [&](int64_t st) {
+        const int64_t ti = st / nch;
+        const int ch = (int)(st - ti * nch);
+        const int64_t tile = gw + ti * GW;
+        const int s = (int)(st % D);
+        if (st >= D) mbar_wait(myempty + s, (unsigned)(((st / D) - 1) & 1));  // both consumers done
+        fence_proxy_async();
+        mbar_expect_tx(myfull + s, (unsigned)(BOX * sizeof(float)));
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+            "[%4];\n" ::"r"(smem_u32(mybox + (size_t)s * BOX)),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(ch * kSqCols), "r"((int)(tile * ROWS)),
+            "r"(smem_u32(myfull + s))
+            : "memory");
+    };
+    if (producer) {
+        const int pro = (int)(steps < D - 1 ? steps : D - 1);
+        for (int st = 0; st < pro; ++st) issue(st);
+    }
+    const int swz = (lane >> 1) & 3;  // 64-byte swizzle: chunk c of row r sits at c ^ ((r >> 1) & 3)
+    const unsigned ub_a = smem_u32(sU + (size_t)h * QW * npad), lb_a = smem_u32(sL + (size_t)h * QW * npad);
+    const unsigned box_a = smem_u32(mybox);
+    float2 acc[QW][R];
+    float tot[QW][R];
+#pragma unroll
+    for (int q = 0; q < QW; ++q)
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            acc[q][i] = make_float2(0.f, 0.f);
+            tot[q][i] = 0.f;
+        }
+    for (int64_t st = 0; st < steps; ++st) {
+        if (producer && st + D - 1 < steps) issue(st + D - 1);
+        const int64_t ti = st / nch;
+        const int ch = (int)(st - ti * nch);
+        const int s = (int)(st % D);
+        mbar_wait(myfull + s, (unsigned)((st / D) & 1));
+        const unsigned xr = box_a + (unsigned)(s * BOX + lane * kSqCols) * 4u;
+        const unsigned ua = ub_a + (unsigned)(ch * kSqCols) * 4u, la = lb_a + (unsigned)(ch * kSqCols) * 4u;
+#pragma unroll
+        for (int k = 0; k < kSqCols / 4; ++k) {
+            float4 xv[R];
+#pragma unroll
+            for (int i = 0; i < R; ++i) xv[i] = lds128(xr + (unsigned)(i * 32 * kSqCols + 4 * (k ^ swz)) * 4u);
+#pragma unroll
+            for (int q = 0; q < QW; ++q) {
+                const float4 u = lds128(ua + (unsigned)(q * npad + 4 * k) * 4u);
+                const float4 l = lds128(la + (unsigned)(q * npad + 4 * k) * 4u);
+#pragma unroll
+                for (int i = 0; i < R; ++i) acc[q][i] = lb4x2<P>(acc[q][i], xv[i], u, l);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(myempty + s);  // this warp is done with box s
+        // two-level summation: the box's 8 + 8 terms per (query, row) fold into the row total
+#pragma unroll
+        for (int q = 0; q < QW; ++q)
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+                tot[q][i] += acc[q][i].x + acc[q][i].y;
+                acc[q][i] = make_float2(0.f, 0.f);
+            }
+        if (ch == nch - 1) {
+            const int64_t c0 = (gw + ti * GW) * ROWS + lane;
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+                const int64_t c = c0 + 32 * i;
+                if (c < N) {
+#pragma unroll
+                    for (int q = 0; q < QW; ++q) {
+                        const int qq = h * QW + q;
+                        const float v = tot[q][i];
+                        if (qq < Q) out[(int64_t)qq * ldo + c] = rooted ? rootp<P>(v) : v;
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < QW; ++q)
+#pragma unroll
+                for (int i = 0; i < R; ++i) tot[q][i] = 0.f;
+        }
     }
 }
 
@@ -384,13 +556,66 @@ int launch_stream_tma_t(const float *U, const float *L, const float *db, int64_t
     return DTWLB_OK;
 }
 
+template <int P, int H, int G, int R>
+int launch_stream_sq_t(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n, bool rooted,
+                       float *out, int64_t ldo, cudaStream_t st) {
+    EncodeTiledFn enc = get_encode_tiled();
+    if (!enc) {
+        set_error(DTWLB_ECUDA, "stream LB_Keogh pass: cuTensorMapEncodeTiled unavailable");
+        return DTWLB_ECUDA;
+    }
+    constexpr int ROWS = 32 * R;
+    CUtensorMap tmap;
+    const cuuint64_t gdim[2] = {(cuuint64_t)n, (cuuint64_t)N};
+    const cuuint64_t gstride[1] = {(cuuint64_t)n * sizeof(float)};
+    const cuuint32_t box[2] = {kSqCols, ROWS};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(db), gdim, gstride, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error(DTWLB_ECUDA, "stream LB_Keogh pass: cuTensorMapEncodeTiled failed (%d)", (int)r);
+        return DTWLB_ECUDA;
+    }
+    const int npad = (n + kSqCols - 1) / kSqCols * kSqCols;
+    const size_t env = (size_t)2 * 4 * H * npad * sizeof(float);
+    int dev = 0, smem_max = 0, nsm = 148;
+    DTWLB_CUDA(cudaGetDevice(&dev));
+    DTWLB_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    DTWLB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const size_t per_stage = (size_t)G * (ROWS * kSqCols * sizeof(float) + 2 * sizeof(uint64_t));
+    static const int env_d = [] { const char *e = getenv("DTWLB_STREAM_STAGES"); return e ? atoi(e) : 0; }();
+    int D = env_d > 1 ? std::min(env_d, 8) : 8;
+    while (D > 2 && env + D * per_stage + 1024 > (size_t)smem_max) --D;
+    const size_t smem = env + D * per_stage + 1024;
+    if (smem > (size_t)smem_max) {
+        set_error(DTWLB_EUNSUPPORTED, "stream LB_Keogh pass: n = %d too long for shared memory", n);
+        return DTWLB_EUNSUPPORTED;
+    }
+    auto k = keogh_stream_sq_kernel<P, H, G, R>;
+    DTWLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t ntiles = ceil_div(N, ROWS);
+    const int grid = (int)std::min<int64_t>(ceil_div(ntiles, G), nsm);  // persistent
+    k<<<grid, G * H * 32, smem, st>>>(tmap, U, L, N, n, (int)Q, D, rooted, out, ldo);
+    DTWLB_LAUNCH_CHECK();
+    return DTWLB_OK;
+}
+
 template <int P>
 int launch_stream_tma_p(const float *U, const float *L, const float *db, int64_t Q, int64_t N, int n, bool rooted,
                         float *out, int64_t ldo, cudaStream_t st) {
     // rows per lane R grows with Q: each envelope read serves R rows (see the kernel)
     if (Q <= 1) return launch_stream_tma_t<P, 1, 1, 8>(U, L, db, Q, N, n, rooted, out, ldo, st);
     if (Q <= 2) return launch_stream_tma_t<P, 2, 2, 8>(U, L, db, Q, N, n, rooted, out, ldo, st);
-    if (Q <= 4) return launch_stream_tma_t<P, 4, 4, 4>(U, L, db, Q, N, n, rooted, out, ldo, st);
+    // split-query shared-box kernel (DTWLB_STREAM_SQ=0 keeps the per-warp-ring kernel): 5..8
+    // queries always, 3..4 queries as one query group (experiment, DTWLB_STREAM_SQ=2)
+    static const int env_sq = [] { const char *e = getenv("DTWLB_STREAM_SQ"); return e ? atoi(e) : 1; }();
+    if (Q <= 4) {
+        if (env_sq == 2 && Q >= 3) return launch_stream_sq_t<P, 1, 8, 4>(U, L, db, Q, N, n, rooted, out, ldo, st);
+        return launch_stream_tma_t<P, 4, 4, 4>(U, L, db, Q, N, n, rooted, out, ldo, st);
+    }
+    if (env_sq == 3) return launch_stream_sq_t<P, 2, 6, 8>(U, L, db, Q, N, n, rooted, out, ldo, st);
+    if (env_sq) return launch_stream_sq_t<P, 2, 4, 8>(U, L, db, Q, N, n, rooted, out, ldo, st);
     return launch_stream_tma_t<P, 8, 4, 4>(U, L, db, Q, N, n, rooted, out, ldo, st);
 }
 

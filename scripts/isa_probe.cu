@@ -35,6 +35,15 @@ __global__ void probe(float *out, float s0, float s1, long long *cycles) {
                 float2 d = make_float2(fmaxf(fmaxf(u.x, l.x), 0.f), fmaxf(fmaxf(u.y, l.y), 0.f));
                 p[j] = __ffma2_rn(d, d, p[j]);
             }
+            if constexpr (OP == 9) {  // FMNMX pair that cannot be folded: max / min swap
+                const float t = fmaxf(a[j], b[j]);
+                b[j] = fminf(a[j], b[j]);
+                a[j] = t + 0.f;
+            }
+            if constexpr (OP == 10) {  // LB_Improved element: FMNMX, FMNMX, FADD, FADD, FMNMX3, FFMA
+                const float d = fmaxf(fmaxf(a[j] - fmaxf(b[j], s0), fminf(b[(j + 1) & 7], s1) - a[j]), 0.f);
+                a[j] = fmaf(d, d, a[j]);
+            }
             if constexpr (OP == 8) {  // DTW cell: FADD, FMNMX3, FFMA
                 float t = s0 - b[j];
                 a[j] = fmaf(t, t, fminf(fminf(a[j], b[(j + 1) & 7]), a[(j + 7) & 7]));
@@ -59,8 +68,17 @@ void run(const char *name, double ops_per_iter_per_thread, double lane_ops_per_i
     cudaMalloc(&out, sizeof(float) * ctas * nt);
     cudaMalloc(&cyc, sizeof(long long) * ctas);
     probe<OP><<<ctas, nt>>>(out, 1.0f, 2.0f, cyc);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
     probe<OP><<<ctas, nt>>>(out, 1.0f, 2.0f, cyc);
+    cudaEventRecord(e1);
     cudaDeviceSynchronize();
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    int khz = 0;
+    cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, 0);
     long long h[4096];
     cudaMemcpy(h, cyc, sizeof(long long) * ctas, cudaMemcpyDeviceToHost);
     double avg = 0;
@@ -70,7 +88,12 @@ void run(const char *name, double ops_per_iter_per_thread, double lane_ops_per_i
     const double warps_per_sm = 4 * nt / 32.0;
     const double winst = warps_per_sm * ITERS * ops_per_iter_per_thread / avg;
     const double lops = warps_per_sm * 32 * ITERS * lane_ops_per_iter / avg;
-    printf("%-40s %6.2f warp-inst/clk/SM  %7.1f lane-ops/clk/SM\n", name, winst, lops);
+    // event-timed: whole grid's warp-instructions / (elapsed x SMs x clock) -- independent of
+    // what clock64() counts (its per-CTA counts gave > 4 warp-inst/clk/SM, i.e. not SM clocks)
+    const double tot_w = (double)ctas * (nt / 32) * ITERS * ops_per_iter_per_thread;
+    const double ev_w = tot_w / (ms * 1e-3 * sms * khz * 1e3);
+    printf("%-40s %6.2f warp-inst/clk/SM  %7.1f lane-ops/clk/SM (clock64)   event-timed: %5.2f warp-inst/clk/SM %7.1f lane-ops/clk/SM  %.3f ms @ %d MHz\n",
+           name, winst, lops, ev_w, ev_w * 32 * lane_ops_per_iter / ops_per_iter_per_thread, ms, khz / 1000);
     cudaFree(out);
     cudaFree(cyc);
 }
@@ -85,5 +108,7 @@ int main() {
     run<6>("LB element (4 ops) [elements]", 32, 8);
     run<7>("packed LB pair (5 ops) [elements]", 40, 16);
     run<8>("DTW cell (3 ops) [cells]", 24, 8);
+    run<9>("FMNMX (max/min swap, 2 ops)", 16, 16);
+    run<10>("LB_Improved element (6 ops) [elements]", 48, 8);
     return 0;
 }
