@@ -408,9 +408,31 @@ def run_ours(args, cfg):
                                   "unit": "Tlane-op/s", "peak": peak,
                                   "note": "3 slots per in-band DTW cell actually computed (kernel counter, early "
                                           "abandon), CUDA events around every walk-round launch"}
+        # Measured instruction-mix peaks (scripts/isa_probe.cu, event-timed, profiles/r02h_isa_probe.txt):
+        # the same SASS sequences in 8 independent chains per thread, 32 warps per SM, elements (cells)
+        # per SM clock.  FMNMX3 and the packed f32x2 ops issue at half rate and FFMA2 at a third, so a
+        # bound element costs more than 3 issue slots: these are the kernels' attainable ALU roofs.
+        mix = {"dtw_cell": 42.0, "lbk_elem": 26.0, "lbi_elem": 25.3, "gate_elem": 24.5, "lbk_packed": 27.7}
+        clk_sm = n_sm * sm_clock * 1e6  # SM-clocks per second, whole GPU
+        if "bound_pass" in kern and kern["bound_pass"]["bound"] == "alu":
+            kern["bound_pass"]["mix_peak"] = 3.0 * mix["gate_elem"] * clk_sm / 1e12
+        if "bound_pass" in kern and kern["bound_pass"]["bound"] == "hbm":
+            # the LB_Keogh arithmetic caps the streaming pass too: Q pair-elements per database element
+            rate = mix["lbk_packed"] if 4 < cfg.Q <= 8 else mix["gate_elem"]
+            kern["bound_pass"]["alu_cap"] = rate * clk_sm / cfg.Q * 4 / 1e9  # GB/s of database
+            kern["bound_pass"]["mix_peak"] = min(hbm_peak, kern["bound_pass"]["alu_cap"])
+        if "survivor_kernel" in kern:
+            kn = (keogh_eval if pf else 0.0) * cfg.n
+            ki = improved * cfg.n
+            t_mix = (kn / mix["lbk_elem"] + ki / mix["lbi_elem"]) / clk_sm
+            kern["survivor_kernel"]["mix_peak"] = kern["survivor_kernel"]["work"] / t_mix if t_mix > 0 else peak
+        if "dtw_kernel" in kern and cfg.w <= 64:
+            kern["dtw_kernel"]["mix_peak"] = 3.0 * mix["dtw_cell"] * clk_sm / 1e12
         for v in kern.values():
             v["achieved"] = v["work"] / (v["ms"] * 1e-3) if v["ms"] > 0 else 0.0
             v["frac"] = v["achieved"] / v["peak"]
+            if "mix_peak" in v:
+                v["frac_of_mix_peak"] = v["achieved"] / v["mix_peak"]
         dom_name = max((kk for kk in kern if kk != "survivor_kernel_l1"),
                        key=lambda kk: kern[kk]["ms"] / kern[kk].get("launches", 1))
         rk = kern[dom_name]
@@ -469,7 +491,11 @@ def run_ours(args, cfg):
                                        "MEASURED_PEAKS hbm_gbs (measured copy bandwidth)"),
                          "ops_note": rk["note"], "kernel_ms": rk["ms"], "traffic_note": traffic_note,
                          "dominant": dom_name,
-                         **{kn: {x: v[x] for x in ("kernel", "bound", "ms", "achieved", "peak", "unit", "frac")}
+                         "mix_peak": rk.get("mix_peak"), "frac_of_mix_peak": rk.get("frac_of_mix_peak"),
+                         "mix_note": "attainable peak of the kernel's own instruction mix, measured by "
+                                     "scripts/isa_probe.cu (profiles/r02h_isa_probe.txt)",
+                         **{kn: {x: v[x] for x in ("kernel", "bound", "ms", "achieved", "peak", "unit", "frac",
+                                                   "mix_peak", "frac_of_mix_peak", "alu_cap") if x in v}
                             for kn, v in kern.items()}},
             "e2e": {"value": pairs / (e2e_ms * 1e-3), "unit": "pairs/s",
                     # whole job: every rank copies the queries and its shard in, its result out
@@ -492,7 +518,7 @@ def run_ours(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C5", choices=sorted(datagen.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

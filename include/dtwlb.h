@@ -145,7 +145,13 @@ typedef struct nn_opts {
      * call's w, exactly as lb_envelope(db, n, w, U, L, N) writes it.  NULL = computed
      * inside the call.  A wrong index gives wrong bounds (not checked). */
     const float *db_env;
-    int32_t reserved[2];
+    /* Database-sharded search: the number of shards G whose thresholds the exchange combines
+     * (0 or 1 = unsharded).  The best-first seed range -- the candidates searched first, whose
+     * k-th best DTW seeds the threshold -- is sized for the WHOLE database and split among the
+     * shards (each shard seeds from 1/G of it), so G shards together do the seed work of one
+     * search instead of G times it.  Affects speed only, never the result. */
+    int32_t shards;
+    int32_t reserved;
 } nn_opts;
 
 #define DTWLB_KEOGH_ONLY 1

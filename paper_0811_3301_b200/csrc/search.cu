@@ -45,6 +45,7 @@ struct Workspace {
     std::vector<size_t> size;
     ~Workspace() { release(); }
     void release() {
+        qb_cache.clear();
         if (ptr.empty()) return;
         int cur = -1;
         cudaGetDevice(&cur);
@@ -56,6 +57,16 @@ struct Workspace {
         size.clear();
     }
     size_t cur_size(int slot) const { return slot < (int)size.size() ? size[slot] : 0; }
+    // query-block size chosen for a problem shape (Q, N, n, mode): cudaMemGetInfo is asked once
+    // per shape -- it contends with NVML clients (nvidia-smi) for a driver lock, and a call of
+    // it inside the pipeline showed up as 5-50 ms device-idle gaps before the bound pass
+    std::vector<std::tuple<int64_t, int64_t, int, int, int64_t>> qb_cache;
+    int64_t cached_qb(int64_t Q, int64_t N, int n, int mode) const {
+        for (auto &t : qb_cache)
+            if (std::get<0>(t) == Q && std::get<1>(t) == N && std::get<2>(t) == n && std::get<3>(t) == mode)
+                return std::get<4>(t);
+        return 0;
+    }
     int get(int slot, size_t bytes, void **out) {
         if ((int)ptr.size() <= slot) { ptr.resize(slot + 1, nullptr); size.resize(slot + 1, 0); }
         bytes = std::max<size_t>(bytes, 256);
@@ -592,11 +603,15 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     tm.mark();  // 1
 
     // ---- query block size from free memory: gate bound (4N) + list (8N) per query ----
+    const int qb_mode = (prefilter ? 1 : 0) | (keogh_only ? 2 : 0) | (stream_mode ? 4 : 0);
+    const int64_t qb_hit = (opts && opts->query_block > 0) ? 0 : ws().cached_qb(Q, N, n, qb_mode);
     size_t free_b = 0, total_b = 0;
-    DTWLB_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    // the block-sized slots this call would reuse count as free: the block size (hence the
-    // pipeline) is then the same on every call of a given problem, not smaller after the first
-    for (int sl : {S_BETA1, S_LIST, S_RES, S_MASK}) free_b += ws().cur_size(sl);
+    if (!qb_hit) {
+        DTWLB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        // the block-sized slots this call would reuse count as free: the block size (hence the
+        // pipeline) is then the same on every call of a given problem, not smaller after the first
+        for (int sl : {S_BETA1, S_LIST, S_RES, S_MASK}) free_b += ws().cur_size(sl);
+    }
     // per query of the block: gate bound (2 B fp16 with the pre-filter, else 4 B) + key list (8 B)
     // per pair, a walk round's completed-pair slots (12 B per item, <= min(N, kDMax) items),
     // the survivor pass's (query, mask) entries (12 B per 64-candidate tile) and the sort's runs
@@ -605,8 +620,11 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     const size_t per_q = (size_t)N * (gate_elem + 8) + (size_t)round_items * 12 + (size_t)ceil_div(N, 64) * 12 +
                          (size_t)ceil_div(N, kRun) * 8 + 4096;
     static const double env_mem = [] { const char *e = getenv("DTWLB_BLOCK_MEM_FRAC"); return e ? atof(e) : 0.0; }();
-    const double mem_frac = env_mem > 0 ? env_mem : 0.45;
-    int64_t Qb = opts && opts->query_block > 0 ? opts->query_block : (int64_t)(free_b * mem_frac / per_q);
+    // (0.6 of the free memory: one 8192-query block at C5, measured 274 vs 281 ms for 2 x 4096)
+    const double mem_frac = env_mem > 0 ? env_mem : 0.6;
+    int64_t Qb = opts && opts->query_block > 0 ? opts->query_block
+                 : qb_hit                     ? qb_hit
+                                              : (int64_t)(free_b * mem_frac / per_q);
     // a walk round holds <= Qb * min(N, kDMax) items, counted in int32 (plan_kernel, dtw4_kernel)
     Qb = std::min<int64_t>(Qb, (int64_t)(0x7fffffff - 1024) / round_items);
     Qb = std::max<int64_t>(1, std::min<int64_t>(Qb, Q));
@@ -615,6 +633,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         const int64_t nb = ceil_div(Q, Qb);
         Qb = std::min<int64_t>(Qb, ceil_div(ceil_div(Q, nb), 64) * 64);
     }
+    if (!qb_hit && !(opts && opts->query_block > 0)) ws().qb_cache.emplace_back(Q, N, n, qb_mode, Qb);
     const int64_t cap = N;
     const int64_t ldb = (N + 7) / 8 * 8;  // 16-byte rows of the fp16 gate block
 
@@ -661,8 +680,10 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     // ranges were slower (326-338): the seed range's survivor pass is dominated by per-entry
     // cost (about one survivor per (query, 64-tile) entry), so a smaller seed is cheaper
     static const int env_S = [] { const char *e = getenv("DTWLB_SEED"); return e ? atoi(e) : 0; }();
+    // (a database shard seeds from 1/G of the whole database's seed range, nn_opts.shards)
+    const int64_t shards = opts && opts->shards > 1 ? opts->shards : 1;
     const int64_t S = std::max<int64_t>(std::max<int64_t>(256, 4LL * k),
-                                        std::min<int64_t>(env_S > 0 ? env_S : kSeedCap, N / 64));
+                                        std::min<int64_t>((env_S > 0 ? env_S : kSeedCap) / shards, N / 64));
     // number of ranges R and the growth G of their sampled sizes (S, S*G, S*G^2, ..., rest)
     static const int env_R = [] { const char *e = getenv("DTWLB_RANGES"); return e ? atoi(e) : 0; }();
     static const int env_G = [] { const char *e = getenv("DTWLB_RANGE_GROWTH"); return e ? atoi(e) : 0; }();

@@ -608,10 +608,11 @@ int launch_stream_tma_p(const float *U, const float *L, const float *db, int64_t
     if (Q <= 1) return launch_stream_tma_t<P, 1, 1, 8>(U, L, db, Q, N, n, rooted, out, ldo, st);
     if (Q <= 2) return launch_stream_tma_t<P, 2, 2, 8>(U, L, db, Q, N, n, rooted, out, ldo, st);
     // split-query shared-box kernel (DTWLB_STREAM_SQ=0 keeps the per-warp-ring kernel): 5..8
-    // queries always, 3..4 queries as one query group (experiment, DTWLB_STREAM_SQ=2)
+    // queries as two query groups, 3..4 queries as one (eight row groups of 4 rows per lane:
+    // C5s4 0.243 vs 0.256 ms for the per-warp-ring kernel)
     static const int env_sq = [] { const char *e = getenv("DTWLB_STREAM_SQ"); return e ? atoi(e) : 1; }();
     if (Q <= 4) {
-        if (env_sq == 2 && Q >= 3) return launch_stream_sq_t<P, 1, 8, 4>(U, L, db, Q, N, n, rooted, out, ldo, st);
+        if (env_sq && Q >= 3) return launch_stream_sq_t<P, 1, 8, 4>(U, L, db, Q, N, n, rooted, out, ldo, st);
         return launch_stream_tma_t<P, 4, 4, 4>(U, L, db, Q, N, n, rooted, out, ldo, st);
     }
     if (env_sq == 3) return launch_stream_sq_t<P, 2, 6, 8>(U, L, db, Q, N, n, rooted, out, ldo, st);

@@ -66,6 +66,7 @@ def sharded_nn_search(queries: torch.Tensor, db_shard: torch.Tensor, shard_lo: i
     if world > 1:
         # all ranks use the same blocking; thresholds are min-reduced after each block's first range
         kw["query_block"] = query_block or common_query_block(db_shard.shape[0], group, dev)
+        kw["shards"] = world  # each shard seeds from 1/world of the best-first range
         if kk >= k:
             kw["exchange"] = lambda thr: dist.all_reduce(thr, op=dist.ReduceOp.MIN, group=group)
         else:

@@ -44,6 +44,12 @@ __global__ void probe(float *out, float s0, float s1, long long *cycles) {
                 const float d = fmaxf(fmaxf(a[j] - fmaxf(b[j], s0), fminf(b[(j + 1) & 7], s1) - a[j]), 0.f);
                 a[j] = fmaf(d, d, a[j]);
             }
+            if constexpr (OP == 11) {  // gate / tile-kernel element pair: FADD2, FADD2, 2x FMNMX3, 2x FFMA
+                float2 u = __fadd2_rd(q2[j], make_float2(-p[j].x, -p[j].y));
+                float2 l = __fadd2_rd(p[j], make_float2(-s1, -s0));
+                const float d0 = fmaxf(fmaxf(u.x, l.x), 0.f), d1 = fmaxf(fmaxf(u.y, l.y), 0.f);
+                p[j].x = __fmaf_rd(d1, d1, __fmaf_rd(d0, d0, p[j].x));
+            }
             if constexpr (OP == 8) {  // DTW cell: FADD, FMNMX3, FFMA
                 float t = s0 - b[j];
                 a[j] = fmaf(t, t, fminf(fminf(a[j], b[(j + 1) & 7]), a[(j + 7) & 7]));
@@ -109,6 +115,7 @@ int main() {
     run<7>("packed LB pair (5 ops) [elements]", 40, 16);
     run<8>("DTW cell (3 ops) [cells]", 24, 8);
     run<9>("FMNMX (max/min swap, 2 ops)", 16, 16);
+    run<11>("gate element pair (FADD2 x2, FMNMX3 x2, FFMA x2) [elements]", 48, 16);
     run<10>("LB_Improved element (6 ops) [elements]", 48, 8);
     return 0;
 }

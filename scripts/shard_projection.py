@@ -64,7 +64,7 @@ def main():
         rec = []
         for lo, hi in bounds:
             blocks = []
-            B.nn_search(qs, db[lo:hi], w, p, k, index_base=lo, query_block=qb,
+            B.nn_search(qs, db[lo:hi], w, p, k, index_base=lo, query_block=qb, shards=G,
                         exchange=lambda thr, b=blocks: b.append(thr.clone()))
             rec.append(torch.cat(blocks))
         thr_min = torch.stack(rec).min(dim=0).values
@@ -78,7 +78,7 @@ def main():
                     n = thr.numel()
                     torch.minimum(thr, thr_min[pos[0]:pos[0] + n], out=thr)
                     pos[0] += n
-                return B.nn_search(qs, db[lo:hi], w, p, k, index_base=lo, query_block=qb, exchange=ex)
+                return B.nn_search(qs, db[lo:hi], w, p, k, index_base=lo, query_block=qb, exchange=ex, shards=G)
             ms, out = timed(run)
             shard_ms.append(ms)
             lists.append(out)

@@ -29,7 +29,7 @@ def _env(qs, w):
 
 @pytest.mark.parametrize("n,w,N", [(4, 1, 300), (128, 12, 40_000), (256, 25, 1_000), (1000, 50, 300),
                                    (96, 100, 777)])
-@pytest.mark.parametrize("Q", [1, 3, 8])
+@pytest.mark.parametrize("Q", [1, 3, 4, 6, 8])
 @pytest.mark.parametrize("p", [1, 2])
 def test_stream_lb_keogh_vs_oracle(cuda_ok, n, w, N, Q, p):
     """N = 40 000 rows of n = 128: 157 tiles of 256 rows over 148 persistent CTAs (several tiles

@@ -31,7 +31,7 @@ def _oracle_search(queries, db, w, p, k, index_base=0, out=None, **_):
     return torch.from_numpy(idx + index_base), torch.from_numpy(dst.astype(np.float32))
 
 
-def _cascade_search(queries, db, w, p, k, index_base=0, out=None, query_block=None, exchange=None):
+def _cascade_search(queries, db, w, p, k, index_base=0, out=None, query_block=None, exchange=None, shards=0):
     """CPU stand-in of nn_search's two-range protocol built from oracle primitives: per
     query block, range 1 = the S candidates with the smallest LB_Keogh (exact DTW, local
     top-k, tau); exchange(tau) may lower tau; range 2 = the other candidates whose
@@ -85,7 +85,10 @@ def _worker_exchange(rank, world, port, N, k, result_q):
         shard = np.ascontiguousarray(shard)
         seen = []
 
-        def search(queries, db, w, p, kk, index_base=0, out=None, query_block=None, exchange=None):
+        def search(queries, db, w, p, kk, index_base=0, out=None, query_block=None, exchange=None, shards=0):
+            # every shard is told the shard count (its best-first seed range is 1/world of the whole)
+            assert shards == world, (shards, world)
+
             def ex(t):
                 before = t.clone()
                 exchange(t)
@@ -216,7 +219,7 @@ def _worker_unbalanced(rank, world, port, bounds, k, result_q):
             shard[1] = qs[0] * np.float32(0.999)
         sent = []
 
-        def search(queries, db, w, p, kk, index_base=0, out=None, query_block=None, exchange=None):
+        def search(queries, db, w, p, kk, index_base=0, out=None, query_block=None, exchange=None, shards=0):
             def ex(t):
                 exchange(t)
                 sent.append(t.numpy().copy())
