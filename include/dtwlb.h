@@ -151,7 +151,12 @@ typedef struct nn_opts {
      * shards (each shard seeds from 1/G of it), so G shards together do the seed work of one
      * search instead of G times it.  Affects speed only, never the result. */
     int32_t shards;
-    int32_t reserved;
+    /* Further exchanges inside the LAST range's DTW walk, when the thresholds tighten fastest:
+     * the exchange is also called after that walk's rounds 2, 4, ..., 2*exchange_walk
+     * (0 <= exchange_walk <= 3; rounds a shard does not run still call it, with its final
+     * thresholds), so a block makes exactly 1 + exchange_walk calls on every shard.  Speed
+     * only (each call may only lower thresholds to values >= the global k-th best). */
+    int32_t exchange_walk;
 } nn_opts;
 
 #define DTWLB_KEOGH_ONLY 1

@@ -36,7 +36,7 @@ EXCHANGE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int64, ctypes.c_v
 class NnOpts(ctypes.Structure):
     _fields_ = [("eps", ctypes.c_float), ("index_base", ctypes.c_int64), ("query_block", ctypes.c_int32),
                 ("flags", ctypes.c_int32), ("exchange", EXCHANGE_FN), ("exchange_user", ctypes.c_void_p),
-                ("db_env", ctypes.c_void_p), ("shards", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("db_env", ctypes.c_void_p), ("shards", ctypes.c_int32), ("exchange_walk", ctypes.c_int32)]
 
 
 class _DeviceArray:
@@ -190,9 +190,10 @@ def dtw_band(x: torch.Tensor, y: torch.Tensor, w: int, p: int) -> torch.Tensor:
 
 
 def _opts(eps, index_base, query_block, keogh_only, prefilter=True, cascade=True, exchange=None, stream=True,
-          db_env=None, shards=0):
+          db_env=None, shards=0, exchange_walk=0):
     o = NnOpts()
     o.shards = shards
+    o.exchange_walk = exchange_walk
     if exchange is not None:
         o.exchange = exchange
     o.eps = eps
@@ -207,7 +208,7 @@ def _opts(eps, index_base, query_block, keogh_only, prefilter=True, cascade=True
 def nn_search(queries, db, w: int, p: int, k: int, *, eps: float = 1e-3, index_base: int = 0,
               query_block: int = 0, keogh_only: bool = False, prefilter: bool = True, cascade: bool = True,
               stream: bool = True, db_env=None, exchange=None, out=None, shards: int = 0,
-              return_stats: bool = False):
+              exchange_walk: int = 0, return_stats: bool = False):
     """Exact k-NN under banded DTW_p.  Returns (idx int64 [Q][k], dist float32 [Q][k]).
 
     queries/db may be CUDA tensors (device path) or host tensors / numpy arrays
@@ -220,7 +221,9 @@ def nn_search(queries, db, w: int, p: int, k: int, *, eps: float = 1e-3, index_b
     database index: a [2][N][n] CUDA tensor holding lb_envelope(db, w) (U block, then L block),
     reused instead of being computed in the call.  ``shards`` (database-sharded search) is the
     number of shards the exchange combines: each shard's best-first seed range is 1/shards of
-    the single-database one (speed only).
+    the single-database one (speed only); ``exchange_walk`` (0..3) adds that many exchange calls
+    inside the last range's DTW walk (after its rounds 2, 4, 6): a block then makes
+    1 + exchange_walk calls on every shard.
     """
     host = not (isinstance(queries, torch.Tensor) and queries.is_cuda)
     if host:
@@ -243,7 +246,8 @@ def nn_search(queries, db, w: int, p: int, k: int, *, eps: float = 1e-3, index_b
         db_env = _dev(db_env, "db_env")
         if tuple(db_env.shape) != (2, N, n):
             raise ValueError(f"db_env must be [2][N][n] = [2][{N}][{n}], got {tuple(db_env.shape)}")
-    o = _opts(eps, index_base, query_block, keogh_only, prefilter, cascade, cb, stream, db_env, shards)
+    o = _opts(eps, index_base, query_block, keogh_only, prefilter, cascade, cb, stream, db_env, shards,
+              exchange_walk)
     st = NnStats()
     _check(load().nn_search(queries.data_ptr(), Q, db.data_ptr(), N, n, w, p, k, idx.data_ptr(),
                             dist.data_ptr(), ctypes.byref(o), ctypes.byref(st) if return_stats else None,

@@ -93,6 +93,11 @@ __device__ __forceinline__ unsigned long long pack_key(float d, uint32_t idx) {
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Start of query q's key list: exact-count lists (per-query offsets) or fixed capacity.
+__device__ __forceinline__ int64_t list_base(const int64_t *loff, int64_t cap, int64_t q) {
+    return loff ? __ldg(loff + q) : q * cap;
+}
+
 // ---- cp.async (global -> shared, no register staging); src_bytes < size zero-fills ----
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src_bytes) {
     unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));

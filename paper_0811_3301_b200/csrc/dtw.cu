@@ -401,8 +401,9 @@ dtw4_kernel(DtwArgs a) {
                         if (it < cend) {
                             while (it >= a.item_off[q + 1]) ++q;
                             const int64_t j = a.pos[q] + (it - a.item_off[q]);
-                            DCHECK(j >= 0 && j < a.cap, "dtw4 item %lld q=%d j=%lld", (long long)it, q, (long long)j);
-                            ckey[lane + 32 * t] = a.list[(int64_t)q * a.cap + j];
+                            DCHECK(j >= 0 && (a.loff ? a.loff[q] + j < a.loff[q + 1] : j < a.cap), "dtw4 item %lld q=%d j=%lld",
+                                   (long long)it, q, (long long)j);
+                            ckey[lane + 32 * t] = a.list[list_base(a.loff, a.cap, q) + j];
                             cq[lane + 32 * t] = q;
                         }
                     }
@@ -643,7 +644,7 @@ __global__ void dtw_generic_kernel(DtwArgs a, const float *__restrict__ yraw, fl
         int hi = a.Qb;
         while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (a.item_off[mid] <= item) lo = mid; else hi = mid; }
         const int64_t j = a.pos[lo] + (item - a.item_off[lo]);
-        const unsigned long long key = a.list[(int64_t)lo * a.cap + j];
+        const unsigned long long key = a.list[list_base(a.loff, a.cap, lo) + j];
         cand = (uint32_t)(key & 0xffffffffu);
         const float beta = __uint_as_float((uint32_t)(key >> 32));
         thr = *reinterpret_cast<volatile float *>(a.thr + lo);

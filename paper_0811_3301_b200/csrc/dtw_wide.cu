@@ -82,6 +82,12 @@ dtw_wide_kernel(DtwArgs a, const float *__restrict__ yp, int LPW, int padL) {
     float thr = kInf;
     const float *xr = nullptr, *yr = nullptr;
     float B[S], Y[NY], xc[4], xn[4], yn[4];
+    // cascading abandon (readings c15, c19; as dtw4_kernel): rest = LB_Keogh^p terms of the rows
+    // not yet computed = beta1 (from the gate slot) minus the terms of the rows lane 0 of the
+    // group has computed; rest_snap = its value after the checkpoint row (r & 7 == 7)
+    const bool casc = WALK && (a.b1 != nullptr || a.b1h != nullptr);
+    float rest = 0.f, rest_snap = 0.f;
+    const float *ur = nullptr, *lr = nullptr;
     float left_in = kInf, diag_in = kInf, segmin = kInf;
     unsigned long long n_cells = 0;
     unsigned n_started = 0, n_abandon = 0;
@@ -118,12 +124,19 @@ dtw_wide_kernel(DtwArgs a, const float *__restrict__ yp, int LPW, int padL) {
                         }
                         qy = lo;
                         const int64_t j = a.pos[qy] + (item - a.item_off[qy]);
-                        const unsigned long long key = a.list[(int64_t)qy * a.cap + j];
+                        const unsigned long long key = a.list[list_base(a.loff, a.cap, qy) + j];
                         cand = (uint32_t)(key & 0xffffffffu);
                         beta = __uint_as_float((uint32_t)(key >> 32));
                         thr = *reinterpret_cast<volatile float *>(a.thr + qy);
                         xr = a.db + (int64_t)cand * n;
                         yr = yp + (int64_t)qy * LPW;
+                        if (casc) {
+                            const int64_t gi = (int64_t)qy * a.ldb + cand;
+                            rest = fabsf(a.b1 ? __ldg(a.b1 + gi) : __half2float(a.b1h[gi]));
+                            rest_snap = rest;
+                            ur = a.Uq + (int64_t)qy * n;
+                            lr = a.Lq + (int64_t)qy * n;
+                        }
                     } else {
                         cand = (uint32_t)item;
                         thr = kInf;
@@ -238,6 +251,11 @@ dtw_wide_kernel(DtwArgs a, const float *__restrict__ yp, int LPW, int padL) {
                 if (t == 0) recv = kInf;
                 left_in = recv;
             }
+            if (casc && t == 0 && active) {
+                const float d = max3f(xc[u] - __ldg(ur + r), __ldg(lr + r) - xc[u], 0.f);
+                rest -= P == 1 ? d : (P == 4 ? (d * d) * (d * d) : d * d);
+                if ((r & 7) == 7) rest_snap = rest;
+            }
             const int ph = s + u - s0;  // group phase (uniform in the group)
             // ---- completion: the last lane finished row n-1 (the shuffles run warp-uniformly:
             //      every lane enters when any group completes)
@@ -270,6 +288,8 @@ dtw_wide_kernel(DtwArgs a, const float *__restrict__ yp, int LPW, int padL) {
                     float m = segmin;
                     m = fminf(m, __shfl_xor_sync(FULL, m, 1, KW));
                     m = fminf(m, __shfl_xor_sync(FULL, m, 2, KW));
+                    // + the LB_Keogh terms of the rows after the checkpoint row (lane 0's snapshot)
+                    if (casc) m += fmaxf(__shfl_sync(FULL, rest_snap, lane & ~3), 0.f);
                     if (busy && ph >= 10) {
                         thr = fminf(thr, *reinterpret_cast<volatile float *>(a.thr + qy));
                         if (m > thr) {

@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(256)
 select_mask_kernel(const T *__restrict__ gate, int64_t ldb, int64_t Qb, int64_t N,
                    const float *__restrict__ lo, const float *__restrict__ hi, const float *__restrict__ thr,
                    bool all, unsigned long long *__restrict__ tile_m, int *__restrict__ tile_q,
-                   int *__restrict__ tile_cnt, int64_t ntiles) {
+                   int *__restrict__ tile_cnt, int64_t ntiles, int *__restrict__ q_count) {
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t tt = gw % ntiles;   // tile
@@ -109,6 +109,7 @@ select_mask_kernel(const T *__restrict__ gate, int64_t ldb, int64_t Qb, int64_t 
         if (lane == j) { my_e = me; my_o = mo; }
     }
     const unsigned long long my_m = spread_bits(my_e) | (spread_bits(my_o) << 1);
+    if (q_count && my_m) atomicAdd(q_count + q0 + lane, __popcll(my_m));
     const unsigned has = __ballot_sync(0xffffffffu, my_m != 0);
     if (!has) return;
     int base = 0;
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(256)
 select_mask8_kernel(const __half *__restrict__ gate, int64_t ldb, int64_t Qb, int64_t N,
                     const float *__restrict__ lo, const float *__restrict__ hi, const float *__restrict__ thr,
                     bool all, unsigned long long *__restrict__ tile_m, int *__restrict__ tile_q,
-                    int *__restrict__ tile_cnt, int64_t ntiles) {
+                    int *__restrict__ tile_cnt, int64_t ntiles, int *__restrict__ q_count) {
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nst = (ntiles + 3) / 4;
@@ -179,6 +180,10 @@ select_mask8_kernel(const __half *__restrict__ gate, int64_t ldb, int64_t Qb, in
         for (int k = 0; k < 8; ++k) m[t] |= spread8(bk[k] >> (8 * t)) << k;
     }
 #pragma unroll
+    if (q_count && lane < nq) {  // the range's gate survivors of query q0 + lane in this super-tile
+        const int c = __popcll(m[0]) + __popcll(m[1]) + __popcll(m[2]) + __popcll(m[3]);
+        if (c) atomicAdd(q_count + q0 + lane, c);
+    }
     for (int t = 0; t < 4; ++t) {
         const int64_t tt = sti * 4 + t;
         const unsigned has = __ballot_sync(0xffffffffu, m[t] != 0ull);
@@ -402,8 +407,8 @@ __device__ __forceinline__ void append_keys(const ImprovedArgs &a, int64_t q, bo
     base = __shfl_sync(0xffffffffu, base, 0);
     if (pass) {
         const int pos = base + __popc(bal & ((1u << lane) - 1));
-        DCHECK(pos < a.cap, "list append q=%lld pos=%d", (long long)q, pos);
-        a.list[q * a.cap + pos] = pack_key(beta, (uint32_t)c);
+        DCHECK(a.loff ? a.loff[q] + pos < a.loff[q + 1] : pos < a.cap, "list append q=%lld pos=%d", (long long)q, pos);
+        a.list[list_base(a.loff, a.cap, q) + pos] = pack_key(beta, (uint32_t)c);
     }
 }
 
@@ -786,33 +791,43 @@ void improved_scratch_bind(ImprovedArgs &a, void *p) {
     a.tile_cnt = reinterpret_cast<int *>(c + (size_t)nt * a.Qb * 12);
 }
 
-int launch_improved(const ImprovedArgs &a, int p, bool keogh_only, bool dense, cudaStream_t st) {
+int launch_select(const ImprovedArgs &a, bool dense, cudaStream_t st) {
     if (a.Qb == 0 || a.N == 0) return DTWLB_OK;
     const int64_t ntiles = ceil_div(a.N, 64);
-    {   // per-tile (query, survivor mask) lists into the caller-provided scratch
-        DTWLB_CUDA(cudaMemsetAsync(a.tile_cnt, 0, sizeof(int) * ntiles, st));
-        const int64_t warps = ntiles * ceil_div(a.Qb, 32);
-        if (a.gate_half && a.ldb % 8 == 0) {
-            const int64_t warps8 = ceil_div(ntiles, 4) * ceil_div(a.Qb, 32);
-            select_mask8_kernel<<<(unsigned)ceil_div(warps8 * 32, 256), 256, 0, st>>>(
-                static_cast<const __half *>(a.gate), a.ldb, a.Qb, a.N, a.lo, a.hi, a.thr, dense, a.tile_m, a.tile_q,
-                a.tile_cnt, ntiles);
-        } else if (a.gate_half)
-            select_mask_kernel<__half><<<(unsigned)ceil_div(warps * 32, 256), 256, 0, st>>>(
-                static_cast<const __half *>(a.gate), a.ldb, a.Qb, a.N, a.lo, a.hi, a.thr, dense, a.tile_m, a.tile_q,
-                a.tile_cnt, ntiles);
-        else
-            select_mask_kernel<float><<<(unsigned)ceil_div(warps * 32, 256), 256, 0, st>>>(
-                static_cast<const float *>(a.gate), a.ldb, a.Qb, a.N, a.lo, a.hi, a.thr, dense, a.tile_m, a.tile_q,
-                a.tile_cnt, ntiles);
-        DTWLB_LAUNCH_CHECK();
-    }
+    // per-tile (query, survivor mask) lists into the caller-provided scratch
+    DTWLB_CUDA(cudaMemsetAsync(a.tile_cnt, 0, sizeof(int) * ntiles, st));
+    const int64_t warps = ntiles * ceil_div(a.Qb, 32);
+    if (a.gate_half && a.ldb % 8 == 0) {
+        const int64_t warps8 = ceil_div(ntiles, 4) * ceil_div(a.Qb, 32);
+        select_mask8_kernel<<<(unsigned)ceil_div(warps8 * 32, 256), 256, 0, st>>>(
+            static_cast<const __half *>(a.gate), a.ldb, a.Qb, a.N, a.lo, a.hi, a.thr, dense, a.tile_m, a.tile_q,
+            a.tile_cnt, ntiles, a.q_count);
+    } else if (a.gate_half)
+        select_mask_kernel<__half><<<(unsigned)ceil_div(warps * 32, 256), 256, 0, st>>>(
+            static_cast<const __half *>(a.gate), a.ldb, a.Qb, a.N, a.lo, a.hi, a.thr, dense, a.tile_m, a.tile_q,
+            a.tile_cnt, ntiles, a.q_count);
+    else
+        select_mask_kernel<float><<<(unsigned)ceil_div(warps * 32, 256), 256, 0, st>>>(
+            static_cast<const float *>(a.gate), a.ldb, a.Qb, a.N, a.lo, a.hi, a.thr, dense, a.tile_m, a.tile_q,
+            a.tile_cnt, ntiles, a.q_count);
+    DTWLB_LAUNCH_CHECK();
+    return DTWLB_OK;
+}
+
+int launch_survivor(const ImprovedArgs &a, int p, bool keogh_only, bool dense, cudaStream_t st) {
+    if (a.Qb == 0 || a.N == 0) return DTWLB_OK;
+    const int64_t ntiles = ceil_div(a.N, 64);
     const int epl = a.npadE / 32;
     if (a.ev0) DTWLB_CUDA(cudaEventRecord(a.ev0, st));
     const int rc = p == 1 ? launch_imp_p<1>(a, epl, keogh_only, dense, ntiles, st)
                           : launch_imp_p<2>(a, epl, keogh_only, dense, ntiles, st);
     if (a.ev1) DTWLB_CUDA(cudaEventRecord(a.ev1, st));
     return rc;
+}
+
+int launch_improved(const ImprovedArgs &a, int p, bool keogh_only, bool dense, cudaStream_t st) {
+    DTWLB_TRY(launch_select(a, dense, st));
+    return launch_survivor(a, p, keogh_only, dense, st);
 }
 
 }  // namespace dtwlb

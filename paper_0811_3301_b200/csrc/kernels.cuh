@@ -75,9 +75,12 @@ struct ImprovedArgs {
     const float *lo, *hi;          // per query: gate survivors satisfy lo < gate <= min(hi, thr)
     const float *thr;              // per query: tau^p (1+eps)  (may be NULL = +inf)
     // LIST mode outputs
-    unsigned long long *list;      // [Qb][cap] keys (beta_lb bits << 32 | c)
+    unsigned long long *list;      // keys (beta_lb bits << 32 | c): query q's at list[loff[q] ..
+                                   // loff[q + 1]) (loff set), else at list[q * cap ..)
     int64_t cap;
+    const int64_t *loff;           // [Qb + 1] per-query list offsets (exact-count lists), or NULL
     int *list_len;                 // [Qb]
+    int *q_count;                  // [Qb] select: gate survivors of the range per query (or NULL)
     // DENSE mode output
     float *dense;                  // [Qb][ldd], rooted
     int64_t ldd;
@@ -93,6 +96,10 @@ struct ImprovedArgs {
 size_t improved_scratch_bytes(int64_t Qb, int64_t N);
 void improved_scratch_bind(ImprovedArgs &a, void *p);
 int launch_improved(const ImprovedArgs &a, int p, bool keogh_only, bool dense, cudaStream_t st);
+// the two halves of launch_improved: the range's (query, survivor mask) tile lists (and the
+// per-query survivor counts when a.q_count is set), then the survivor kernel
+int launch_select(const ImprovedArgs &a, bool dense, cudaStream_t st);
+int launch_survivor(const ImprovedArgs &a, int p, bool keogh_only, bool dense, cudaStream_t st);
 int improved_epl(int n);  // elements per lane (4, 8, 16, 32); 0 if n > 1024 (unsupported fast path)
 
 // Banded DTW (a5).
@@ -110,8 +117,9 @@ struct DtwArgs {
     const int *chunk_off;  // [Qb+1] prefix offsets of this round's warp chunks per query
     int64_t nchunks;       // WALK: number of warp chunks (kDtwIpw items of one query each)
     const int *pos;        // [Qb] list position of the query's first item this round
-    const unsigned long long *list;  // [Qb][cap]
+    const unsigned long long *list;  // query q's keys at list[loff[q] ..) (loff set) or list[q * cap ..)
     int64_t cap;
+    const int64_t *loff;
     int Qb;
     float *thr;            // [Qb] tau^p (1+eps); WALK: lowered by walk_result as the top-k fills
     int64_t total;         // number of items (WALK with dev_total: an upper bound, see below)

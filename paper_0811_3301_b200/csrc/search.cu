@@ -220,7 +220,52 @@ __global__ void __launch_bounds__(1024) make_runs_kernel(const int *__restrict__
     if (threadIdx.x == 0) *nruns = carry;
 }
 
+// Exact-count key lists: off[q] = sum_{q' < q} cnt[q'] (int64), off[Qb] = the total, off[Qb + 1] =
+// the largest count.  One CTA.
+__global__ void __launch_bounds__(1024) list_offsets_kernel(const int *__restrict__ cnt, int Qb,
+                                                            int64_t *__restrict__ off) {
+    __shared__ long long warp_sums[32];
+    __shared__ long long carry;
+    __shared__ int mx;
+    if (threadIdx.x == 0) { carry = 0; mx = 0; }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int base = 0; base < Qb; base += blockDim.x) {
+        const int q = base + threadIdx.x;
+        const long long m = q < Qb ? cnt[q] : 0;
+        if (m) atomicMax(&mx, (int)m);
+        long long v = m;  // inclusive scan
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += t;
+        }
+        if (lane == 31) warp_sums[wid] = v;
+        __syncthreads();
+        if (wid == 0) {
+            long long u = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long t = __shfl_up_sync(0xffffffffu, u, o);
+                if (lane >= o) u += t;
+            }
+            warp_sums[lane] = u;
+        }
+        __syncthreads();
+        const long long ex = carry + v - m + (wid ? warp_sums[wid - 1] : 0);
+        if (q < Qb) off[q] = ex;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry = ex + m;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        off[Qb] = carry;
+        off[Qb + 1] = mx;
+    }
+}
+
 __global__ void __launch_bounds__(kSortThreads) sort_runs_kernel(unsigned long long *__restrict__ list, int64_t cap,
+                                                                 const int64_t *__restrict__ loff,
                                                                  const int *__restrict__ run_q,
                                                                  const int *__restrict__ run_idx,
                                                                  const int *__restrict__ len,
@@ -230,9 +275,10 @@ __global__ void __launch_bounds__(kSortThreads) sort_runs_kernel(unsigned long l
     const int nr = *nruns;
     for (int t = blockIdx.x; t < nr; t += gridDim.x) {
     const int q = run_q[t], r = run_idx[t];
-    const int64_t base = (int64_t)q * cap + (int64_t)r * kRun;
+    const int64_t base = list_base(loff, cap, q) + (int64_t)r * kRun;
     const int m = min(kRun, len[q] - r * kRun);
-    DCHECK(m > 0 && (int64_t)r * kRun + m <= cap, "sort q=%d r=%d m=%d cap=%lld", q, r, m, (long long)cap);
+    DCHECK(m > 0 && (loff ? base + m <= loff[q + 1] : (int64_t)r * kRun + m <= cap), "sort q=%d r=%d m=%d cap=%lld",
+           q, r, m, (long long)cap);
     unsigned key[kSortItems], val[kSortItems];
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
@@ -257,7 +303,7 @@ __global__ void __launch_bounds__(kSortThreads) sort_runs_kernel(unsigned long l
 // a warp takes four keys at a time, lane l & 7 covers the columns 4 (l & 7) .. + 3 (c0 <= 32).
 template <int P>
 __global__ void __launch_bounds__(256) rest0_kernel(const unsigned long long *__restrict__ list, int64_t cap,
-                                                    const int *__restrict__ run_q, const int *__restrict__ run_idx,
+                                                    const int64_t *__restrict__ loff, const int *__restrict__ run_q, const int *__restrict__ run_idx,
                                                     const int *__restrict__ len, const int *__restrict__ nruns,
                                                     const float *__restrict__ yq,
                                                     const float *__restrict__ LUq, const float *__restrict__ ULq,
@@ -275,7 +321,7 @@ __global__ void __launch_bounds__(256) rest0_kernel(const unsigned long long *__
         lu = __ldg(reinterpret_cast<const float4 *>(LUq + (int64_t)q * n + 4 * src));
         ul = __ldg(reinterpret_cast<const float4 *>(ULq + (int64_t)q * n + 4 * src));
     }
-    const unsigned long long *lq = list + (int64_t)q * cap + (int64_t)r * kRun;
+    const unsigned long long *lq = list + list_base(loff, cap, q) + (int64_t)r * kRun;
     for (int j0 = warp * 4; j0 < m; j0 += (blockDim.x >> 5) * 4) {
         const int j = j0 + grp;
         float s = 0.f, beta = 0.f;
@@ -313,6 +359,8 @@ struct QState {
     int *lock;                 // [Qb] top-k insertion locks (dtw.cu walk_result)
     int *prev_cnt;             // [Qb] items of the query in the previous walk round
     unsigned long long *stat;  // [0] improved evals, [1] dtw items started, [2] cells, [3] abandoned
+    int *q_count;              // [Qb] the range's gate survivors per query (select kernel)
+    int64_t *loff;             // [Qb + 1] offsets of the range's exact-count key lists
 };
 
 __global__ void init_state_kernel(QState s, int Qb, int k) {
@@ -328,6 +376,7 @@ __global__ void set_range_kernel(QState s, int Qb, int macro, int R) {
         s.lo[q] = macro == 0 ? -kInf : s.tS[(int64_t)(macro - 1) * Qb + q];
         s.hi[q] = macro == R - 1 ? kInf : s.tS[(int64_t)macro * Qb + q];
         s.len[q] = 0;
+        s.q_count[q] = 0;
     }
 }
 
@@ -376,7 +425,8 @@ __device__ __forceinline__ int2 block_scan2(int2 v, int2 *warp_sums, int2 &total
 // into the top-k and tau directly): the walk advances past them and skips the rest of
 // a sorted run once its next bound exceeds tau (1+eps).
 __global__ void __launch_bounds__(1024) plan_kernel(QState s, int Qb, const unsigned long long *__restrict__ list,
-                                                    int64_t cap, bool sorted, int d0, int gs) {
+                                                    int64_t cap, const int64_t *__restrict__ loff, bool sorted, int d0,
+                                                    int gs) {
     __shared__ int2 warp_sums[32];
     int2 carry = make_int2(0, 0);
     for (int base = 0; base < Qb; base += blockDim.x) {
@@ -388,7 +438,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(QState s, int Qb, const unsi
             if (s.prev_cnt[q] > 0 && sorted) {
                 s.rnd[q] += 1;
                 const float thr = *reinterpret_cast<volatile float *>(s.thr + q);
-                const unsigned long long *lq = list + (int64_t)q * cap;
+                const unsigned long long *lq = list + list_base(loff, cap, q);
                 while (pos < len && __uint_as_float((uint32_t)(lq[pos] >> 32)) > thr)
                     pos = (pos / kRun + 1) * kRun;
             }
@@ -602,7 +652,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     }
     tm.mark();  // 1
 
-    // ---- query block size from free memory: gate bound (4N) + list (8N) per query ----
+    // ---- query block size from free memory ----
     const int qb_mode = (prefilter ? 1 : 0) | (keogh_only ? 2 : 0) | (stream_mode ? 4 : 0);
     const int64_t qb_hit = (opts && opts->query_block > 0) ? 0 : ws().cached_qb(Q, N, n, qb_mode);
     size_t free_b = 0, total_b = 0;
@@ -610,14 +660,17 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         DTWLB_CUDA(cudaMemGetInfo(&free_b, &total_b));
         // the block-sized slots this call would reuse count as free: the block size (hence the
         // pipeline) is then the same on every call of a given problem, not smaller after the first
-        for (int sl : {S_BETA1, S_LIST, S_RES, S_MASK}) free_b += ws().cur_size(sl);
+        for (int sl : {S_BETA1, S_LIST, S_RES, S_MASK, S_COUNT}) free_b += ws().cur_size(sl);
     }
-    // per query of the block: gate bound (2 B fp16 with the pre-filter, else 4 B) + key list (8 B)
-    // per pair, a walk round's completed-pair slots (12 B per item, <= min(N, kDMax) items),
-    // the survivor pass's (query, mask) entries (12 B per 64-candidate tile) and the sort's runs
+    // per query of the block: gate bound (2 B fp16 with the pre-filter, else 4 B) per pair, a
+    // walk round's completed-pair slots (12 B per item, <= min(N, kDMax) items), the survivor
+    // pass's (query, mask) entries (12 B per 64-candidate tile), and a budget for the key lists:
+    // those are sized per range by the exact survivor count (8 B per gate survivor of the range,
+    // list pool below); the budget assumes <= 1/8 of the pairs survive a range's gate on
+    // average (C5: 3.8 %) -- a block whose lists do not fit is redone as two half blocks
     const size_t gate_elem = prefilter ? 2 : 4;
     const int64_t round_items = std::min<int64_t>(N, kDMax);
-    const size_t per_q = (size_t)N * (gate_elem + 8) + (size_t)round_items * 12 + (size_t)ceil_div(N, 64) * 12 +
+    const size_t per_q = (size_t)N * gate_elem + (size_t)N + (size_t)round_items * 12 + (size_t)ceil_div(N, 64) * 12 +
                          (size_t)ceil_div(N, kRun) * 8 + 4096;
     static const double env_mem = [] { const char *e = getenv("DTWLB_BLOCK_MEM_FRAC"); return e ? atof(e) : 0.0; }();
     // (0.6 of the free memory: one 8192-query block at C5, measured 274 vs 281 ms for 2 x 4096)
@@ -638,20 +691,19 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     const int64_t ldb = (N + 7) / 8 * 8;  // 16-byte rows of the fp16 gate block
 
     float *beta1;
-    unsigned long long *list;
+    unsigned long long *list = nullptr;  // the range's exact-count key lists (pool, S_LIST)
     {   // float, or __half with the pre-filter
         void *g = nullptr;
         DTWLB_TRY(ws().get(S_BETA1, (size_t)Qb * ldb * gate_elem, &g));
         beta1 = static_cast<float *>(g);
     }
-    DTWLB_TRY(wsget(S_LIST, (size_t)Qb * cap, &list));
     const int64_t res_cap = Qb * round_items;  // items of one walk round (< 2^31, see Qb)
     char *rbuf;  // completed pairs of a round: keys [res_cap] u64 + queries [res_cap] int
     DTWLB_TRY(wsget(S_RES, (size_t)res_cap * 12 + 64, &rbuf));
     char *imp_scratch;
     DTWLB_TRY(wsget(S_MASK, improved_scratch_bytes(Qb, N), &imp_scratch));
     char *stb;
-    const size_t st_bytes = (size_t)Qb * 4 * (10 + kMaxRanges) + (Qb + 1) * 8 + 64 + 64 + 16 * 16;
+    const size_t st_bytes = (size_t)Qb * 4 * (11 + kMaxRanges) + (Qb + 2) * 8 * 2 + 64 + 64 + 16 * 16;
     DTWLB_TRY(wsget(S_STATE, st_bytes, &stb));
     QState s;
     {
@@ -671,6 +723,8 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         s.prev_cnt = reinterpret_cast<int *>(take(Qb * 4));
         s.item_off = reinterpret_cast<int *>(take((Qb + 1) * 4));
         s.chunk_off = reinterpret_cast<int *>(take((Qb + 1) * 4));
+        s.q_count = reinterpret_cast<int *>(take(Qb * 4));
+        s.loff = reinterpret_cast<int64_t *>(take((Qb + 2) * 8));
     }
     DTWLB_TRY(wsget(S_TOPK, (size_t)Qb * k, &s.topk));
     DTWLB_CUDA(cudaMemsetAsync(s.stat, 0, 8 * 8, st));
@@ -690,11 +744,10 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     const int R = std::min(kMaxRanges, std::max(2, env_R > 0 ? env_R : 2));
     const int G = std::max(2, env_G > 0 ? env_G : 8);
 
-    // run lists of the sort: at most Qb * ceil(cap / kRun) runs of (query, index), + the count
-    const int64_t max_runs = Qb * ceil_div(cap, kRun);
-    int *d_runs;
-    DTWLB_TRY(wsget(S_COUNT, (size_t)max_runs * 2 + 64, &d_runs));
-    int *d_nruns = d_runs + 2 * max_runs;
+    // run lists of the sort: at most sum_q ceil(len_q / kRun) <= Qb + total / kRun runs of
+    // (query, index), + the count; sized per range with the lists
+    int64_t max_runs = 0;
+    int *d_runs = nullptr, *d_nruns = nullptr;
     double ms_keogh = 0, ms_select = 0, ms_improved = 0, ms_dtw = 0, ms_survivor = 0, ms_dtw_kernel = 0;
     int64_t walk_rounds = 0;
     // stats: CUDA-event spans resolved after the call's final synchronisation (no host waits
@@ -704,13 +757,21 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     auto new_ev = [&]() { cudaEvent_t e; cudaEventCreate(&e); evpool.push_back(e); return e; };
     auto rec = [&]() { cudaEvent_t e = new_ev(); cudaEventRecord(e, st); return e; };
     auto span = [&](cudaEvent_t a, cudaEvent_t b, double *acc) { spans.emplace_back(a, b, acc); };
-    const int64_t nblocks = ceil_div(Q, Qb);
-    unsigned long long *snap = nullptr;  // [nblocks][2][4]: stat after range 1, after the last range
-    if (stats) DTWLB_TRY(wsget(S_SNAP, (size_t)nblocks * 8, &snap));
+    // blocks actually run (a block whose key lists do not fit is redone as two half blocks)
+    const int64_t snap_cap = 4 * ceil_div(Q, Qb) + 64;
+    int64_t nblocks = 0;
+    unsigned long long *snap = nullptr;  // [blocks][2][4]: stat after range 1, after the last range
+    if (stats) DTWLB_TRY(wsget(S_SNAP, (size_t)snap_cap * 8 + 8, &snap));
+    unsigned long long *stat_save = stats ? snap + snap_cap * 8 : nullptr;  // stat at the block start
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
 
-    for (int64_t qb0 = 0; qb0 < Q; qb0 += Qb) {
-        const int64_t qn = std::min<int64_t>(Qb, Q - qb0);
+    int64_t Qcur = Qb;  // current block size
+    int64_t rcap = cap;               // the range's list capacity per query (uniform lists)
+    const int64_t *loff_r = nullptr;  // or its exact per-query offsets
+    for (int64_t qb0 = 0; qb0 < Q;) {
+        const int64_t qn = std::min<int64_t>(Qcur, Q - qb0);
+        bool redo = false;  // the range's key lists did not fit: redo this block as two halves
+        if (stats) DTWLB_CUDA(cudaMemcpyAsync(stat_save, s.stat, 64, cudaMemcpyDeviceToDevice, st));
         // ---- dense gate pass for the block: the piecewise-sum bound beta0 (pre-filter,
         //      LB_Keogh then runs on its survivors inside the survivor pass), or a2 itself ----
         if (stats) ev0 = rec();
@@ -777,14 +838,48 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 ia.lo = s.lo;
                 ia.hi = s.hi;
                 ia.thr = s.thr;
-                ia.list = list;
                 ia.cap = cap;
+                ia.loff = nullptr;  // (set below with the lists)
+                ia.q_count = s.q_count;
                 ia.list_len = s.len;
                 ia.n_eval = s.stat + 0;
                 ia.n_entries = s.stat + 5;
                 if (stats) { ev_s0 = new_ev(); ev_s1 = new_ev(); ia.ev0 = ev_s0; ia.ev1 = ev_s1; }
                 improved_scratch_bind(ia, imp_scratch);
-                DTWLB_TRY(launch_improved(ia, p, keogh_only, false, st));
+                DTWLB_TRY(launch_select(ia, false, st));
+                // exact-count key lists: the range's gate survivors per query bound its keys
+                list_offsets_kernel<<<1, 1024, 0, st>>>(s.q_count, (int)qn, s.loff);
+                DTWLB_LAUNCH_CHECK();
+                int64_t tm2[2] = {0, 0};  // total keys, largest count
+                DTWLB_CUDA(cudaMemcpyAsync(tm2, s.loff + qn, sizeof(tm2), cudaMemcpyDeviceToHost, st));
+                DTWLB_CUDA(cudaStreamSynchronize(st));
+                const int64_t total = tm2[0];
+                // lists of a uniform capacity (the range's largest count: the survivor kernel's
+                // append then needs no per-query offset load, measured 84 vs 92 ms at C5), or
+                // exact per-query offsets when the uniform ones do not fit
+                rcap = std::max<int64_t>(tm2[1], 1);
+                loff_r = nullptr;
+                if (wsget(S_LIST, (size_t)qn * rcap, &list) != DTWLB_OK) {
+                    cudaGetLastError();
+                    loff_r = s.loff;
+                }
+                const int64_t nkeys = loff_r ? total : qn * rcap;
+                max_runs = qn + nkeys / kRun + 1;
+                // (DTWLB_LIST_POOL_MAX: a cap on the pool in keys, to exercise the redo path in tests)
+                static const long long pool_max = [] { const char *e = getenv("DTWLB_LIST_POOL_MAX"); return e ? atoll(e) : 0LL; }();
+                const bool over = pool_max > 0 && nkeys > pool_max;
+                if (over) set_error(DTWLB_ENOMEM, "key lists of %lld keys exceed DTWLB_LIST_POOL_MAX", (long long)total);
+                if (over || (loff_r && wsget(S_LIST, (size_t)std::max<int64_t>(total, 1), &list) != DTWLB_OK) ||
+                    wsget(S_COUNT, (size_t)max_runs * 2 + 64, &d_runs) != DTWLB_OK) {
+                    if (qn == 1 || (opts && opts->exchange)) return DTWLB_ENOMEM;  // (error set by wsget)
+                    redo = true;
+                    break;
+                }
+                d_nruns = d_runs + 2 * max_runs;
+                ia.list = list;
+                ia.cap = rcap;
+                ia.loff = loff_r;
+                DTWLB_TRY(launch_survivor(ia, p, keogh_only, false, st));
             } else {
                 set_error(DTWLB_EUNSUPPORTED, "nn_search: n = %d > 1024 not supported", n);
                 return DTWLB_EUNSUPPORTED;
@@ -798,13 +893,13 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 DTWLB_LAUNCH_CHECK();
                 const unsigned grid = (unsigned)std::min<int64_t>(max_runs, 148 * 8);
                 if (sorted) {
-                    sort_runs_kernel<<<grid, kSortThreads, 0, st>>>(list, cap, d_runs, d_runs + max_runs, s.len,
-                                                                    d_nruns);
+                    sort_runs_kernel<<<grid, kSortThreads, 0, st>>>(list, rcap, loff_r, d_runs, d_runs + max_runs,
+                                                                    s.len, d_nruns);
                     DTWLB_LAUNCH_CHECK();
                 }
                 if (col_c0 > 0) {  // row+column cascade start values (reading c21)
                     auto rk = p == 1 ? rest0_kernel<1> : rest0_kernel<2>;
-                    rk<<<grid, 256, 0, st>>>(list, cap, d_runs, d_runs + max_runs, s.len, d_nruns, queries + qb0 * n,
+                    rk<<<grid, 256, 0, st>>>(list, rcap, loff_r, d_runs, d_runs + max_runs, s.len, d_nruns, queries + qb0 * n,
                                              LU + qb0 * n, UL + qb0 * n, dbenv, dbenv + (size_t)N * n, n, col_c0,
                                              reinterpret_cast<__half *>(beta1), ldb);
                     DTWLB_LAUNCH_CHECK();
@@ -819,9 +914,16 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
             // check per batch; the generic kernel sizes its grid from it (one check per round).
             const bool dev_rounds = !generic_dtw;  // (w <= 64: the dtw4 kernels)
             const int batch = dev_rounds ? kRoundBatch : 1;
+            // shard threshold exchanges inside the last range's walk (nn_opts.exchange_walk):
+            // after its rounds 2, 4, .., 2 * ex_walk; calls left when the walk ends early are made
+            // after it, so every shard makes the same number of calls per block
+            const int ex_walk = (opts && opts->exchange && macro == R - 1 && macro > 0)
+                                    ? std::max(0, std::min(3, (int)opts->exchange_walk)) : 0;
+            int range_round = 0, ex_done = 0;
             for (bool walking = true; walking;) {
                 for (int b = 0; b < batch && walking; ++b) {
                     ++walk_rounds;
+                    ++range_round;
                     static const int env_d0 = [] { const char *e = getenv("DTWLB_D0"); return e ? atoi(e) : 0; }();
                     // batch per query and round: kD0 << (round * gs).  The first round stays small (its
                     // pairs run with tau = +inf: none is abandoned, and every completed pair is merged
@@ -830,7 +932,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                     // round instead of 2x (fewer, fuller rounds)
                     const int d0 = env_d0 > 0 ? env_d0 : kD0;
                     const int gs = qn <= 64 ? 3 : 1;
-                    plan_kernel<<<1, 1024, 0, st>>>(s, (int)qn, list, cap, sorted, d0, gs);
+                    plan_kernel<<<1, 1024, 0, st>>>(s, (int)qn, list, rcap, loff_r, sorted, d0, gs);
                     DTWLB_LAUNCH_CHECK();
                     int tot2[2] = {0, 0};
                     if (!dev_rounds) {
@@ -851,7 +953,8 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                     da.nchunks = tot2[1];
                     da.pos = s.pos;
                     da.list = list;
-                    da.cap = cap;
+                    da.cap = rcap;
+                    da.loff = loff_r;
                     da.Qb = (int)qn;
                     da.thr = s.thr;
                     da.topk = s.topk;
@@ -903,8 +1006,30 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                         const cudaEvent_t d0 = stats ? rec() : nullptr;
                         DTWLB_TRY(launch_dtw(da, p, true, st));
                         if (stats) span(d0, rec(), &ms_dtw_kernel);
+                        static const bool dbg_rounds = [] { const char *e = getenv("DTWLB_DEBUG_ROUNDS"); return e && atoi(e); }();
+                        if (stats && dbg_rounds) {  // per-round items, time and cells (debug: syncs)
+                            const cudaEvent_t d1 = evpool.back();
+                            DTWLB_CUDA(cudaStreamSynchronize(st));
+                            float ms_r = 0;
+                            cudaEventElapsedTime(&ms_r, d0, d1);
+                            int c2[2];
+                            unsigned long long h4[4];
+                            DTWLB_CUDA(cudaMemcpy(c2, s.counters, sizeof(c2), cudaMemcpyDeviceToHost));
+                            DTWLB_CUDA(cudaMemcpy(h4, s.stat, sizeof(h4), cudaMemcpyDeviceToHost));
+                            static unsigned long long prev[4] = {0, 0, 0, 0};
+                            if (h4[1] < prev[1]) prev[0] = prev[1] = prev[2] = prev[3] = 0;  // a new call
+                            fprintf(stderr, "[dtwlb] range %d round %lld: items %d, %.3f ms, started %llu, cells %llu, abandoned %llu, %.3g cells/s\n",
+                                    macro, (long long)walk_rounds, c2[0], ms_r, h4[1] - prev[1], h4[2] - prev[2],
+                                    h4[3] - prev[3], ms_r > 0 ? (double)(h4[2] - prev[2]) / (ms_r * 1e-3) : 0.0);
+                            for (int j = 0; j < 4; ++j) prev[j] = h4[j];
+                        }
                     }
                     DTWLB_TRY(launch_topk_merge(da, st));  // a6: the round's completed pairs -> top-k, tau
+                    if (ex_done < ex_walk && range_round == 2 * (ex_done + 1)) {
+                        opts->exchange(s.thr, qn, opts->exchange_user);  // (stream-ordered)
+                        DTWLB_CUDA(cudaGetLastError());
+                        ++ex_done;
+                    }
                 }
                 if (dev_rounds && walking) {  // one host check per batch: did the last round have items?
                     int tot0 = 0;
@@ -912,6 +1037,10 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                     DTWLB_CUDA(cudaStreamSynchronize(st));
                     walking = tot0 > 0;
                 }
+            }
+            for (; ex_done < ex_walk; ++ex_done) {  // the walk ended before its scheduled exchanges
+                opts->exchange(s.thr, qn, opts->exchange_user);
+                DTWLB_CUDA(cudaGetLastError());
             }
             if (opts && opts->exchange && macro + 1 < R) {
                 // a7: shard threshold exchange after the best-first range (stream-ordered)
@@ -923,13 +1052,22 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 span(ev0, ev1, &ms_improved);
                 span(ev1, e2, &ms_dtw);
                 if (macro == 0 || macro == R - 1)  // cumulative counters after range 1 / the block
-                    DTWLB_CUDA(cudaMemcpyAsync(snap + (qb0 / Qb) * 8 + (macro == 0 ? 0 : 4), s.stat, 32,
+                    if (nblocks < snap_cap)
+                    DTWLB_CUDA(cudaMemcpyAsync(snap + nblocks * 8 + (macro == 0 ? 0 : 4), s.stat, 32,
                                                cudaMemcpyDeviceToDevice, st));
             }
+        }
+        if (redo) {  // undo the block's counters, then redo it as two half blocks
+            if (stats) DTWLB_CUDA(cudaMemcpyAsync(s.stat, stat_save, 64, cudaMemcpyDeviceToDevice, st));
+            cudaGetLastError();
+            Qcur = std::max<int64_t>(1, qn / 2);
+            continue;
         }
         finalize_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(qn * k, 256), 4096)), 256, 0, st>>>(
             s.topk, (int)qn, k, p, index_base, out_idx + qb0 * k, out_dist + qb0 * k);
         DTWLB_LAUNCH_CHECK();
+        qb0 += qn;
+        ++nblocks;
     }
     if (!out_dev) {
         DTWLB_CUDA(cudaMemcpyAsync(out_idx_in, out_idx, sizeof(int64_t) * Q * k, cudaMemcpyDeviceToHost, st));
@@ -963,10 +1101,11 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
             *std::get<2>(sp) += t;
         }
         for (auto &e : evpool) cudaEventDestroy(e);
-        std::vector<unsigned long long> hs((size_t)nblocks * 8);
-        DTWLB_CUDA(cudaMemcpy(hs.data(), snap, hs.size() * 8, cudaMemcpyDeviceToHost));
+        const int64_t nsnap = std::min(nblocks, snap_cap);
+        std::vector<unsigned long long> hs((size_t)std::max<int64_t>(nsnap, 1) * 8);
+        if (nsnap) DTWLB_CUDA(cudaMemcpy(hs.data(), snap, (size_t)nsnap * 64, cudaMemcpyDeviceToHost));
         unsigned long long r1[3] = {0, 0, 0};
-        for (int64_t b = 0; b < nblocks; ++b)
+        for (int64_t b = 0; b < nsnap; ++b)
             for (int j = 0; j < 3; ++j) r1[j] += hs[b * 8 + j] - (b ? hs[(b - 1) * 8 + 4 + j] : 0ull);
         unsigned long long h[8];
         DTWLB_CUDA(cudaMemcpy(h, s.stat, sizeof(h), cudaMemcpyDeviceToHost));

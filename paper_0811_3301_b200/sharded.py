@@ -23,6 +23,11 @@ from typing import Callable, Optional
 import torch
 import torch.distributed as dist
 
+# threshold exchanges inside the last range's DTW walk (nn_opts.exchange_walk: after its rounds
+# 2, 4, 6) on top of the one after the best-first range: within the last range each shard's
+# threshold otherwise tightens only from its own 1/G of the candidates
+EXCHANGE_WALK = 3
+
 
 def shard_range(N: int, world: int, rank: int):
     """Contiguous, balanced rows [lo, hi) of rank `rank` (sizes differ by at most 1)."""
@@ -67,6 +72,7 @@ def sharded_nn_search(queries: torch.Tensor, db_shard: torch.Tensor, shard_lo: i
         # all ranks use the same blocking; thresholds are min-reduced after each block's first range
         kw["query_block"] = query_block or common_query_block(db_shard.shape[0], group, dev)
         kw["shards"] = world  # each shard seeds from 1/world of the best-first range
+        kw["exchange_walk"] = EXCHANGE_WALK  # + exchanges inside the last range's walk
         if kk >= k:
             kw["exchange"] = lambda thr: dist.all_reduce(thr, op=dist.ReduceOp.MIN, group=group)
         else:
@@ -88,7 +94,8 @@ def sharded_nn_search(queries: torch.Tensor, db_shard: torch.Tensor, shard_lo: i
         if world > 1:  # an empty shard still takes part in every block's threshold exchange
             qb = kw["query_block"]
             for b0 in range(0, Q, qb):
-                kw["exchange"](torch.full((min(qb, Q - b0),), float("inf"), dtype=torch.float32, device=dev))
+                for _ in range(1 + kw["exchange_walk"]):  # the calls every other shard makes per block
+                    kw["exchange"](torch.full((min(qb, Q - b0),), float("inf"), dtype=torch.float32, device=dev))
     if kk < k:  # pad to k
         pad_i = torch.full((Q, k - kk), -1, dtype=torch.int64, device=dev)
         pad_d = torch.full((Q, k - kk), float("inf"), dtype=torch.float32, device=dev)

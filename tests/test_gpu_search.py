@@ -240,3 +240,48 @@ def test_wide_band_walk(cuda_ok, name, Q, N, w):
     g_idx, g_dist = run(qs, db, w, c.p, k)
     o_idx, o_dist, _ = oracle.nn_twopass(qs, db, w, c.p, k + EXTRA, threads=THREADS)
     assert_knn_match(g_idx, g_dist, o_idx, o_dist, k)
+
+
+@pytest.mark.parametrize("name", ["C5", "C3", "C4"])
+def test_full_size_oracle_cache(cuda_ok, name):
+    """Full BASELINE size, bench.py's launch configuration, against the oracle-result cache
+    (tests/golden/oracle_knn_<cfg>.npz, written by scripts/oracle_cache.py from oracle/ only:
+    Alg. 3 fp64 scan, 256 sampled queries); two cached queries are re-verified live."""
+    from paper_0811_3301_b200 import nn_search
+    path = os.path.join(os.path.dirname(__file__), "golden", f"oracle_knn_{name}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"no oracle cache for {name} (python scripts/oracle_cache.py {name})")
+    g = np.load(path)
+    c = datagen.CONFIGS[name]
+    assert (int(g["Q"]), int(g["N"]), int(g["n"]), int(g["w"]), int(g["p"]), int(g["seed"])) == \
+        (c.Q, c.N, c.n, c.w, c.p, c.seed), "stale cache: config changed"
+    qs, db = datagen.make(c)
+    rows = g["rows"]
+    live = rows[[1, len(rows) // 2]]  # re-verify a subset of the cache against the oracle itself
+    l_idx, l_dist, _ = oracle.nn_twopass(qs[live], db, c.w, c.p, int(g["k"]), threads=THREADS)
+    pos = [int(np.searchsorted(rows, r)) for r in live]
+    assert np.array_equal(l_idx, g["idx"][pos]) and np.array_equal(l_dist, g["dist"][pos])
+    idx, dist = nn_search(dev(qs), dev(db), c.w, c.p, c.k)
+    idx, dist = idx.cpu().numpy(), dist.cpu().numpy()
+    assert_knn_match(idx[rows], dist[rows], g["idx"], g["dist"], c.k)
+
+
+def test_key_list_pool_redo(cuda_ok):
+    """Exact-count key lists: a range whose lists exceed the pool (DTWLB_LIST_POOL_MAX, read once
+    per process -> a subprocess) makes nn_search redo the query block as two half blocks, down to
+    blocks that fit; the result is unchanged."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import datagen, oracle\n"
+        "from knn_compare import assert_knn_match\n"
+        "from paper_0811_3301_b200 import nn_search\n"
+        "qs, db = datagen.make('C2p2', Q=40, N=6000)\n"
+        "idx, dist = nn_search(torch.from_numpy(qs).cuda(), torch.from_numpy(db).cuda(), 25, 2, 5, query_block=40)\n"
+        "o_idx, o_dist = oracle.nn_brute(qs, db, 25, 2, 13, threads=8)\n"
+        "assert_knn_match(idx.cpu().numpy(), dist.cpu().numpy(), o_idx, o_dist, 5)\n"
+        "print('ok')\n") % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.dirname(__file__))
+    env = dict(os.environ, DTWLB_LIST_POOL_MAX="3000")  # ~40 queries x 6000 x a few % survive per range
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr

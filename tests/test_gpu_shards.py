@@ -27,39 +27,44 @@ def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
 
 
-def emulate(qs, db, w, p, k, bounds, query_block=8):
+def emulate(qs, db, w, p, k, bounds, query_block=8, walk=0):
     """G logical shards [bounds[g], bounds[g+1]) searched one after the other; returns the
-    merged (idx, dist) from nn_merge and the number of threshold entries the exchange lowered."""
+    merged (idx, dist) from nn_merge and the number of threshold entries the exchange lowered.
+    walk = nn_opts.exchange_walk: each block makes 1 + walk exchange calls (phase = call index
+    within the block), each phase with its own running minimum over the shards."""
     from paper_0811_3301_b200 import nn_merge, nn_search
     Q = qs.shape[0]
     G = len(bounds) - 1
     q_t = dev(qs)
-    shared = torch.full((Q,), float("inf"), dtype=torch.float32, device="cuda")
+    shared = torch.full((1 + walk, Q), float("inf"), dtype=torch.float32, device="cuda")
     lowered = [0]
     g_idx = torch.empty((G, Q, k), dtype=torch.int64, device="cuda")
     g_dst = torch.empty((G, Q, k), dtype=torch.float32, device="cuda")
     for g in range(G):
         lo, hi = bounds[g], bounds[g + 1]
         kk = min(k, hi - lo)
-        pos = [0]
+        pos = [0] * (1 + walk)
+        calls = [0]
 
-        def exchange(thr, kk=kk):
+        def exchange(thr, kk=kk, pos=pos, calls=calls):
             n = thr.numel()
-            view = shared[pos[0]:pos[0] + n]
+            ph = calls[0] % (1 + walk)
+            calls[0] += 1
+            view = shared[ph, pos[ph]:pos[ph] + n]
             before = thr.clone()
             if kk == k:  # a shard with fewer than k rows contributes +inf (sharded.py)
                 torch.minimum(view, thr, out=view)
             torch.minimum(thr, view, out=thr)
             lowered[0] += int((thr < before).sum().item())
-            pos[0] += n
+            pos[ph] += n
 
         if kk == 0:
             g_idx[g].fill_(-1)
             g_dst[g].fill_(float("inf"))
             continue
         idx, dst = nn_search(q_t, dev(db[lo:hi]), w, p, kk, index_base=lo, query_block=query_block,
-                             exchange=exchange)
-        assert pos[0] == Q  # one exchange per query block, covering every query
+                             exchange=exchange, shards=G, exchange_walk=walk)
+        assert pos == [Q] * (1 + walk)  # 1 + walk exchanges per query block, covering every query
         g_idx[g, :, :kk] = idx
         g_dst[g, :, :kk] = dst
         if kk < k:
@@ -70,16 +75,17 @@ def emulate(qs, db, w, p, k, bounds, query_block=8):
     return m_idx.cpu().numpy(), m_dst.cpu().numpy(), lowered[0]
 
 
+@pytest.mark.parametrize("walk", [0, 3])
 @pytest.mark.parametrize("G", [2, 3, 8])
 @pytest.mark.parametrize("name,Q,N", [("C5", 16, 24_000), ("C2p2", 24, 10_000), ("C2p1", 12, 10_000)])
-def test_sharded_emulation_equals_global(cuda_ok, G, name, Q, N):
+def test_sharded_emulation_equals_global(cuda_ok, G, name, Q, N, walk):
     from paper_0811_3301_b200 import nn_search
     from paper_0811_3301_b200.sharded import shard_range
     c = datagen.CONFIGS[name]
     k = c.k if name == "C5" else 3
     qs, db = datagen.make(c, Q=Q, N=N)
     bounds = [shard_range(N, G, g)[0] for g in range(G)] + [N]
-    m_idx, m_dst, lowered = emulate(qs, db, c.w, c.p, k, bounds)
+    m_idx, m_dst, lowered = emulate(qs, db, c.w, c.p, k, bounds, walk=walk)
     o_idx, o_dst, _ = oracle.nn_twopass(qs, db, c.w, c.p, k + 8, threads=THREADS)
     assert_knn_match(m_idx, m_dst, o_idx, o_dst, k)
     s_idx, s_dst = nn_search(dev(qs), dev(db), c.w, c.p, k, query_block=8)
@@ -97,7 +103,7 @@ def test_sharded_emulation_unbalanced_and_small_shards(cuda_ok):
     db[1] = qs[0]
     db[2] = qs[3] * np.float32(0.99)
     bounds = [0, 3, 3, 1700, 3000]  # shard sizes 3 (< k), 0, 1697, 1300
-    m_idx, m_dst, _ = emulate(qs, db, c.w, c.p, k, bounds, query_block=4)
+    m_idx, m_dst, _ = emulate(qs, db, c.w, c.p, k, bounds, query_block=4, walk=3)
     o_idx, o_dst = oracle.nn_brute(qs, db, c.w, c.p, k + 8, threads=THREADS)
     assert_knn_match(m_idx, m_dst, o_idx, o_dst, k)
     assert m_idx[0, 0] == 1 and m_dst[0, 0] == 0.0

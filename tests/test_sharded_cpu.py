@@ -16,6 +16,7 @@ import torch.multiprocessing as mp
 
 import datagen
 import oracle
+from paper_0811_3301_b200.sharded import EXCHANGE_WALK
 
 
 def _free_port():
@@ -31,11 +32,13 @@ def _oracle_search(queries, db, w, p, k, index_base=0, out=None, **_):
     return torch.from_numpy(idx + index_base), torch.from_numpy(dst.astype(np.float32))
 
 
-def _cascade_search(queries, db, w, p, k, index_base=0, out=None, query_block=None, exchange=None, shards=0):
+def _cascade_search(queries, db, w, p, k, index_base=0, out=None, query_block=None, exchange=None, shards=0,
+                    exchange_walk=0):
     """CPU stand-in of nn_search's two-range protocol built from oracle primitives: per
     query block, range 1 = the S candidates with the smallest LB_Keogh (exact DTW, local
     top-k, tau); exchange(tau) may lower tau; range 2 = the other candidates whose
-    LB_Keogh <= tau (1+eps) with tau tightening as results arrive."""
+    LB_Keogh <= tau (1+eps) with tau tightening as results arrive, walked in 1 + exchange_walk
+    parts with an exchange after each of the first exchange_walk parts (nn_opts.exchange_walk)."""
     qs, dbn = queries.numpy().astype(np.float64), db.numpy().astype(np.float64)
     Q, N = qs.shape[0], dbn.shape[0]
     eps = 1e-3
@@ -62,8 +65,15 @@ def _cascade_search(queries, db, w, p, k, index_base=0, out=None, query_block=No
             visit(q, np.argsort(lbs[q], kind="stable")[:S])
         if exchange is not None:
             exchange(thr)
+        parts = 1 + (exchange_walk if exchange is not None else 0)
+        rest = {q: np.argsort(lbs[q], kind="stable")[S:] for q in rows}
+        for part in range(parts):
+            for q in rows:
+                r2 = rest[q]
+                visit(q, r2[part * len(r2) // parts:(part + 1) * len(r2) // parts])
+            if part + 1 < parts:
+                exchange(thr)
         for q in rows:
-            visit(q, np.argsort(lbs[q], kind="stable")[S:])
             for r, (d, c) in enumerate(tops[q]):
                 idx[q, r] = c + index_base
                 dst[q, r] = d ** (1.0 / p)
@@ -85,7 +95,8 @@ def _worker_exchange(rank, world, port, N, k, result_q):
         shard = np.ascontiguousarray(shard)
         seen = []
 
-        def search(queries, db, w, p, kk, index_base=0, out=None, query_block=None, exchange=None, shards=0):
+        def search(queries, db, w, p, kk, index_base=0, out=None, query_block=None, exchange=None, shards=0,
+                   exchange_walk=0):
             # every shard is told the shard count (its best-first seed range is 1/world of the whole)
             assert shards == world, (shards, world)
 
@@ -93,7 +104,7 @@ def _worker_exchange(rank, world, port, N, k, result_q):
                 before = t.clone()
                 exchange(t)
                 seen.append((before.numpy().copy(), t.numpy().copy()))
-            return _cascade_search(queries, db, w, p, kk, index_base, out, query_block, ex)
+            return _cascade_search(queries, db, w, p, kk, index_base, out, query_block, ex, exchange_walk=exchange_walk)
 
         idx, dst = sharded_nn_search(torch.from_numpy(qs), torch.from_numpy(shard), lo, 3, cfg.p, k,
                                      search=search, merge=merge_reference, query_block=3)
@@ -129,7 +140,8 @@ def test_threshold_exchange_is_exact_and_tightens():
     for rank, idx, dst, seen in res:
         assert np.array_equal(idx, o_idx)
         assert np.allclose(dst, o_dst, rtol=1e-6)
-        assert len(seen) == 2  # blocks of 3 queries: 4 queries -> 2 exchanges on every rank
+        # blocks of 3 queries: 4 queries -> 2 blocks x (1 + EXCHANGE_WALK) exchanges on every rank
+        assert len(seen) == 2 * (1 + EXCHANGE_WALK)
         for before, after in seen:
             assert np.all(after <= before)
     lowered = sum(int(np.any(a < b)) for _, _, _, seen in res for b, a in seen)
@@ -219,11 +231,12 @@ def _worker_unbalanced(rank, world, port, bounds, k, result_q):
             shard[1] = qs[0] * np.float32(0.999)
         sent = []
 
-        def search(queries, db, w, p, kk, index_base=0, out=None, query_block=None, exchange=None, shards=0):
+        def search(queries, db, w, p, kk, index_base=0, out=None, query_block=None, exchange=None, shards=0,
+                   exchange_walk=0):
             def ex(t):
                 exchange(t)
                 sent.append(t.numpy().copy())
-            return _cascade_search(queries, db, w, p, kk, index_base, out, query_block, ex)
+            return _cascade_search(queries, db, w, p, kk, index_base, out, query_block, ex, exchange_walk=exchange_walk)
 
         idx, dst = sharded_nn_search(torch.from_numpy(qs), torch.from_numpy(shard), lo, 3, cfg.p, k,
                                      search=search, merge=merge_reference, query_block=4)
