@@ -17,6 +17,7 @@ oracle/) on this box's host cores over a bounded sample of the same workload.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -242,6 +243,8 @@ def run_ours(args, cfg):
     barrier()
     stats_all = []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    gc.collect()
+    gc.disable()  # no collector pause inside the timed region (the walk is host-driven)
     with ClockSampler(dev.index) as clk:
         time.sleep(0.5)  # let nvidia-smi start polling before the timed region (its start-up stalls the GPU)
         barrier()
@@ -253,6 +256,7 @@ def run_ours(args, cfg):
             step_ev[-1].record(st)
         ev1.record(st)
         barrier()
+    gc.enable()
     ms = ev0.elapsed_time(ev1) / args.steps
     # per-step device times (run-to-run diagnostics: one slow step shows up here)
     step_ms = [round((step_ev[i - 1] if i else ev0).elapsed_time(step_ev[i]), 3) for i in range(args.steps)]

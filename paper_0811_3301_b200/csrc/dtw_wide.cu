@@ -30,7 +30,7 @@ namespace dtwlb {
 
 namespace {
 
-constexpr int KW = 4;      // lanes per pair
+constexpr int KW4 = 4;     // lanes per pair (default; KW = 8 for narrower segments, see dtw_wide_plan)
 constexpr int NTW = 128;   // threads per CTA
 constexpr int kWChunk = 32;
 
@@ -54,22 +54,24 @@ __device__ __forceinline__ unsigned long long wband_cells(int r, int n, int w) {
 //      true : column coordinates (cell e of lane t = column tS + e), w >= n - 1 only.
 // yp: padded query rows [rows][LPW], yp[u] = y[u - padL] (+inf outside [0, n)).
 template <int S>
-constexpr int wide_min_blocks() { return S <= 32 ? 3 : 2; }
+constexpr int wide_min_blocks() { return S <= 16 ? 4 : (S <= 32 ? 3 : 2); }
+// lanes t == 0 of every group of KW lanes
+template <int KW>
+__host__ __device__ constexpr unsigned group_leads() { return KW == 8 ? 0x01010101u : 0x11111111u; }
 
-template <int S, int P, bool WALK, bool COL>
+template <int KW, int S, int P, bool WALK, bool COL>
 __global__ void __launch_bounds__(NTW, wide_min_blocks<S>())
 dtw_wide_kernel(DtwArgs a, const float *__restrict__ yp, int LPW, int padL) {
+    static_assert(KW == 4 || KW == 8, "lanes per pair");
     constexpr int NY = COL ? S : S + 3;
-    const int lane = threadIdx.x & 31, t = lane & 3;
+    const int lane = threadIdx.x & 31, t = lane & (KW - 1);
     const unsigned FULL = 0xffffffffu;
     const int n = a.n, w = a.w, NB = 2 * w + 1;
     const int64_t total = (WALK && a.dev_total) ? (int64_t)*a.dev_total : a.total;
-    // band mode: lane 3 holds M = 4S - NB invalid cells at its top positions (0 <= M <= 3);
+    // band mode: lane KW-1 holds M = KW*S - NB invalid cells at its top positions (0 <= M < KW);
     // they are reset to +inf after every row so they never feed a valid cell
-    const int M = COL ? 0 : 4 * S - NB;
-    const float mk0 = (!COL && t == 3 && M >= 3) ? kInf : -kInf;
-    const float mk1 = (!COL && t == 3 && M >= 2) ? kInf : -kInf;
-    const float mk2 = (!COL && t == 3 && M >= 1) ? kInf : -kInf;
+    const int M = COL ? 0 : KW * S - NB;
+    const int mfirst = (!COL && t == KW - 1) ? S - M : S;  // first invalid cell of this lane
     // cell holding D(n-1, n-1): band position w, or column n-1
     const int dfin = COL ? n - 1 : w;
     const int tfin = dfin / S, efin = dfin - tfin * S;
@@ -82,11 +84,15 @@ dtw_wide_kernel(DtwArgs a, const float *__restrict__ yp, int LPW, int padL) {
     float thr = kInf;
     const float *xr = nullptr, *yr = nullptr;
     float B[S], Y[NY], xc[4], xn[4], yn[4];
+    // column coordinates: the rows alternate between B and B2 (cell e reads the previous row's
+    // e-1 and e after its left neighbour overwrote e-1: in place, every cell would cost a move)
+    float B2[COL ? S : 1];
+    float res_hold = kInf;  // COL: the result cell D(n-1, n-1), captured when its row is computed
     // cascading abandon (readings c15, c19; as dtw4_kernel): rest = LB_Keogh^p terms of the rows
     // not yet computed = beta1 (from the gate slot) minus the terms of the rows lane 0 of the
     // group has computed; rest_snap = its value after the checkpoint row (r & 7 == 7)
     const bool casc = WALK && (a.b1 != nullptr || a.b1h != nullptr);
-    float rest = 0.f, rest_snap = 0.f;
+    float rest = 0.f, rest_snap = 0.f, u_nx = 0.f, l_nx = 0.f;  // (U, L of lane 0's next row)
     const float *ur = nullptr, *lr = nullptr;
     float left_in = kInf, diag_in = kInf, segmin = kInf;
     unsigned long long n_cells = 0;
@@ -98,7 +104,7 @@ dtw_wide_kernel(DtwArgs a, const float *__restrict__ yp, int LPW, int padL) {
         // ---------------- refill (phase 0 of 8): free groups start new pairs at s0 = s
         if ((s & 7) == 0) {
             while (true) {
-                const unsigned needm = __ballot_sync(FULL, t == 0 && !busy) & 0x11111111u;
+                const unsigned needm = __ballot_sync(FULL, t == 0 && !busy) & group_leads<KW>();
                 if (!needm || !more_items) break;
                 if (wcur >= wend) {
                     int64_t base = 0;
@@ -108,7 +114,7 @@ dtw_wide_kernel(DtwArgs a, const float *__restrict__ yp, int LPW, int padL) {
                     wcur = base;
                     wend = base + kWChunk < total ? base + kWChunk : total;
                 }
-                const int rank = __popc(needm & ((1u << (lane & ~3)) - 1u));
+                const int rank = __popc(needm & ((1u << (lane & ~(KW - 1))) - 1u));
                 const int take = __popc(needm);
                 const int64_t mine = wcur + rank;
                 const bool got = !busy && mine < wend;
@@ -136,6 +142,8 @@ dtw_wide_kernel(DtwArgs a, const float *__restrict__ yp, int LPW, int padL) {
                             rest_snap = rest;
                             ur = a.Uq + (int64_t)qy * n;
                             lr = a.Lq + (int64_t)qy * n;
+                            u_nx = __ldg(ur);  // row 0 (lane 0 starts there)
+                            l_nx = __ldg(lr);
                         }
                     } else {
                         cand = (uint32_t)item;
@@ -197,28 +205,39 @@ dtw_wide_kernel(DtwArgs a, const float *__restrict__ yp, int LPW, int padL) {
             const int r = rb + u;
             const bool active = busy && r >= 0 && r < n;
             if constexpr (COL) {
-                if (active) {
+                auto col_row = [&](float (&Bi)[COL ? S : 1], float (&Bo)[COL ? S : 1]) {
+                    // computed unconditionally (no divergent merge, hence no moves): a lane's rows
+                    // before row 0 see +inf everywhere and stay +inf (the start state), rows after
+                    // n-1 are garbage -- the result cell is captured at row n-1 -- and idle lanes
+                    // are re-initialised at their refill
                     float dg = diag_in, lf = left_in;
 #pragma unroll
                     for (int e = 0; e < S; ++e) {
-                        const float up = B[e];
+                        const float up = Bi[e];
                         const float v = wcell<P>(min3f(dg, up, lf), xc[u] - Y[e]);
                         dg = up;
                         lf = v;
-                        B[e] = v;
+                        Bo[e] = v;
                     }
-                    if (WALK && (r & 7) == 7) {
-                        float m = B[0];
+                    if (WALK && active && (r & 7) == 7) {
+                        float m = Bo[0];
 #pragma unroll
-                        for (int e = 1; e + 1 < S; e += 2) m = min3f(m, B[e], B[e + 1]);
-                        if ((S & 1) == 0) m = fminf(m, B[S - 1]);
+                        for (int e = 1; e + 1 < S; e += 2) m = min3f(m, Bo[e], Bo[e + 1]);
+                        if ((S & 1) == 0) m = fminf(m, Bo[S - 1]);
                         segmin = m;
                     }
-                }
-                float recv = __shfl_up_sync(FULL, B[S - 1], 1, KW);
-                if (t == 0) recv = kInf;
-                diag_in = left_in;
-                left_in = recv;
+                    if (busy && r == n - 1 && t == tfin) {
+#pragma unroll
+                        for (int e = 0; e < S; ++e)
+                            if (e == efin) res_hold = Bo[e];
+                    }
+                    float recv = __shfl_up_sync(FULL, Bo[S - 1], 1, KW);
+                    if (t == 0) recv = kInf;
+                    diag_in = left_in;
+                    left_in = recv;
+                };
+                if (u & 1) col_row(B2, B);  // (u is a constant of the unrolled loop)
+                else col_row(B, B2);
             } else {
                 float v0 = B[0];
                 if (active) {
@@ -236,9 +255,9 @@ dtw_wide_kernel(DtwArgs a, const float *__restrict__ yp, int LPW, int padL) {
                         prev = v;
                     }
                     B[S - 1] = wcell<P>(min3f(B[S - 1], upl, prev), xc[u] - Y[S - 1 + u]);
-                    B[S - 3] = fmaxf(B[S - 3], mk0);
-                    B[S - 2] = fmaxf(B[S - 2], mk1);
-                    B[S - 1] = fmaxf(B[S - 1], mk2);
+#pragma unroll
+                    for (int e = (S > KW - 1 ? S - (KW - 1) : 0); e < S; ++e)
+                        if (e >= mfirst) B[e] = kInf;
                     if (WALK && (r & 7) == 7) {
                         float m = B[0];
 #pragma unroll
@@ -252,7 +271,12 @@ dtw_wide_kernel(DtwArgs a, const float *__restrict__ yp, int LPW, int padL) {
                 left_in = recv;
             }
             if (casc && t == 0 && active) {
-                const float d = max3f(xc[u] - __ldg(ur + r), __ldg(lr + r) - xc[u], 0.f);
+                const float uu = u_nx, ll = l_nx;
+                if (r + 1 < n) {  // the next row's envelope, loaded a row (a 51-cell chain) ahead
+                    u_nx = __ldg(ur + r + 1);
+                    l_nx = __ldg(lr + r + 1);
+                }
+                const float d = max3f(xc[u] - uu, ll - xc[u], 0.f);
                 rest -= P == 1 ? d : (P == 4 ? (d * d) * (d * d) : d * d);
                 if ((r & 7) == 7) rest_snap = rest;
             }
@@ -264,9 +288,9 @@ dtw_wide_kernel(DtwArgs a, const float *__restrict__ yp, int LPW, int padL) {
                 float res = kInf;
 #pragma unroll
                 for (int e = 0; e < S; ++e)
-                    if (t == tfin && e == efin) res = B[e];
-                res = fminf(res, __shfl_xor_sync(FULL, res, 1, KW));
-                res = fminf(res, __shfl_xor_sync(FULL, res, 2, KW));
+                    if (t == tfin && e == efin) res = COL ? res_hold : B[e];
+#pragma unroll
+                for (int o = 1; o < KW; o <<= 1) res = fminf(res, __shfl_xor_sync(FULL, res, o, KW));
                 if (done && t == 0) {
                     n_cells += wband_cells(n, n, w);
                     if constexpr (WALK) {
@@ -284,18 +308,18 @@ dtw_wide_kernel(DtwArgs a, const float *__restrict__ yp, int LPW, int padL) {
             }
             // ---- exact early abandon (reading c15): checkpoint row 8m+7 complete in all lanes
             if constexpr (WALK) {
-                if (((s + u) & 7) == 2) {  // (uniform: every group's s0 is a multiple of 8)
+                if (((s + u) & 7) == ((KW + 6) & 7)) {  // (uniform: every group's s0 is a multiple of 8)
                     float m = segmin;
-                    m = fminf(m, __shfl_xor_sync(FULL, m, 1, KW));
-                    m = fminf(m, __shfl_xor_sync(FULL, m, 2, KW));
+#pragma unroll
+                    for (int o = 1; o < KW; o <<= 1) m = fminf(m, __shfl_xor_sync(FULL, m, o, KW));
                     // + the LB_Keogh terms of the rows after the checkpoint row (lane 0's snapshot)
-                    if (casc) m += fmaxf(__shfl_sync(FULL, rest_snap, lane & ~3), 0.f);
-                    if (busy && ph >= 10) {
+                    if (casc) m += fmaxf(__shfl_sync(FULL, rest_snap, lane & ~(KW - 1)), 0.f);
+                    if (busy && ph >= KW + 6) {
                         thr = fminf(thr, *reinterpret_cast<volatile float *>(a.thr + qy));
                         if (m > thr) {
                             if (t == 0) {
                                 ++n_abandon;
-                                n_cells += wband_cells(ph - KW + 2, n, w);  // rows 0 .. ph-3 done
+                                n_cells += wband_cells(ph - KW + 2, n, w);  // rows 0 .. ph-KW+1 done
                             }
                             busy = false;
                         }
@@ -335,56 +359,80 @@ __global__ void build_ywide_kernel(const float *__restrict__ y, int64_t rows, in
     }
 }
 
-template <int S, int P, bool WALK, bool COL>
+template <int KW, int S, int P, bool WALK, bool COL>
 int launch_wide_t(const DtwArgs &a, const float *yp, int LPW, int padL, cudaStream_t st) {
     DTWLB_CUDA(cudaMemsetAsync(a.queue, 0, sizeof(unsigned), st));
     int dev = 0, nsm = 148;
     DTWLB_CUDA(cudaGetDevice(&dev));
     DTWLB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    // enough warps to hold every pair of the round (8 per warp), at most 3 CTAs x 4 warps per SM
-    const int64_t warps = std::min<int64_t>(ceil_div(std::max<int64_t>(a.total, 1), 8), (int64_t)nsm * 12);
+    // enough warps to hold every pair of the round (32 / KW per warp), at most the resident
+    // CTAs x 4 warps per SM
+    const int64_t warps = std::min<int64_t>(ceil_div(std::max<int64_t>(a.total, 1), 32 / KW),
+                                            (int64_t)nsm * 4 * wide_min_blocks<S>());
     const int64_t grid = ceil_div(warps * 32, NTW);
-    dtw_wide_kernel<S, P, WALK, COL><<<(unsigned)grid, NTW, 0, st>>>(a, yp, LPW, padL);
+    dtw_wide_kernel<KW, S, P, WALK, COL><<<(unsigned)grid, NTW, 0, st>>>(a, yp, LPW, padL);
     DTWLB_LAUNCH_CHECK();
     return DTWLB_OK;
 }
 
 template <int P, bool WALK>
-int launch_wide_p(const DtwArgs &a, const float *yp, int LPW, int padL, int mode, int S, cudaStream_t st) {
+int launch_wide_p(const DtwArgs &a, const float *yp, int LPW, int padL, int mode, int S, int KW, cudaStream_t st) {
     if (mode == 1) {  // column coordinates (w >= n - 1)
-        switch (S) {
-            case 16: return launch_wide_t<16, P, WALK, true>(a, yp, LPW, padL, st);
-            case 25: return launch_wide_t<25, P, WALK, true>(a, yp, LPW, padL, st);
-            case 32: return launch_wide_t<32, P, WALK, true>(a, yp, LPW, padL, st);
-            case 48: return launch_wide_t<48, P, WALK, true>(a, yp, LPW, padL, st);
-            case 64: return launch_wide_t<64, P, WALK, true>(a, yp, LPW, padL, st);
+        if (KW == 8) {
+            switch (S) {
+                case 13: return launch_wide_t<8, 13, P, WALK, true>(a, yp, LPW, padL, st);
+                case 16: return launch_wide_t<8, 16, P, WALK, true>(a, yp, LPW, padL, st);
+                case 32: return launch_wide_t<8, 32, P, WALK, true>(a, yp, LPW, padL, st);
+            }
+        } else {
+            switch (S) {
+                case 16: return launch_wide_t<4, 16, P, WALK, true>(a, yp, LPW, padL, st);
+                case 25: return launch_wide_t<4, 25, P, WALK, true>(a, yp, LPW, padL, st);
+                case 32: return launch_wide_t<4, 32, P, WALK, true>(a, yp, LPW, padL, st);
+                case 48: return launch_wide_t<4, 48, P, WALK, true>(a, yp, LPW, padL, st);
+                case 64: return launch_wide_t<4, 64, P, WALK, true>(a, yp, LPW, padL, st);
+            }
         }
     } else {
-        switch (S) {
-            case 51: return launch_wide_t<51, P, WALK, false>(a, yp, LPW, padL, st);
-        }
+        if (KW == 8 && S == 26) return launch_wide_t<8, 26, P, WALK, false>(a, yp, LPW, padL, st);
+        if (KW == 4 && S == 51) return launch_wide_t<4, 51, P, WALK, false>(a, yp, LPW, padL, st);
     }
-    set_error(DTWLB_EINVAL, "internal: no wide DTW kernel for S = %d", S);
+    set_error(DTWLB_EINVAL, "internal: no wide DTW kernel for KW = %d, S = %d", KW, S);
     return DTWLB_EINVAL;
+}
+
+// Lanes per pair KW and segment length S for (n, w): mode 1 = column coordinates (w >= n-1,
+// n <= 256), mode 2 = band coordinates (w = 100, 101); 0 = none (generic kernel).  KW = 4 lanes
+// per pair; DTWLB_WIDE_KW=8 halves each lane's serial cell chain and its registers (more warps
+// resident) but measured slower: C3 w = 100 DTW 56.0 vs 44.8 ms, Appendix B 2.64 vs 2.89 10^12
+// cells/s (profiles/r02o_wide_kw.txt) -- twice the shuffles per cell and a 7-row pipeline skew.
+int wide_plan(int n, int w, int *S_out, int *KW_out) {
+    static const int env_kw = [] { const char *e = getenv("DTWLB_WIDE_KW"); return e ? atoi(e) : 0; }();
+    const int KW = env_kw == 8 ? 8 : 4;
+    *KW_out = KW;
+    if (w >= n - 1 && n <= 256) {
+        const int need = (n + KW - 1) / KW;
+        const int o8[] = {13, 16, 32}, o4[] = {16, 25, 32, 48, 64};
+        const int *opts = KW == 8 ? o8 : o4;
+        const int nopt = KW == 8 ? 3 : 5;
+        for (int i = 0; i < nopt; ++i)
+            if (opts[i] >= need) { *S_out = opts[i]; return 1; }
+    }
+    const int S = (2 * w + 1 + KW - 1) / KW;
+    if ((KW == 8 && S == 26) || (KW == 4 && S == 51)) { *S_out = S; return 2; }
+    return 0;
 }
 
 }  // namespace
 
-// Which wide kernel handles (n, w), if any: mode 1 = column coordinates (w >= n-1, n <= 256),
-// mode 2 = band coordinates (S = ceil((2w+1)/4) instantiated: w = 100, 101); 0 = none (generic).
 int dtw_wide_plan(int n, int w, int *S_out) {
-    if (w >= n - 1 && n <= 256) {
-        const int need = (n + KW - 1) / KW;
-        const int opts[] = {16, 25, 32, 48, 64};
-        for (int S : opts)
-            if (S >= need) { *S_out = S; return 1; }
-    }
-    const int S = (2 * w + 1 + KW - 1) / KW;
-    if (S == 51) { *S_out = S; return 2; }
-    return 0;
+    int KW = 0;
+    return wide_plan(n, w, S_out, &KW);
 }
 
 int dtw_wide_padded(int n, int w, int S, int *padL) {
+    int S2 = 0, KW = 4;
+    wide_plan(n, w, &S2, &KW);
     *padL = (w + 8 + 3) / 4 * 4;
     return (*padL + n + KW * S + 16 + 3) / 4 * 4;
 }
@@ -399,8 +447,8 @@ int launch_build_ywide(const float *y, int64_t rows, int n, float *yp, int LPW, 
 }
 
 int launch_dtw_wide(const DtwArgs &a, const float *yp, int LPW, int padL, int p, bool walk, cudaStream_t st) {
-    int S = 0;
-    const int mode = dtw_wide_plan(a.n, a.w, &S);
+    int S = 0, KW = 4;
+    const int mode = wide_plan(a.n, a.w, &S, &KW);
     if (mode == 0) {
         set_error(DTWLB_EINVAL, "internal: no wide DTW kernel for n = %d, w = %d", a.n, a.w);
         return DTWLB_EINVAL;
@@ -415,19 +463,19 @@ int launch_dtw_wide(const DtwArgs &a, const float *yp, int LPW, int padL, int p,
             set_error(DTWLB_EUNSUPPORTED, "nn_search: p = infinity unsupported");
             return DTWLB_EUNSUPPORTED;
         }
-        return launch_wide_p<0, false>(a, yp, LPW, padL, mode, S, st);
+        return launch_wide_p<0, false>(a, yp, LPW, padL, mode, S, KW, st);
     }
     if (p == 4) {
         if (walk) {
             set_error(DTWLB_EUNSUPPORTED, "nn_search: p = 4 unsupported");
             return DTWLB_EUNSUPPORTED;
         }
-        return launch_wide_p<4, false>(a, yp, LPW, padL, mode, S, st);
+        return launch_wide_p<4, false>(a, yp, LPW, padL, mode, S, KW, st);
     }
-    if (p == 1) return walk ? launch_wide_p<1, true>(a, yp, LPW, padL, mode, S, st)
-                            : launch_wide_p<1, false>(a, yp, LPW, padL, mode, S, st);
-    return walk ? launch_wide_p<2, true>(a, yp, LPW, padL, mode, S, st)
-                : launch_wide_p<2, false>(a, yp, LPW, padL, mode, S, st);
+    if (p == 1) return walk ? launch_wide_p<1, true>(a, yp, LPW, padL, mode, S, KW, st)
+                            : launch_wide_p<1, false>(a, yp, LPW, padL, mode, S, KW, st);
+    return walk ? launch_wide_p<2, true>(a, yp, LPW, padL, mode, S, KW, st)
+                : launch_wide_p<2, false>(a, yp, LPW, padL, mode, S, KW, st);
 }
 
 }  // namespace dtwlb

@@ -44,8 +44,17 @@ struct Workspace {
     std::vector<void *> ptr;
     std::vector<size_t> size;
     ~Workspace() { release(); }
+    cudaStream_t copy_stream = nullptr;  // host->device database chunks of the e2e path
+    cudaStream_t get_copy_stream() {
+        if (!copy_stream && cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+            cudaGetLastError();
+            copy_stream = nullptr;
+        }
+        return copy_stream;
+    }
     void release() {
         qb_cache.clear();
+        if (copy_stream) { cudaStreamDestroy(copy_stream); copy_stream = nullptr; }
         if (ptr.empty()) return;
         int cur = -1;
         cudaGetDevice(&cur);
@@ -560,16 +569,25 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         DTWLB_CUDA(cudaMemcpyAsync(d, queries_in, sizeof(float) * Q * n, cudaMemcpyHostToDevice, st));
         queries = d;
     }
+    const float *db_host = nullptr;
     if (!is_device_ptr(db_in)) {
         float *d;
         DTWLB_TRY(wsget(S_DBSTAGE, (size_t)N * n, &d));
-        DTWLB_CUDA(cudaMemcpyAsync(d, db_in, sizeof(float) * N * n, cudaMemcpyHostToDevice, st));
         db = d;
+        db_host = db_in;
     }
     // stream mode (Q <= kStreamMaxQ): LB_Keogh of all Q queries in one streaming pass over the
     // database (stream.cu), no pre-filter
     const bool stream_mode = !(opts && (opts->flags & DTWLB_NO_STREAM)) && keogh_stream_ok(Q, n, db);
     if (stream_mode) prefilter = false;
+    // A host database with the pre-filter (the e2e path): it is copied in chunks on a side stream
+    // and the database-side setup and the first block's gate run chunk by chunk as the chunks
+    // land, so the host->device copy hides behind the gate (bench e2e); else one copy up front
+    static const bool gate_split = [] { const char *e = getenv("DTWLB_GATE_SPLIT"); return e && atoi(e); }();
+    const bool chunked = db_host && prefilter && !(opts && opts->db_env) && !gate_split &&
+                         ws().get_copy_stream() != nullptr;
+    if (db_host && !chunked)
+        DTWLB_CUDA(cudaMemcpyAsync(const_cast<float *>(db), db_host, sizeof(float) * N * n, cudaMemcpyHostToDevice, st));
     const bool out_dev = is_device_ptr(out_idx_in) && is_device_ptr(out_dist_in);
     int64_t *out_idx = out_idx_in;
     float *out_dist = out_dist_in;
@@ -608,7 +626,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     if (prefilter) {
         DTWLB_TRY(wsget(S_PAA, (size_t)2 * N * Dp, &xpaa));
         DTWLB_TRY(wsget(S_QPAA, (size_t)2 * Q * Dp, &qpaa));
-        DTWLB_TRY(launch_paa_sums(db, N, n, xpaa, xpaa + (size_t)N * Dp, st));
+        if (!chunked) DTWLB_TRY(launch_paa_sums(db, N, n, xpaa, xpaa + (size_t)N * Dp, st));
         DTWLB_TRY(launch_paa_env_sums(U, L, Q, n, qpaa, qpaa + (size_t)Q * Dp, st));
     }
     const bool generic_dtw = w > 64;
@@ -638,7 +656,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     if (!dbenv && (!keogh_only || prefilter)) {
         float *e;
         DTWLB_TRY(wsget(S_DBENV, (size_t)2 * N * n, &e));
-        DTWLB_TRY(launch_envelope(db, n, w, e, e + (size_t)N * n, N, st));
+        if (!chunked) DTWLB_TRY(launch_envelope(db, n, w, e, e + (size_t)N * n, N, st));
         dbenv = e;
     }
     // symmetric gate (reading c20): reverse piecewise sums P(U(x)) up, P(L(x)) down [2][N][Dp]
@@ -646,7 +664,8 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     float *rpaa = nullptr;
     if (prefilter) {
         DTWLB_TRY(wsget(S_RPAA, (size_t)2 * N * Dp + (size_t)2 * Q * Dp, &rpaa));
-        DTWLB_TRY(launch_paa_env_sums(dbenv, dbenv + (size_t)N * n, N, n, rpaa, rpaa + (size_t)N * Dp, st));
+        if (!chunked)
+            DTWLB_TRY(launch_paa_env_sums(dbenv, dbenv + (size_t)N * n, N, n, rpaa, rpaa + (size_t)N * Dp, st));
         float *yp = rpaa + (size_t)2 * N * Dp;
         DTWLB_TRY(launch_paa_sums(queries, Q, n, yp, yp + (size_t)Q * Dp, st));
     }
@@ -736,8 +755,11 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     static const int env_S = [] { const char *e = getenv("DTWLB_SEED"); return e ? atoi(e) : 0; }();
     // (a database shard seeds from 1/G of the whole database's seed range, nn_opts.shards)
     const int64_t shards = opts && opts->shards > 1 ? opts->shards : 1;
+    // (N / 768: measured seed sweeps, profiles/r02n_seed_sweep.txt -- C5 (N = 10^6) is flat for
+    // S in 512..2048, C3 (10^5) and C4 (2 10^5) are 7-9 % faster at 256 than at the old N/64)
     const int64_t S = std::max<int64_t>(std::max<int64_t>(256, 4LL * k),
-                                        std::min<int64_t>((env_S > 0 ? env_S : kSeedCap) / shards, N / 64));
+                                        std::min<int64_t>((env_S > 0 ? env_S : kSeedCap) / shards,
+                                                          env_S > 0 ? (int64_t)env_S : N / 768));
     // number of ranges R and the growth G of their sampled sizes (S, S*G, S*G^2, ..., rest)
     static const int env_R = [] { const char *e = getenv("DTWLB_RANGES"); return e ? atoi(e) : 0; }();
     static const int env_G = [] { const char *e = getenv("DTWLB_RANGE_GROWTH"); return e ? atoi(e) : 0; }();
@@ -765,6 +787,41 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     unsigned long long *stat_save = stats ? snap + snap_cap * 8 : nullptr;  // stat at the block start
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
 
+    int64_t gate0_qn = -1;  // rows of the first block whose gate ran with the chunked copy
+    if (chunked) {
+        cudaStream_t cs = ws().get_copy_stream();
+        cudaEvent_t e_in;
+        DTWLB_CUDA(cudaEventCreateWithFlags(&e_in, cudaEventDisableTiming));
+        DTWLB_CUDA(cudaEventRecord(e_in, st));  // the staging buffer is free once st gets here
+        DTWLB_CUDA(cudaStreamWaitEvent(cs, e_in, 0));
+        cudaEventDestroy(e_in);
+        const int64_t qn0 = std::min<int64_t>(Qb, Q);
+        const int64_t rows_per = std::max<int64_t>(1, std::min<int64_t>(131072, ceil_div(N, 4)));
+        const float *yp = rpaa + (size_t)2 * N * Dp;
+        float *dbs = const_cast<float *>(db);
+        float *ex = const_cast<float *>(dbenv);
+        for (int64_t r0 = 0; r0 < N; r0 += rows_per) {
+            const int64_t cnt = std::min<int64_t>(rows_per, N - r0);
+            cudaEvent_t e_c;
+            DTWLB_CUDA(cudaEventCreateWithFlags(&e_c, cudaEventDisableTiming));
+            DTWLB_CUDA(cudaMemcpyAsync(dbs + r0 * n, db_host + r0 * n, sizeof(float) * cnt * n,
+                                       cudaMemcpyHostToDevice, cs));
+            DTWLB_CUDA(cudaEventRecord(e_c, cs));
+            DTWLB_CUDA(cudaStreamWaitEvent(st, e_c, 0));
+            cudaEventDestroy(e_c);
+            DTWLB_TRY(launch_paa_sums(db + r0 * n, cnt, n, xpaa + r0 * Dp, xpaa + (size_t)N * Dp + r0 * Dp, st));
+            DTWLB_TRY(launch_envelope(db + r0 * n, n, w, ex + r0 * n, ex + (size_t)N * n + r0 * n, cnt, st));
+            DTWLB_TRY(launch_paa_env_sums(ex + r0 * n, ex + (size_t)N * n + r0 * n, cnt, n, rpaa + r0 * Dp,
+                                          rpaa + (size_t)N * Dp + r0 * Dp, st));
+            const cudaEvent_t g0 = stats ? rec() : nullptr;
+            DTWLB_TRY(launch_paa_bound_sym(qpaa, qpaa + (size_t)Q * Dp, yp, yp + (size_t)Q * Dp, xpaa + r0 * Dp,
+                                           xpaa + (size_t)N * Dp + r0 * Dp, rpaa + r0 * Dp,
+                                           rpaa + (size_t)N * Dp + r0 * Dp, qn0, cnt, n, p, false,
+                                           reinterpret_cast<__half *>(beta1) + r0, ldb, st));
+            if (stats) span(g0, rec(), &ms_keogh);
+        }
+        gate0_qn = qn0;
+    }
     int64_t Qcur = Qb;  // current block size
     int64_t rcap = cap;               // the range's list capacity per query (uniform lists)
     const int64_t *loff_r = nullptr;  // or its exact per-query offsets
@@ -778,9 +835,10 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         if (prefilter) {
             // symmetric gate: max of the forward and the reverse piecewise-sum bounds (readings c18,
             // c20), one fused tile pass (DTWLB_GATE_SPLIT=1: two launches, the second max-combining)
-            static const bool gate_split = [] { const char *e = getenv("DTWLB_GATE_SPLIT"); return e && atoi(e); }();
             const float *yp = rpaa + (size_t)2 * N * Dp;
-            if (gate_split) {
+            if (qb0 == 0 && qn == gate0_qn) {
+                // (computed chunk by chunk with the database copy, above)
+            } else if (gate_split) {
                 DTWLB_TRY(launch_paa_bound(qpaa + qb0 * Dp, qpaa + (size_t)Q * Dp + qb0 * Dp, xpaa,
                                            xpaa + (size_t)N * Dp, qn, N, n, p, false, beta1, ldb, st));
                 DTWLB_TRY(launch_paa_bound_rev(yp + qb0 * Dp, yp + (size_t)Q * Dp + qb0 * Dp, rpaa,

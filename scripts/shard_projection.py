@@ -23,6 +23,7 @@ bit-identical to the single-GPU result.
 usage: python scripts/shard_projection.py [--config C5] [--gpus 2,4,8] > profiles/<round>_shard_projection.json
 """
 import argparse
+import gc
 import json
 import os
 import sys
@@ -40,17 +41,21 @@ from paper_0811_3301_b200.sharded import (EXCHANGE_WALK as WALK, common_query_bl
 REP_MS = []  # per-repetition times of the last timed() call
 
 
-def timed(fn, reps=3):
+def timed(fn, reps=5):
     """Median over reps of the per-call device time (CUDA events around each call), after a
-    warm-up call that sizes the workspace."""
+    warm-up call that sizes the workspace; Python's garbage collector is off meanwhile (a
+    collection inside an exchange callback stalls the host-driven walk by tens of ms)."""
     fn()
     torch.cuda.synchronize()
+    gc.collect()
+    gc.disable()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
     ev[0].record()
     for r in range(reps):
         out = fn()
         ev[r + 1].record()
     torch.cuda.synchronize()
+    gc.enable()
     REP_MS[:] = [ev[r].elapsed_time(ev[r + 1]) for r in range(reps)]
     return sorted(REP_MS)[reps // 2], out
 

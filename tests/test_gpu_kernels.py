@@ -5,6 +5,8 @@ LB_Keogh / LB_Improved relative 1e-5; DTW relative 1e-4 (BASELINE north_star).
 Shapes span several CTA tiles plus ragged tails (n not a multiple of 4 or 32,
 N not a multiple of the 128-candidate tile), w = 0, w >= n, w > 64 (generic DTW).
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -258,3 +260,28 @@ def test_dtw_band_p4(cuda_ok, n, w):
     ref = np.array([oracle.dtw(x[r], y[r], w, 4) for r in range(count)])
     close(out, ref, 1e-4, 1e-6)
     assert out[0] == 0.0
+
+
+def test_dtw_band_wide_eight_lanes(cuda_ok):
+    """The eight-lanes-per-pair variant of the wide kernel (DTWLB_WIDE_KW=8, read once per
+    process -> a subprocess): band (w = 100) and column (w = n - 1) coordinates, p = 1, 2,
+    against the oracle."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, %r)\n"
+        "import oracle\n"
+        "from paper_0811_3301_b200 import dtw_band\n"
+        "rng = np.random.default_rng(11)\n"
+        "for n, w in ((150, 100), (333, 101), (100, 99), (128, 127), (256, 255)):\n"
+        "    for p in (1, 2):\n"
+        "        x = np.cumsum(rng.standard_normal((70, n)), axis=1).astype(np.float32)\n"
+        "        y = np.cumsum(rng.standard_normal((70, n)), axis=1).astype(np.float32)\n"
+        "        out = dtw_band(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), w, p).cpu().numpy()\n"
+        "        ref = np.array([oracle.dtw(x[r], y[r], w, p) for r in range(70)])\n"
+        "        assert np.allclose(out, ref, rtol=1e-4, atol=1e-6), (n, w, p)\n"
+        "print('ok')\n") % root
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, DTWLB_WIDE_KW="8"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
