@@ -196,7 +196,10 @@ def run_ours(args, cfg):
     qs = torch.from_numpy(qs_h).to(dev)
     db = torch.from_numpy(db_h).to(dev)
     k = cfg.k
-    from paper_0811_3301_b200.sharded import sharded_nn_search
+    from paper_0811_3301_b200.sharded import make_communicator, sharded_nn_search
+    # database-sharded N > 1: the library's own NCCL communicator does the threshold exchange
+    # inside nn_search (no Python callback in the search loop); --py-exchange keeps the callback
+    comm = make_communicator(device=dev) if ws > 1 and not qshard and not args.py_exchange else None
     idx = torch.empty((cfg.Q, k), dtype=torch.int64, device=dev)
     dst = torch.empty((cfg.Q, k), dtype=torch.float32, device=dev)
     gbufs = (torch.empty((ws * cfg.Q, k), dtype=torch.int64, device=dev),
@@ -230,7 +233,7 @@ def run_ours(args, cfg):
             query_sharded_nn_search(qs, db, cfg.w, cfg.p, k, search=search)
         else:
             sharded_nn_search(qs, db, lo, cfg.w, cfg.p, k, search=search, merge=B.nn_merge, out_local=(idx, dst),
-                              gather_bufs=gbufs)
+                              gather_bufs=gbufs, comm=comm)
         return last["st"] if stats else None
 
     def barrier():
@@ -285,7 +288,7 @@ def run_ours(args, cfg):
                 gi, gd = query_sharded_nn_search(q_dev, d_dev, cfg.w, cfg.p, k, search=search)
             else:
                 gi, gd = sharded_nn_search(q_dev, d_dev, lo, cfg.w, cfg.p, k, search=search, merge=B.nn_merge,
-                                           out_local=(idx, dst), gather_bufs=gbufs)
+                                           out_local=(idx, dst), gather_bufs=gbufs, comm=comm)
             h_idx.copy_(gi, non_blocking=True)
             h_dst.copy_(gd, non_blocking=True)
 
@@ -533,6 +536,9 @@ def main():
     ap.add_argument("--shard", default="db", choices=["db", "queries"],
                     help="N > 1: shard the database (default, SURVEY 8(e)) or the queries (comparison "
                          "mode: replicated database, no collective during the search)")
+    ap.add_argument("--py-exchange", action="store_true",
+                    help="N > 1, database-sharded: threshold exchange by a Python torch.distributed callback "
+                         "instead of the library's NCCL communicator")
     ap.add_argument("--no-stream", action="store_true",
                     help="Q <= 8: the tiled bound pass instead of the streaming one (DTWLB_NO_STREAM)")
     ap.add_argument("--db-index", action="store_true",

@@ -102,9 +102,9 @@ int lb_piecewise_sym(const float *q, const float *q_env, const float *db, int64_
  * projection H, both with locality constraint w.  q: device [Q][n] queries;
  * q_env: device [2][Q][n] envelope of q with the same w; db: device [N][n];
  * out: device [Q][N].  Dense form; nn_search evaluates it only on LB_Keogh
- * survivors.  Errors: as lb_keogh, plus EINVAL for w < 0, EUNSUPPORTED for
- * n > 1024 (the survivor kernel keeps a pair's n samples in one warp's registers,
- * at most 32 per lane). */
+ * survivors.  Any n: n <= 1024 runs the survivor kernel (a pair's n samples in one
+ * warp's registers, at most 32 per lane), longer series a warp-per-pair kernel with
+ * the same closed form.  Errors: as lb_keogh, plus EINVAL for w < 0. */
 int lb_improved(const float *q, const float *q_env, const float *db, int64_t Q, int64_t N,
                 int32_t n, int32_t w, int32_t p, float *out, void *stream);
 
@@ -157,6 +157,12 @@ typedef struct nn_opts {
      * thresholds), so a block makes exactly 1 + exchange_walk calls on every shard.  Speed
      * only (each call may only lower thresholds to values >= the global k-th best). */
     int32_t exchange_walk;
+    /* The library's own threshold exchange (alternative to `exchange`, used when `exchange` is
+     * NULL): an NCCL communicator from dtwlb_comm_init; at every exchange point the block's
+     * thresholds are min-reduced in place with ONE ncclAllReduce(ncclMin) on `stream` -- no host
+     * callback.  Same call schedule as `exchange` (1 + exchange_walk per block, equal
+     * query_block on every rank).  NULL = no exchange. */
+    void *nccl_comm;
 } nn_opts;
 
 #define DTWLB_KEOGH_ONLY 1
@@ -198,14 +204,16 @@ typedef struct nn_stats {
  * Without the pre-filter (DTWLB_NO_PREFILTER) LB_Keogh runs over the whole
  * database, as Alg. 3 is printed.  With few queries (Q <= 8, n % 4 == 0) the bound
  * pass is memory-bound: LB_Keogh then runs as ONE streaming pass over the database
- * for all Q queries (no pre-filter; DTWLB_NO_STREAM disables this mode).
+ * for all Q queries (no pre-filter; DTWLB_NO_STREAM disables this mode).  n > 1024:
+ * Alg. 2 (LB_Keogh over every pair, then DTW; no LB_Improved pass) -- still exact.
  *   queries: [Q][n] float32, db: [N][n] float32 -- device OR host pointers
  *            (host buffers are staged to the device inside the call);
  *   out_idx: [Q][k] int64 (index_base + row), out_dist: [Q][k] float32 rooted
  *            DTW_p, ascending -- device or host pointers.
  * Errors: EINVAL (n < 1, w < 0, k < 1, Q < 0, N < 1, k > N, N > 2^32 - 1, NULL
  * pointers, an output overlapping an input or the other output), EUNSUPPORTED
- * (p not 1 or 2, k > DTWLB_MAX_K, n > 1024 -- see lb_improved), ENOMEM, ECUDA.
+ * (p not 1 or 2, k > DTWLB_MAX_K), ENOMEM (also: a query block whose key lists do
+ * not fit even as single queries, or with a threshold exchange), ECUDA, ENCCL.
  * Q == 0 is a no-op.  Synchronous with respect to `stream`. */
 int nn_search(const float *queries, int64_t Q, const float *db, int64_t N, int32_t n, int32_t w,
               int32_t p, int32_t k, int64_t *out_idx, float *out_dist, const nn_opts *opts,
@@ -220,6 +228,16 @@ int nn_merge(const int64_t *in_idx, const float *in_dist, int32_t G, int64_t Q, 
 
 /* Last error message of the calling thread ("" if none). */
 const char *dtwlb_last_error(void);
+
+/* Multi-GPU bootstrap of the library's communicator (database-sharded search,
+ * one process per GPU).  Rank 0 calls dtwlb_get_unique_id and broadcasts the 128 bytes (e.g.
+ * with torch.distributed); every rank then calls dtwlb_comm_init with its rank on its current
+ * device and passes the communicator as nn_opts.nccl_comm.  NCCL is loaded at run time
+ * (libnccl.so.2).  Errors: EINVAL (NULL pointers, rank outside [0, nranks)), ECUDA (no sm_100
+ * device), ENCCL (NCCL not loadable or failing).  dtwlb_comm_destroy(NULL) is a no-op. */
+int dtwlb_get_unique_id(void *out128);
+int dtwlb_comm_init(const void *id128, int32_t nranks, int32_t rank, void **comm);
+int dtwlb_comm_destroy(void *comm);
 
 /* Release the library's cached device workspace (optional). */
 void dtwlb_release_workspace(void);

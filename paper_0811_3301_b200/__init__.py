@@ -6,8 +6,10 @@ kernels behind the C ABI of ``include/dtwlb.h`` (``libdtwlb.so``).  This package
 is the thin Python binding (``binding``) plus the database-sharded multi-GPU
 driver (``sharded``).  Importing it does not require a GPU; calling it does.
 """
-from .binding import (DtwlbError, KEOGH_ONLY, MAX_K, NO_PREFILTER, dtw_band, lb_envelope, lb_improved,
-                      lb_keogh, lb_piecewise, lb_piecewise_sym, load, nn_merge, nn_search, release_workspace)
+from .binding import (Communicator, DtwlbError, KEOGH_ONLY, MAX_K, NO_PREFILTER, dtw_band, get_unique_id,
+                      lb_envelope, lb_improved, lb_keogh, lb_piecewise, lb_piecewise_sym, load, nn_merge, nn_search,
+                      release_workspace)
 
-__all__ = ["DtwlbError", "KEOGH_ONLY", "MAX_K", "NO_PREFILTER", "dtw_band", "lb_envelope", "lb_improved",
-           "lb_keogh", "lb_piecewise", "lb_piecewise_sym", "load", "nn_merge", "nn_search", "release_workspace"]
+__all__ = ["Communicator", "DtwlbError", "KEOGH_ONLY", "MAX_K", "NO_PREFILTER", "dtw_band", "get_unique_id",
+           "lb_envelope", "lb_improved", "lb_keogh", "lb_piecewise", "lb_piecewise_sym", "load", "nn_merge",
+           "nn_search", "release_workspace"]

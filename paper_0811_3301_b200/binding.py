@@ -36,7 +36,8 @@ EXCHANGE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int64, ctypes.c_v
 class NnOpts(ctypes.Structure):
     _fields_ = [("eps", ctypes.c_float), ("index_base", ctypes.c_int64), ("query_block", ctypes.c_int32),
                 ("flags", ctypes.c_int32), ("exchange", EXCHANGE_FN), ("exchange_user", ctypes.c_void_p),
-                ("db_env", ctypes.c_void_p), ("shards", ctypes.c_int32), ("exchange_walk", ctypes.c_int32)]
+                ("db_env", ctypes.c_void_p), ("shards", ctypes.c_int32), ("exchange_walk", ctypes.c_int32),
+                ("nccl_comm", ctypes.c_void_p)]
 
 
 class _DeviceArray:
@@ -74,7 +75,8 @@ class NnStats(ctypes.Structure):
 
 
 EXPORTS = ["lb_envelope", "lb_keogh", "lb_piecewise", "lb_piecewise_sym", "lb_improved", "dtw_band", "nn_search",
-           "nn_merge", "dtwlb_last_error", "dtwlb_release_workspace"]
+           "nn_merge", "dtwlb_last_error", "dtwlb_release_workspace", "dtwlb_get_unique_id", "dtwlb_comm_init",
+           "dtwlb_comm_destroy"]
 
 _lib = None
 
@@ -98,6 +100,11 @@ def load():
         lib.nn_merge.argtypes = [vp, vp, i32, i64, i32, vp, vp, vp]
         for f in ("lb_envelope", "lb_keogh", "lb_piecewise", "lb_piecewise_sym", "lb_improved", "dtw_band",
                   "nn_search", "nn_merge"):
+            getattr(lib, f).restype = ctypes.c_int
+        lib.dtwlb_get_unique_id.argtypes = [vp]
+        lib.dtwlb_comm_init.argtypes = [vp, i32, i32, ctypes.POINTER(ctypes.c_void_p)]
+        lib.dtwlb_comm_destroy.argtypes = [vp]
+        for f in ("dtwlb_get_unique_id", "dtwlb_comm_init", "dtwlb_comm_destroy"):
             getattr(lib, f).restype = ctypes.c_int
         lib.dtwlb_last_error.restype = ctypes.c_char_p
         lib.dtwlb_last_error.argtypes = []
@@ -190,8 +197,9 @@ def dtw_band(x: torch.Tensor, y: torch.Tensor, w: int, p: int) -> torch.Tensor:
 
 
 def _opts(eps, index_base, query_block, keogh_only, prefilter=True, cascade=True, exchange=None, stream=True,
-          db_env=None, shards=0, exchange_walk=0):
+          db_env=None, shards=0, exchange_walk=0, nccl_comm=None):
     o = NnOpts()
+    o.nccl_comm = nccl_comm.handle if isinstance(nccl_comm, Communicator) else nccl_comm
     o.shards = shards
     o.exchange_walk = exchange_walk
     if exchange is not None:
@@ -208,7 +216,7 @@ def _opts(eps, index_base, query_block, keogh_only, prefilter=True, cascade=True
 def nn_search(queries, db, w: int, p: int, k: int, *, eps: float = 1e-3, index_base: int = 0,
               query_block: int = 0, keogh_only: bool = False, prefilter: bool = True, cascade: bool = True,
               stream: bool = True, db_env=None, exchange=None, out=None, shards: int = 0,
-              exchange_walk: int = 0, return_stats: bool = False):
+              exchange_walk: int = 0, nccl_comm=None, return_stats: bool = False):
     """Exact k-NN under banded DTW_p.  Returns (idx int64 [Q][k], dist float32 [Q][k]).
 
     queries/db may be CUDA tensors (device path) or host tensors / numpy arrays
@@ -223,7 +231,8 @@ def nn_search(queries, db, w: int, p: int, k: int, *, eps: float = 1e-3, index_b
     number of shards the exchange combines: each shard's best-first seed range is 1/shards of
     the single-database one (speed only); ``exchange_walk`` (0..3) adds that many exchange calls
     inside the last range's DTW walk (after its rounds 2, 4, 6): a block then makes
-    1 + exchange_walk calls on every shard.
+    1 + exchange_walk calls on every shard.  ``nccl_comm`` (a ``Communicator``) makes the library
+    itself min-reduce the thresholds at those points with NCCL, instead of ``exchange``.
     """
     host = not (isinstance(queries, torch.Tensor) and queries.is_cuda)
     if host:
@@ -247,7 +256,7 @@ def nn_search(queries, db, w: int, p: int, k: int, *, eps: float = 1e-3, index_b
         if tuple(db_env.shape) != (2, N, n):
             raise ValueError(f"db_env must be [2][N][n] = [2][{N}][{n}], got {tuple(db_env.shape)}")
     o = _opts(eps, index_base, query_block, keogh_only, prefilter, cascade, cb, stream, db_env, shards,
-              exchange_walk)
+              exchange_walk, nccl_comm)
     st = NnStats()
     _check(load().nn_search(queries.data_ptr(), Q, db.data_ptr(), N, n, w, p, k, idx.data_ptr(),
                             dist.data_ptr(), ctypes.byref(o), ctypes.byref(st) if return_stats else None,
@@ -271,3 +280,35 @@ def nn_merge(in_idx: torch.Tensor, in_dist: torch.Tensor):
 
 def release_workspace():
     load().dtwlb_release_workspace()
+
+
+class Communicator:
+    """The library's NCCL communicator (dtwlb_comm_init) for the database-sharded search's
+    threshold exchange (nn_opts.nccl_comm).  Create it on every rank with the same 128-byte id."""
+
+    def __init__(self, unique_id: bytes, nranks: int, rank: int):
+        if len(unique_id) != 128:
+            raise ValueError("unique_id must be the 128 bytes of dtwlb_get_unique_id")
+        h = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        _check(load().dtwlb_comm_init(buf, nranks, rank, ctypes.byref(h)))
+        self.handle = h.value
+        self.nranks, self.rank = nranks, rank
+
+    def close(self):
+        if self.handle:
+            _check(load().dtwlb_comm_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def get_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0; broadcast it to the other ranks)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load().dtwlb_get_unique_id(buf))
+    return buf.raw

@@ -19,7 +19,8 @@ CHECKED = os.environ.get("DTWLB_CHECKED") == "1"  # debug build with device boun
 LIB = os.path.join(HERE, "libdtwlb_checked.so" if CHECKED else "libdtwlb.so")
 OBJ = os.path.join(HERE, "_obj_checked" if CHECKED else "_obj")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
-SOURCES = ["abi.cu", "envelope.cu", "keogh.cu", "stream.cu", "improved.cu", "dtw.cu", "dtw_wide.cu", "search.cu"]
+SOURCES = ["abi.cu", "envelope.cu", "keogh.cu", "stream.cu", "improved.cu", "dtw.cu", "dtw_wide.cu", "search.cu",
+           "comm.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-I", INCLUDE] + (["-DDTWLB_CHECKED"] if CHECKED else [])
@@ -49,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs = list(ex.map(compile_one, SOURCES))
     tmp = LIB + f".{os.getpid()}.tmp"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
-           "-o", tmp, *objs]
+           "-o", tmp, *objs, "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -180,12 +180,24 @@ int lb_improved(const float *q, const float *q_env, const float *db, int64_t Q, 
     CHECK_ARG(q && q_env && db && out, "lb_improved: NULL pointer");
     DTWLB_TRY(require_device());
     const int epl = improved_epl(n);
-    if (epl == 0) {
-        set_error(DTWLB_EUNSUPPORTED, "lb_improved: n = %d > 1024 unsupported", n);
-        return DTWLB_EUNSUPPORTED;
-    }
     std::lock_guard<std::mutex> lock(api_mutex());
     cudaStream_t st = as_stream(stream);
+    if (epl == 0) {  // n > 1024: the generic warp-per-pair kernel (same closed form)
+        const int64_t ldb = N;
+        float *beta1, *env, *dbenv;
+        DTWLB_TRY(ws_get_bytes(0, sizeof(float) * Q * ldb, (void **)&beta1));
+        DTWLB_TRY(ws_get_bytes(1, sizeof(float) * 3 * Q * n, (void **)&env));
+        DTWLB_TRY(ws_get_bytes(3, sizeof(float) * 2 * N * n, (void **)&dbenv));
+        const float *U = q_env, *L = q_env + Q * n;
+        float *LU = env, *UL = env + Q * n, *scr = env + 2 * Q * n;
+        DTWLB_TRY(launch_keogh(U, L, db, Q, N, n, p, false, beta1, ldb, st));
+        DTWLB_TRY(launch_envelope(L, n, w, LU, scr, Q, st));
+        DTWLB_TRY(launch_envelope(U, n, w, scr, UL, Q, st));
+        DTWLB_TRY(launch_envelope(db, n, w, dbenv, dbenv + N * n, N, st));
+        DTWLB_TRY(launch_improved_generic(q, LU, UL, dbenv, dbenv + N * n, beta1, ldb, Q, N, n, p, out, N, st));
+        DTWLB_CUDA(cudaStreamSynchronize(st));  // workspace reuse safety
+        return DTWLB_OK;
+    }
     const int npadE = 32 * epl;
     const int64_t ldb = (N + 7) / 8 * 8;  // 16-byte rows of the fp16 gate block
     float *beta1, *env, *qpad, *dbenv;

@@ -778,6 +778,48 @@ int launch_imp_p(const ImprovedArgs &a, int epl, bool keogh_only, bool dense, in
 
 }  // namespace
 
+namespace {
+
+// Any n (the dense lb_improved entry point for n > 1024, beyond the survivor kernel's register
+// layout): one warp per (query, candidate) pair, lanes striding over i, the same closed form
+// for the envelope of H; out = rooted(beta1 + beta2) with beta1 from the dense LB_Keogh pass.
+template <int P>
+__global__ void __launch_bounds__(256) improved_generic_kernel(const float *__restrict__ y, const float *__restrict__ LU,
+                                                               const float *__restrict__ UL, const float *__restrict__ Ux,
+                                                               const float *__restrict__ Lx, const float *__restrict__ beta1,
+                                                               int64_t ldb, int64_t Q, int64_t N, int n,
+                                                               float *__restrict__ out, int64_t ldd) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t pr = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; pr < Q * N; pr += nw) {
+        const int64_t q = pr / N, c = pr - q * N;
+        const float *yr = y + q * n, *lur = LU + q * n, *ulr = UL + q * n;
+        const float *uxr = Ux + c * n, *lxr = Lx + c * n;
+        float acc = 0.f;
+        for (int i = lane; i < n; i += 32)
+            acc = accp<P>(acc, max3f(yr[i] - fmaxf(__ldg(uxr + i), lur[i]), fminf(__ldg(lxr + i), ulr[i]) - yr[i], 0.f));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) out[q * ldd + c] = rootp<P>(__ldg(beta1 + q * ldb + c) + acc);
+    }
+}
+
+}  // namespace
+
+int launch_improved_generic(const float *y, const float *LU, const float *UL, const float *Ux, const float *Lx,
+                            const float *beta1, int64_t ldb, int64_t Q, int64_t N, int n, int p, float *out,
+                            int64_t ldd, cudaStream_t st) {
+    if (Q == 0 || N == 0) return DTWLB_OK;
+    const int64_t warps = Q * N;
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(warps * 32, 256), 148 * 64);
+    if (p == 1)
+        improved_generic_kernel<1><<<grid, 256, 0, st>>>(y, LU, UL, Ux, Lx, beta1, ldb, Q, N, n, out, ldd);
+    else
+        improved_generic_kernel<2><<<grid, 256, 0, st>>>(y, LU, UL, Ux, Lx, beta1, ldb, Q, N, n, out, ldd);
+    DTWLB_LAUNCH_CHECK();
+    return DTWLB_OK;
+}
+
 // scratch bytes of the per-tile lists: masks (8 B) + queries (4 B) per (tile, query), + counts
 size_t improved_scratch_bytes(int64_t Qb, int64_t N) {
     const int64_t nt = ceil_div(N, 64);

@@ -101,6 +101,10 @@ int launch_improved(const ImprovedArgs &a, int p, bool keogh_only, bool dense, c
 int launch_select(const ImprovedArgs &a, bool dense, cudaStream_t st);
 int launch_survivor(const ImprovedArgs &a, int p, bool keogh_only, bool dense, cudaStream_t st);
 int improved_epl(int n);  // elements per lane (4, 8, 16, 32); 0 if n > 1024 (unsupported fast path)
+// dense LB_Improved for any n: rooted(beta1 + beta2) per pair, beta1 dense [Q][ldb] (p-th power)
+int launch_improved_generic(const float *y, const float *LU, const float *UL, const float *Ux, const float *Lx,
+                            const float *beta1, int64_t ldb, int64_t Q, int64_t N, int n, int p, float *out,
+                            int64_t ldd, cudaStream_t st);
 
 // Banded DTW (a5).
 struct DtwArgs {

@@ -543,6 +543,8 @@ struct Timer {
 
 }  // namespace
 
+int comm_allreduce_min(void *comm, float *thr, int64_t count, cudaStream_t st);  // comm.cu
+
 // ------------------------------------------------------------------ pipeline
 int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64_t N, int n, int w, int p,
                    int k, int64_t *out_idx_in, float *out_dist_in, const nn_opts *opts, nn_stats *stats,
@@ -550,10 +552,17 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     std::lock_guard<std::mutex> lock(ws_mutex());
     const float eps = opts ? opts->eps : 1e-3f;
     const int64_t index_base = opts ? opts->index_base : 0;
-    const bool keogh_only = opts && (opts->flags & DTWLB_KEOGH_ONLY);
+    bool keogh_only = opts && (opts->flags & DTWLB_KEOGH_ONLY);
     // piecewise-sum pre-filter as the dense gate pass, LB_Keogh on its survivors;
     // not with few queries (stream mode below: the LB_Keogh pass is then memory-bound)
     bool prefilter = !(opts && (opts->flags & DTWLB_NO_PREFILTER));
+    if (improved_epl(n) == 0) {
+        // n > 1024: the survivor kernel keeps a pair's samples in one warp's registers (<= 1024),
+        // so the search runs Alg. 2: LB_Keogh over every pair, then DTW -- exact,
+        // without the LB_Improved pass (the key lists come from the dense LB_Keogh values)
+        keogh_only = true;
+        prefilter = false;
+    }
     // DTW early abandon on rowmin + LB_Keogh terms of the remaining rows (reading c19)
     const bool cascade = !(opts && (opts->flags & DTWLB_NO_CASCADE));
     w = std::min(w, n - 1);
@@ -601,7 +610,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     // ---- a1: envelopes ----
     const int epl = improved_epl(n);
     const int npadE = 32 * std::max(epl, 4);
-    const bool fast_improved = epl != 0;
+
     float *env;  // U, L, LU, UL, scratch: [5][Q][n]
     DTWLB_TRY(wsget(S_ENV, (size_t)5 * Q * n, &env));
     float *U = env, *L = env + (size_t)Q * n, *LU = env + 2 * (size_t)Q * n, *UL = env + 3 * (size_t)Q * n,
@@ -755,6 +764,16 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     static const int env_S = [] { const char *e = getenv("DTWLB_SEED"); return e ? atoi(e) : 0; }();
     // (a database shard seeds from 1/G of the whole database's seed range, nn_opts.shards)
     const int64_t shards = opts && opts->shards > 1 ? opts->shards : 1;
+    // the shard threshold exchange: the caller's callback, or the library's NCCL all-reduce MIN
+    const bool has_exchange = opts && (opts->exchange || opts->nccl_comm);
+    auto exchange_thr = [&](float *thr, int64_t count) -> int {
+        if (opts->exchange) {
+            opts->exchange(thr, count, opts->exchange_user);
+            DTWLB_CUDA(cudaGetLastError());
+            return DTWLB_OK;
+        }
+        return comm_allreduce_min(opts->nccl_comm, thr, count, st);
+    };
     // (N / 768: measured seed sweeps, profiles/r02n_seed_sweep.txt -- C5 (N = 10^6) is flat for
     // S in 512..2048, C3 (10^5) and C4 (2 10^5) are 7-9 % faster at 256 than at the old N/64)
     const int64_t S = std::max<int64_t>(std::max<int64_t>(256, 4LL * k),
@@ -872,7 +891,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
             DTWLB_LAUNCH_CHECK();
             if (stats) ev0 = rec();
             // ---- a4: LB_Improved on the range's LB_Keogh survivors ----
-            if (fast_improved) {
+            {
                 ImprovedArgs ia{};
                 ia.yq = qpad + qb0 * npadE;
                 ia.LUq = qpad + (size_t)Q * npadE + qb0 * npadE;
@@ -929,7 +948,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 if (over) set_error(DTWLB_ENOMEM, "key lists of %lld keys exceed DTWLB_LIST_POOL_MAX", (long long)total);
                 if (over || (loff_r && wsget(S_LIST, (size_t)std::max<int64_t>(total, 1), &list) != DTWLB_OK) ||
                     wsget(S_COUNT, (size_t)max_runs * 2 + 64, &d_runs) != DTWLB_OK) {
-                    if (qn == 1 || (opts && opts->exchange)) return DTWLB_ENOMEM;  // (error set by wsget)
+                    if (qn == 1 || has_exchange) return DTWLB_ENOMEM;  // (error set by wsget)
                     redo = true;
                     break;
                 }
@@ -938,9 +957,6 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 ia.cap = rcap;
                 ia.loff = loff_r;
                 DTWLB_TRY(launch_survivor(ia, p, keogh_only, false, st));
-            } else {
-                set_error(DTWLB_EUNSUPPORTED, "nn_search: n = %d > 1024 not supported", n);
-                return DTWLB_EUNSUPPORTED;
             }
             // ---- a3: sort each query's list in runs (run list built on the device) ----
             if (stats) span(ev_s0, ev_s1, &ms_survivor);
@@ -975,7 +991,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
             // shard threshold exchanges inside the last range's walk (nn_opts.exchange_walk):
             // after its rounds 2, 4, .., 2 * ex_walk; calls left when the walk ends early are made
             // after it, so every shard makes the same number of calls per block
-            const int ex_walk = (opts && opts->exchange && macro == R - 1 && macro > 0)
+            const int ex_walk = (has_exchange && macro == R - 1 && macro > 0)
                                     ? std::max(0, std::min(3, (int)opts->exchange_walk)) : 0;
             int range_round = 0, ex_done = 0;
             for (bool walking = true; walking;) {
@@ -1084,8 +1100,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                     }
                     DTWLB_TRY(launch_topk_merge(da, st));  // a6: the round's completed pairs -> top-k, tau
                     if (ex_done < ex_walk && range_round == 2 * (ex_done + 1)) {
-                        opts->exchange(s.thr, qn, opts->exchange_user);  // (stream-ordered)
-                        DTWLB_CUDA(cudaGetLastError());
+                        DTWLB_TRY(exchange_thr(s.thr, qn));  // (stream-ordered)
                         ++ex_done;
                     }
                 }
@@ -1096,14 +1111,11 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                     walking = tot0 > 0;
                 }
             }
-            for (; ex_done < ex_walk; ++ex_done) {  // the walk ended before its scheduled exchanges
-                opts->exchange(s.thr, qn, opts->exchange_user);
-                DTWLB_CUDA(cudaGetLastError());
-            }
-            if (opts && opts->exchange && macro + 1 < R) {
+            for (; ex_done < ex_walk; ++ex_done)  // the walk ended before its scheduled exchanges
+                DTWLB_TRY(exchange_thr(s.thr, qn));
+            if (has_exchange && macro + 1 < R) {
                 // a7: shard threshold exchange after the best-first range (stream-ordered)
-                opts->exchange(s.thr, qn, opts->exchange_user);
-                DTWLB_CUDA(cudaGetLastError());
+                DTWLB_TRY(exchange_thr(s.thr, qn));
             }
             if (stats) {
                 const cudaEvent_t e2 = rec();

@@ -50,14 +50,34 @@ def common_query_block(N_shard: int, group: Optional[dist.ProcessGroup] = None, 
     return qb
 
 
+def broadcast_unique_id(group: Optional[dist.ProcessGroup] = None, device=None) -> bytes:
+    """Rank 0's 128-byte NCCL id (dtwlb_get_unique_id), broadcast to every rank of `group`."""
+    from . import binding
+    buf = torch.zeros(128, dtype=torch.uint8, device=device)
+    if dist.get_rank(group) == 0:
+        buf.copy_(torch.frombuffer(bytearray(binding.get_unique_id()), dtype=torch.uint8))
+    dist.broadcast(buf, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    return bytes(buf.cpu().numpy().tobytes())
+
+
+def make_communicator(group: Optional[dist.ProcessGroup] = None, device=None):
+    """The library's NCCL communicator over `group` (nn_opts.nccl_comm): rank 0 creates the
+    128-byte id, torch.distributed broadcasts it, every rank joins on its current device."""
+    from . import binding
+    uid = broadcast_unique_id(group, device)
+    return binding.Communicator(uid, dist.get_world_size(group), dist.get_rank(group))
+
+
 def sharded_nn_search(queries: torch.Tensor, db_shard: torch.Tensor, shard_lo: int, w: int, p: int, k: int,
                       group: Optional[dist.ProcessGroup] = None,
                       search: Optional[Callable] = None, merge: Optional[Callable] = None,
-                      out_local=None, gather_bufs=None, query_block: Optional[int] = None):
+                      out_local=None, gather_bufs=None, query_block: Optional[int] = None, comm=None):
     """Global k-NN over the union of all ranks' shards; every rank gets the result.
 
     Shards with fewer than k rows contribute their whole shard padded with
-    (index -1, distance +inf), which the merge ignores.
+    (index -1, distance +inf), which the merge ignores.  ``comm`` (make_communicator) makes the
+    library min-reduce the thresholds itself with NCCL (no Python in the search loop); it is used
+    only when every shard holds >= k rows (checked collectively), else the Python exchange runs.
     """
     if search is None or merge is None:
         from . import binding
@@ -73,7 +93,14 @@ def sharded_nn_search(queries: torch.Tensor, db_shard: torch.Tensor, shard_lo: i
         kw["query_block"] = query_block or common_query_block(db_shard.shape[0], group, dev)
         kw["shards"] = world  # each shard seeds from 1/world of the best-first range
         kw["exchange_walk"] = EXCHANGE_WALK  # + exchanges inside the last range's walk
-        if kk >= k:
+        use_comm = False
+        if comm is not None:  # every rank must take the same path: min over the shards of kk
+            t = torch.tensor([kk], dtype=torch.int64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+            use_comm = int(t.item()) >= k
+        if use_comm:
+            kw["nccl_comm"] = comm
+        elif kk >= k:
             kw["exchange"] = lambda thr: dist.all_reduce(thr, op=dist.ReduceOp.MIN, group=group)
         else:
             # a shard with fewer than k rows: its kk-th best is NOT an upper bound on the global

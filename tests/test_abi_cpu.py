@@ -76,3 +76,19 @@ def test_no_device_means_ecuda_not_fallback(lib):
     st = lib.lb_envelope(ctypes.c_void_p(a), 8, 1, ctypes.c_void_p(a + 64), ctypes.c_void_p(a + 128), 2, None)
     assert st == 4, st                                                    # DTWLB_ECUDA
     assert b"device" in lib.dtwlb_last_error().lower()
+
+
+def test_communicator_bootstrap_without_device(lib):
+    """dtwlb_get_unique_id needs no GPU (NCCL builds the id from the host); dtwlb_comm_init
+    validates its arguments, then reports ECUDA without an sm_100 device -- never a fallback."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    buf = ctypes.create_string_buffer(128)
+    st = lib.dtwlb_get_unique_id(buf)
+    assert st in (0, 5), st                                       # OK, or ENCCL if NCCL is absent
+    h = ctypes.c_void_p()
+    assert lib.dtwlb_comm_init(buf, 2, 2, ctypes.byref(h)) == 1   # rank outside [0, nranks)
+    assert lib.dtwlb_comm_init(None, 1, 0, ctypes.byref(h)) == 1  # NULL id
+    assert lib.dtwlb_comm_init(buf, 1, 0, ctypes.byref(h)) == 4   # no device: ECUDA
+    assert lib.dtwlb_comm_destroy(None) == 0

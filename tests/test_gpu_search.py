@@ -285,3 +285,21 @@ def test_key_list_pool_redo(cuda_ok):
     env = dict(os.environ, DTWLB_LIST_POOL_MAX="3000")  # ~40 queries x 6000 x a few % survive per range
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("n,w,p", [(1100, 40, 2), (1500, 150, 1)])
+def test_long_series_beyond_survivor_kernel(cuda_ok, n, w, p):
+    """n > 1024 (beyond the survivor kernel's 32 samples per lane): nn_search runs Alg. 2
+    (LB_Keogh over every pair, then the DTW walk; any n must work) and lb_improved
+    the warp-per-pair kernel; both against the oracle."""
+    from paper_0811_3301_b200 import lb_envelope, lb_improved
+    rng = np.random.default_rng(n + w)
+    qs = np.cumsum(rng.standard_normal((5, n)), axis=1).astype(np.float32)
+    db = np.cumsum(rng.standard_normal((700, n)), axis=1).astype(np.float32)
+    db[123] = qs[2] + np.float32(0.01)
+    check(qs, db, w, p, 3)
+    U, L = lb_envelope(dev(qs), w)
+    env = torch.stack([U, L]).contiguous()
+    got = lb_improved(dev(qs), env, dev(db[:40]), w, p).cpu().numpy()
+    want = np.array([[oracle.lb_improved(db[c], qs[q], w, p) for c in range(40)] for q in range(5)])
+    assert np.allclose(got, want, rtol=1e-5, atol=1e-6)

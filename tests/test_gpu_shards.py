@@ -132,3 +132,25 @@ def test_nn_merge_against_host_merge(cuda_ok):
         ri, rd = merge_reference(torch.from_numpy(i), torch.from_numpy(d))
         assert np.array_equal(gi.cpu().numpy(), ri.numpy())
         assert np.array_equal(gd.cpu().numpy(), rd.numpy())
+
+
+def test_library_nccl_exchange_single_rank(cuda_ok):
+    """nn_opts.nccl_comm: the library's own NCCL communicator (dtwlb_get_unique_id /
+    dtwlb_comm_init, one rank on this GPU) min-reduces the thresholds at every exchange point
+    (after the first range and 3 times inside the last walk) on the call's stream; with one
+    rank the reduction is the identity, so the result equals the unsharded search bit for bit."""
+    from paper_0811_3301_b200 import Communicator, get_unique_id, nn_search
+    c = datagen.CONFIGS["C2p2"]
+    qs, db = datagen.make(c, Q=24, N=10_000)
+    comm = Communicator(get_unique_id(), 1, 0)
+    try:
+        a_idx, a_dst = nn_search(dev(qs), dev(db), c.w, c.p, 3, query_block=8, nccl_comm=comm, shards=1,
+                                 exchange_walk=3)
+        torch.cuda.synchronize()
+    finally:
+        comm.close()
+    b_idx, b_dst = nn_search(dev(qs), dev(db), c.w, c.p, 3, query_block=8)
+    assert np.array_equal(a_idx.cpu().numpy(), b_idx.cpu().numpy())
+    assert np.array_equal(a_dst.cpu().numpy(), b_dst.cpu().numpy())
+    o_idx, o_dst = oracle.nn_brute(qs, db, c.w, c.p, 3 + 8, threads=THREADS)
+    assert_knn_match(a_idx.cpu().numpy(), a_dst.cpu().numpy(), o_idx, o_dst, 3)

@@ -332,3 +332,40 @@ def test_query_sharded_equals_global(Q):
         assert np.array_equal(idx, o_idx)
         assert np.allclose(dst, o_dst, rtol=1e-6)
         assert calls == [Q // 2 if rank == 0 else Q - Q // 2]
+
+
+def _worker_uid(rank, world, port, result_q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_0811_3301_b200.binding import DtwlbError
+        from paper_0811_3301_b200.sharded import broadcast_unique_id
+        try:
+            uid = broadcast_unique_id()
+        except DtwlbError as e:  # NCCL not loadable in this image: nothing to bootstrap
+            uid = repr(e).encode()
+        result_q.put((rank, uid))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:
+        result_q.put((rank, repr(e).encode()))
+        raise
+
+
+def test_communicator_id_broadcast():
+    """Bootstrap of the library's NCCL communicator (nn_opts.nccl_comm): rank 0's 128-byte
+    dtwlb_get_unique_id reaches every rank unchanged (gloo here; the GPU ranks then call
+    dtwlb_comm_init with it)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_uid, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert res[0] == res[1]
+    assert len(res[0]) == 128
