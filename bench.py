@@ -415,17 +415,19 @@ def run_ours(args, cfg):
                                   "unit": "Tlane-op/s", "peak": peak,
                                   "note": "3 slots per in-band DTW cell actually computed (kernel counter, early "
                                           "abandon), CUDA events around every walk-round launch"}
-        # Measured instruction-mix peaks (scripts/isa_probe.cu, event-timed, profiles/r02h_isa_probe.txt):
+        # Measured instruction-mix peaks (scripts/isa_probe.cu, event-timed, profiles/r02h_isa_probe.txt,
+        # profiles/r02x_isa_probe.txt for the midpoint-form gate element):
         # the same SASS sequences in 8 independent chains per thread, 32 warps per SM, elements (cells)
         # per SM clock.  FMNMX3 and the packed f32x2 ops issue at half rate and FFMA2 at a third, so a
         # bound element costs more than 3 issue slots: these are the kernels' attainable ALU roofs.
-        mix = {"dtw_cell": 42.0, "lbk_elem": 26.0, "lbi_elem": 25.3, "gate_elem": 24.5, "lbk_packed": 27.7}
+        mix = {"dtw_cell": 42.0, "lbk_elem": 26.0, "lbi_elem": 25.3, "gate_elem": 26.8, "lbk_packed": 27.7,
+               "lb_pair": 24.6}  # lb_pair: FADD2 x2, FMNMX3 x2, FFMA x2 per element pair (streaming pass)
         clk_sm = n_sm * sm_clock * 1e6  # SM-clocks per second, whole GPU
         if "bound_pass" in kern and kern["bound_pass"]["bound"] == "alu":
             kern["bound_pass"]["mix_peak"] = 3.0 * mix["gate_elem"] * clk_sm / 1e12
         if "bound_pass" in kern and kern["bound_pass"]["bound"] == "hbm":
             # the LB_Keogh arithmetic caps the streaming pass too: Q pair-elements per database element
-            rate = mix["lbk_packed"] if 4 < cfg.Q <= 8 else mix["gate_elem"]
+            rate = mix["lbk_packed"] if 4 < cfg.Q <= 8 else mix["lb_pair"]
             kern["bound_pass"]["alu_cap"] = rate * clk_sm / cfg.Q * 4 / 1e9  # GB/s of database
             kern["bound_pass"]["mix_peak"] = min(hbm_peak, kern["bound_pass"]["alu_cap"])
         if "survivor_kernel" in kern:

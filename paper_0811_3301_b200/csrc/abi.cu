@@ -155,13 +155,13 @@ int lb_piecewise_sym(const float *q, const float *q_env, const float *db, int64_
     DTWLB_TRY(ws_get_bytes(8, sizeof(float) * 4 * N * Dp, (void **)&xs));
     DTWLB_TRY(ws_get_bytes(9, sizeof(float) * 4 * Q * Dp, (void **)&qs));
     DTWLB_TRY(ws_get_bytes(3, sizeof(float) * 2 * N * n, (void **)&dbenv));
-    // forward operands: candidate sums, query envelope sums
-    DTWLB_TRY(launch_paa_sums(db, N, n, xs, xs + N * Dp, st));
-    DTWLB_TRY(launch_paa_env_sums(q_env, q_env + Q * n, Q, n, qs, qs + Q * Dp, st));
-    // reverse operands: candidate envelope sums, query sums
+    // forward operands: candidate sums, query envelope boxes (midpoint-radius form)
+    DTWLB_TRY(launch_paa_mid(db, db, N, n, xs, xs + N * Dp, false, st));
+    DTWLB_TRY(launch_paa_mid(q_env + Q * n, q_env, Q, n, qs, qs + Q * Dp, true, st));
+    // reverse operands: candidate envelope boxes, query sums
     DTWLB_TRY(launch_envelope(db, n, w, dbenv, dbenv + N * n, N, st));
-    DTWLB_TRY(launch_paa_env_sums(dbenv, dbenv + N * n, N, n, xs + 2 * N * Dp, xs + 3 * N * Dp, st));
-    DTWLB_TRY(launch_paa_sums(q, Q, n, qs + 2 * Q * Dp, qs + 3 * Q * Dp, st));
+    DTWLB_TRY(launch_paa_mid(dbenv + N * n, dbenv, N, n, xs + 2 * N * Dp, xs + 3 * N * Dp, true, st));
+    DTWLB_TRY(launch_paa_mid(q, q, Q, n, qs + 2 * Q * Dp, qs + 3 * Q * Dp, false, st));
     // both terms, max-combined, in one pass (the kernel nn_search's gate runs)
     DTWLB_TRY(launch_paa_bound_sym(qs, qs + Q * Dp, qs + 2 * Q * Dp, qs + 3 * Q * Dp, xs, xs + N * Dp, xs + 2 * N * Dp,
                                    xs + 3 * N * Dp, Q, N, n, p, true, out, N, st));

@@ -158,18 +158,28 @@ select_mask8_kernel(const __half *__restrict__ gate, int64_t ldb, int64_t Qb, in
     const bool inrow = c0 < ldb;
     const int nvalid = c0 >= N ? 0 : (N - c0 >= 8 ? 8 : (int)(N - c0));
     unsigned bk[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // query q0 + lane: ballot k (candidate 8l + k of lane l)
-#pragma unroll 8
-    for (int j = 0; j < nq; ++j) {
-        uint4 raw = make_uint4(0x7c007c00u, 0x7c007c00u, 0x7c007c00u, 0x7c007c00u);  // +inf
-        if (inrow) raw = __ldg(reinterpret_cast<const uint4 *>(gate + (q0 + j) * ldb + c0));
-        const float l = __shfl_sync(0xffffffffu, my_l, j), h = __shfl_sync(0xffffffffu, my_h, j);
-        const unsigned wv[4] = {raw.x, raw.y, raw.z, raw.w};
+    // eight rows' loads issued before their ballots (the compiler kept one in flight per warp
+    // when each load fed its ballots directly: the pass ran at ~half of the HBM bandwidth)
+    for (int j0 = 0; j0 < nq; j0 += 8) {
+        uint4 raws[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const float v = __half2float(__ushort_as_half((unsigned short)((k & 1) ? wv[k >> 1] >> 16 : wv[k >> 1] & 0xffffu)));
-            // (test c < N explicitly: the +inf / padding must not pass a range whose hi is +inf)
-            const unsigned b = __ballot_sync(0xffffffffu, k < nvalid && v > l && v <= h);
-            if (lane == j) bk[k] = b;
+        for (int u = 0; u < 8; ++u) {
+            raws[u] = make_uint4(0x7c007c00u, 0x7c007c00u, 0x7c007c00u, 0x7c007c00u);  // +inf
+            if (inrow && j0 + u < nq) raws[u] = __ldg(reinterpret_cast<const uint4 *>(gate + (q0 + j0 + u) * ldb + c0));
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = j0 + u;
+            if (j >= nq) break;
+            const float l = __shfl_sync(0xffffffffu, my_l, j), h = __shfl_sync(0xffffffffu, my_h, j);
+            const unsigned wv[4] = {raws[u].x, raws[u].y, raws[u].z, raws[u].w};
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const float v = __half2float(__ushort_as_half((unsigned short)((k & 1) ? wv[k >> 1] >> 16 : wv[k >> 1] & 0xffffu)));
+                // (test c < N explicitly: the +inf / padding must not pass a range whose hi is +inf)
+                const unsigned b = __ballot_sync(0xffffffffu, k < nvalid && v > l && v <= h);
+                if (lane == j) bk[k] = b;
+            }
         }
     }
     unsigned long long m[4];

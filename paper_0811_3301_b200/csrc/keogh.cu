@@ -19,12 +19,13 @@
 // sides, which contributes max(0-0, 0-0, 0) = 0.
 //
 // The same tile kernel evaluates the piecewise-sum pre-filter over
-// segment sums (PAA = true): D = n/8 "samples" per row, directed rounding.  With
-// REV it evaluates the REVERSE piecewise-sum bound -- the query's segment sums
-// against the candidate's envelope sums, sum_j d(P(y)_j, [P(L(x))_j, P(U(x))_j])^p,
-// a lower bound of LB_Keogh_p(y, x) <= DTW_p(y, x) = DTW_p(x, y) (symmetry, P:1052;
-// DESIGN.md reading c20) -- and stores max(stored bound, reverse bound): the
-// symmetric gate of the cascade.
+// segment sums (PAA = true): D = n/8 "samples" per row, directed rounding (the forward
+// term alone: the C-ABI lb_piecewise).  nn_search's symmetric gate -- the max of this
+// forward term and the REVERSE term, the query's segment sums against the candidate's
+// envelope sums, sum_j d(P(y)_j, [P(L(x))_j, P(U(x))_j])^p, a lower bound of
+// LB_Keogh_p(y, x) <= DTW_p(y, x) = DTW_p(x, y) (symmetry; DESIGN.md reading
+// c20) -- is gate_sym_kernel below.
+#include <cfloat>
 #include <cstdlib>
 
 #include <cuda_fp16.h>
@@ -108,7 +109,7 @@ __device__ __forceinline__ float lb_elem(float acc, float xl, float xh, float u,
     }
 }
 
-template <int P, bool VEC, bool ROOTED, bool PAA, bool REV>
+template <int P, bool VEC, bool ROOTED, bool PAA>
 __global__ void __launch_bounds__(NT, 2)
 keogh_tile_kernel(const float *__restrict__ U, const float *__restrict__ L, const float *__restrict__ db,
                   const float *__restrict__ db2, int64_t Q, int64_t N, int n, void *__restrict__ out,
@@ -174,16 +175,7 @@ keogh_tile_kernel(const float *__restrict__ U, const float *__restrict__ L, cons
                 if constexpr (PAA) xw = *reinterpret_cast<const float4 *>(&s.X2[cg + 16 * j][k]);
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    if constexpr (PAA && REV) {
-                        // query side (U, L slots) = (P(y) lo, P(y) hi); candidate side (X, X2
-                        // slots) = (P(U(x)) hi, P(L(x)) lo): d = max(ylo - Uxhi, Lxlo - yhi, 0)
-                        float t = acc[r][j];
-                        t = lb_elem2<P, PAA>(t, make_float2(uv[r].x, uv[r].y), make_float2(lv[r].x, lv[r].y),
-                                             make_float2(xv.x, xv.y), make_float2(xw.x, xw.y));
-                        t = lb_elem2<P, PAA>(t, make_float2(uv[r].z, uv[r].w), make_float2(lv[r].z, lv[r].w),
-                                             make_float2(xv.z, xv.w), make_float2(xw.z, xw.w));
-                        acc[r][j] = t;
-                    } else if constexpr (PAA) {
+                    if constexpr (PAA) {
                         float t = acc[r][j];
                         t = lb_elem2<P, PAA>(t, make_float2(xv.x, xv.y), make_float2(xw.x, xw.y),
                                              make_float2(uv[r].x, uv[r].y), make_float2(lv[r].x, lv[r].y));
@@ -229,20 +221,20 @@ keogh_tile_kernel(const float *__restrict__ U, const float *__restrict__ L, cons
             if constexpr (PAA && !ROOTED) {  // nn_search's gate block: fp16, rounded down (still a lower bound)
                 __half *o = reinterpret_cast<__half *>(out) + q * ldo + c;
                 const __half h = __float2half_rd(v);
-                *o = REV ? __hmax(*o, h) : h;  // max of two lower bounds
+                *o = h;
             } else {
                 float *o = reinterpret_cast<float *>(out) + q * ldo + c;
-                *o = REV ? fmaxf(*o, v) : v;
+                *o = v;
             }
         }
     }
 }
 
-template <int P, bool VEC, bool ROOTED, bool PAA, bool REV>
+template <int P, bool VEC, bool ROOTED, bool PAA>
 int launch_tile_t(const float *U, const float *L, const float *db, const float *db2, int64_t Q, int64_t N,
                   int n, void *out, int64_t ldo, cudaStream_t st) {
     const size_t smem = 2 * sizeof(Stage<PAA>);
-    auto k = keogh_tile_kernel<P, VEC, ROOTED, PAA, REV>;
+    auto k = keogh_tile_kernel<P, VEC, ROOTED, PAA>;
     DTWLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t nqt = ceil_div(Q, TQ), nct = ceil_div(N, TC);
     const int64_t tiles = nqt * nct;
@@ -255,14 +247,14 @@ int launch_tile_t(const float *U, const float *L, const float *db, const float *
     return DTWLB_OK;
 }
 
-template <bool PAA, bool REV = false>
+template <bool PAA>
 int launch_tile(const float *U, const float *L, const float *db, const float *db2, int64_t Q, int64_t N, int n,
                 int p, bool rooted, void *out, int64_t ldo, cudaStream_t st) {
     if (Q == 0 || N == 0) return DTWLB_OK;
     const bool vec = (n % 4 == 0) && ((reinterpret_cast<uintptr_t>(U) | reinterpret_cast<uintptr_t>(L) |
                                        reinterpret_cast<uintptr_t>(db) | reinterpret_cast<uintptr_t>(db2)) %
                                       16 == 0);
-#define DTWLB_K(P_, V_, R_) return launch_tile_t<P_, V_, R_, PAA, REV>(U, L, db, db2, Q, N, n, out, ldo, st)
+#define DTWLB_K(P_, V_, R_) return launch_tile_t<P_, V_, R_, PAA>(U, L, db, db2, Q, N, n, out, ldo, st)
     if (p == 1) {
         if (vec) { if (rooted) DTWLB_K(1, true, true); else DTWLB_K(1, true, false); }
         else { if (rooted) DTWLB_K(1, false, true); else DTWLB_K(1, false, false); }
@@ -279,24 +271,46 @@ int launch_tile(const float *U, const float *L, const float *db, const float *db
 // and the reverse term (query sums against the candidate's envelope sums) accumulate in two
 // register tiles and the maximum is written once -- instead of a forward launch writing the
 // fp16 gate block and a reverse launch reading it back (a read-modify-write of the whole block
-// whose load stalled the reverse epilogue).  Same directed rounding, same per-term arithmetic
-// order, so the result equals max(forward launch, reverse launch) bit for bit.  With Dp <= 32
-// (n <= 256) the single chunk is staged once (one 110 KB stage: 2 CTAs per SM).
+// whose load stalled the reverse epilogue).  With Dp <= 32 (n <= 256) the single chunk is staged
+// once (one 110 KB stage: 2 CTAs per SM).
+//
+// Midpoint form (4 full-rate FADD/FFMA per element instead of FADD2 + FMNMX3 + FFMA, which
+// issue at half rate: 4.4 vs 5.3 cycles per element, profiles/r02h_isa_probe.txt).  Every
+// operand is an interval in midpoint-radius form, outward-rounded by paa_mid_kernel: a point
+// sum X_j lies in [m - r, m + r] (r ~ 1 ulp) and a box [P(L)_j, P(U)_j] inside [m - r, m + r].
+// The distance of a point of the first to the second is >= |m_x - m_b| - (r_x + r_b), so
+//   d_j >= max(|m_x - m_b| - R, 0),  R = r_b + max over the CTA's point intervals of r_x
+// (the point radii are ~1 ulp: the tile maximum, taken per segment in shared memory, loosens
+// the bound by ~1e-6 and leaves one radius per element).  Per element, rounded so the fp32
+// value never exceeds the exact one: t1 = m_x - m_b toward zero (|t1| <= |exact|), t2 = |t1| - R
+// rounded down, t3 = t2 + |t2| = 2 max(t2, 0) (exact), acc += t3^p rounded down; the total is
+// scaled by 2^-p (exact) -- the same bound as max(Xlo - Uhi, Llo - Xhi, 0), whose two terms are
+// (t1 sign-split) |m_x - m_b| - R.
 struct SymStage {
-    float X[TC][KP], X2[TC][KP];    // candidate segment sums: lo, hi            (forward)
-    float XR[TC][KP], XR2[TC][KP];  // candidate envelope sums: P(U(x)) hi, P(L(x)) lo (reverse)
-    float U[TQ][KP], L[TQ][KP];     // query envelope sums: P(U(y)) hi, P(L(y)) lo   (forward)
-    float UR[TQ][KP], LR[TQ][KP];   // query sums: P(y) lo, hi                       (reverse)
+    float X[TC][KP], X2[TC][KP];    // candidate segment sums: midpoint, radius            (forward)
+    float XR[TC][KP], XR2[TC][KP];  // candidate envelope boxes [P(L(x)), P(U(x))]: m, r   (reverse)
+    float U[TQ][KP], L[TQ][KP];     // query envelope boxes [P(L(y)), P(U(y))]: m, r       (forward)
+    float UR[TQ][KP], LR[TQ][KP];   // query segment sums: midpoint, radius                (reverse)
 };
+
+template <int P>
+__device__ __forceinline__ float mid_elem(float acc, float mx, float mb, float R) {
+    const float t1 = __fsub_rz(mx, mb);         // |t1| <= |mx - mb|
+    const float t2 = __fsub_rd(fabsf(t1), R);   // <= |mx - mb| - R
+    const float t3 = t2 + fabsf(t2);            // 2 max(t2, 0), exact
+    if constexpr (P == 1) return __fadd_rd(acc, t3);
+    else return __fmaf_rd(t3, t3, acc);
+}
 
 template <int P, bool VEC, bool ROOTED>
 __global__ void __launch_bounds__(NT, 2)
-gate_sym_kernel(const float *__restrict__ Uhi, const float *__restrict__ Llo, const float *__restrict__ Ylo,
-                const float *__restrict__ Yhi, const float *__restrict__ Xlo, const float *__restrict__ Xhi,
-                const float *__restrict__ Uxhi, const float *__restrict__ Lxlo, int64_t Q, int64_t N, int n,
+gate_sym_kernel(const float *__restrict__ Qm, const float *__restrict__ Qr, const float *__restrict__ Ym,
+                const float *__restrict__ Yr, const float *__restrict__ Xm, const float *__restrict__ Xr,
+                const float *__restrict__ Bm, const float *__restrict__ Br, int64_t Q, int64_t N, int n,
                 void *__restrict__ out, int64_t ldo, int nqt) {
     extern __shared__ __align__(16) unsigned char smraw[];
     SymStage *st = reinterpret_cast<SymStage *>(smraw);
+    __shared__ float red[2][8][KC];  // partial tile maxima of the point radii
     const int64_t tile = blockIdx.x;
     const int64_t q0 = (tile % nqt) * TQ;
     const int64_t c0 = (tile / nqt) * TC;
@@ -310,14 +324,14 @@ gate_sym_kernel(const float *__restrict__ Uhi, const float *__restrict__ Llo, co
     const int nchunks = (n + KC - 1) / KC;
     const int nbuf = nchunks > 1 ? 2 : 1;
     auto stage = [&](SymStage &S, int k0) {
-        stage_rows<TC, VEC>(S.X, Xlo, c0, N, n, k0);
-        stage_rows<TC, VEC>(S.X2, Xhi, c0, N, n, k0);
-        stage_rows<TC, VEC>(S.XR, Uxhi, c0, N, n, k0);
-        stage_rows<TC, VEC>(S.XR2, Lxlo, c0, N, n, k0);
-        stage_rows<TQ, VEC>(S.U, Uhi, q0, Q, n, k0);
-        stage_rows<TQ, VEC>(S.L, Llo, q0, Q, n, k0);
-        stage_rows<TQ, VEC>(S.UR, Ylo, q0, Q, n, k0);
-        stage_rows<TQ, VEC>(S.LR, Yhi, q0, Q, n, k0);
+        stage_rows<TC, VEC>(S.X, Xm, c0, N, n, k0);
+        stage_rows<TC, VEC>(S.X2, Xr, c0, N, n, k0);
+        stage_rows<TC, VEC>(S.XR, Bm, c0, N, n, k0);
+        stage_rows<TC, VEC>(S.XR2, Br, c0, N, n, k0);
+        stage_rows<TQ, VEC>(S.U, Qm, q0, Q, n, k0);
+        stage_rows<TQ, VEC>(S.L, Qr, q0, Q, n, k0);
+        stage_rows<TQ, VEC>(S.UR, Ym, q0, Q, n, k0);
+        stage_rows<TQ, VEC>(S.LR, Yr, q0, Q, n, k0);
     };
     stage(st[0], 0);
     cp_commit();
@@ -326,49 +340,64 @@ gate_sym_kernel(const float *__restrict__ Uhi, const float *__restrict__ Llo, co
         cp_commit();
         cp_wait<1>();
         __syncthreads();
-        const SymStage &S = st[ch % nbuf];
+        SymStage &S = st[ch % nbuf];
+        {   // per segment: the tile maxima of the point radii (128 candidates, 64 queries), added
+            // to the other side's box radii (rounded up; FLT_MAX stays the "whole line" padding)
+            const int k = tid & (KC - 1), part = tid >> 5;  // 8 parts
+            float mc = 0.f, mq = 0.f;
+#pragma unroll 4
+            for (int c = part * (TC / 8); c < (part + 1) * (TC / 8); ++c) mc = fmaxf(mc, S.X2[c][k]);
+#pragma unroll 4
+            for (int q = part * (TQ / 8); q < (part + 1) * (TQ / 8); ++q) mq = fmaxf(mq, S.LR[q][k]);
+            red[0][part][k] = mc;
+            red[1][part][k] = mq;
+            __syncthreads();
+            mc = red[0][0][k];
+            mq = red[1][0][k];
+#pragma unroll
+            for (int t = 1; t < 8; ++t) { mc = fmaxf(mc, red[0][t][k]); mq = fmaxf(mq, red[1][t][k]); }
+            for (int q = part; q < TQ; q += 8) S.L[q][k] = fminf(__fadd_ru(S.L[q][k], mc), FLT_MAX);
+            for (int c = part; c < TC; c += 8) S.XR2[c][k] = fminf(__fadd_ru(S.XR2[c][k], mq), FLT_MAX);
+            __syncthreads();
+        }
 #pragma unroll 2
         for (int k = 0; k < KC; k += 4) {
-            {   // forward: d = max(Xlo - Uhi, Llo - Xhi, 0)
-                float4 uv[4], lv[4];
+            {   // forward: candidate sums against the query's envelope box
+                float4 mv[4], rv[4];
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    uv[r] = *reinterpret_cast<const float4 *>(&S.U[4 * qg + r][k]);
-                    lv[r] = *reinterpret_cast<const float4 *>(&S.L[4 * qg + r][k]);
+                    mv[r] = *reinterpret_cast<const float4 *>(&S.U[4 * qg + r][k]);
+                    rv[r] = *reinterpret_cast<const float4 *>(&S.L[4 * qg + r][k]);
                 }
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const float4 xv = *reinterpret_cast<const float4 *>(&S.X[cg + 16 * j][k]);
-                    const float4 xw = *reinterpret_cast<const float4 *>(&S.X2[cg + 16 * j][k]);
 #pragma unroll
                     for (int r = 0; r < 4; ++r) {
                         float t = acc[r][j];
-                        t = lb_elem2<P, true>(t, make_float2(xv.x, xv.y), make_float2(xw.x, xw.y),
-                                              make_float2(uv[r].x, uv[r].y), make_float2(lv[r].x, lv[r].y));
-                        t = lb_elem2<P, true>(t, make_float2(xv.z, xv.w), make_float2(xw.z, xw.w),
-                                              make_float2(uv[r].z, uv[r].w), make_float2(lv[r].z, lv[r].w));
+                        t = mid_elem<P>(t, xv.x, mv[r].x, rv[r].x);
+                        t = mid_elem<P>(t, xv.y, mv[r].y, rv[r].y);
+                        t = mid_elem<P>(t, xv.z, mv[r].z, rv[r].z);
+                        t = mid_elem<P>(t, xv.w, mv[r].w, rv[r].w);
                         acc[r][j] = t;
                     }
                 }
             }
-            {   // reverse: d = max(Ylo - Uxhi, Lxlo - Yhi, 0)
-                float4 yl[4], yh[4];
+            {   // reverse: query sums against the candidate's envelope box
+                float4 yv[4];
 #pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    yl[r] = *reinterpret_cast<const float4 *>(&S.UR[4 * qg + r][k]);
-                    yh[r] = *reinterpret_cast<const float4 *>(&S.LR[4 * qg + r][k]);
-                }
+                for (int r = 0; r < 4; ++r) yv[r] = *reinterpret_cast<const float4 *>(&S.UR[4 * qg + r][k]);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const float4 ux = *reinterpret_cast<const float4 *>(&S.XR[cg + 16 * j][k]);
-                    const float4 lx = *reinterpret_cast<const float4 *>(&S.XR2[cg + 16 * j][k]);
+                    const float4 bm = *reinterpret_cast<const float4 *>(&S.XR[cg + 16 * j][k]);
+                    const float4 br = *reinterpret_cast<const float4 *>(&S.XR2[cg + 16 * j][k]);
 #pragma unroll
                     for (int r = 0; r < 4; ++r) {
                         float t = accr[r][j];
-                        t = lb_elem2<P, true>(t, make_float2(yl[r].x, yl[r].y), make_float2(yh[r].x, yh[r].y),
-                                              make_float2(ux.x, ux.y), make_float2(lx.x, lx.y));
-                        t = lb_elem2<P, true>(t, make_float2(yl[r].z, yl[r].w), make_float2(yh[r].z, yh[r].w),
-                                              make_float2(ux.z, ux.w), make_float2(lx.z, lx.w));
+                        t = mid_elem<P>(t, yv[r].x, bm.x, br.x);
+                        t = mid_elem<P>(t, yv[r].y, bm.y, br.y);
+                        t = mid_elem<P>(t, yv[r].z, bm.z, br.z);
+                        t = mid_elem<P>(t, yv[r].w, bm.w, br.w);
                         accr[r][j] = t;
                     }
                 }
@@ -384,8 +413,11 @@ gate_sym_kernel(const float *__restrict__ Uhi, const float *__restrict__ Llo, co
         for (int j = 0; j < 8; ++j) {
             const int64_t c = c0 + cg + 16 * j;
             if (c >= N) continue;
-            float v = fmaxf(acc[r][j], accr[r][j]);  // max of two lower bounds (exact)
-            if constexpr (P == 2) v = __fmul_rd(v, 1.0f / kSeg);
+            // max of two lower bounds (exact); the accumulators hold sums of (2 d)^p: scale by
+            // 2^-p (exact), and by 1/s for p = 2 (reading c18)
+            float v = fmaxf(acc[r][j], accr[r][j]);
+            if constexpr (P == 2) v = __fmul_rd(v, 0.25f / kSeg);
+            else v = v * 0.5f;
             if constexpr (ROOTED) {
                 if constexpr (P == 2) v = __fsqrt_rd(v);
                 reinterpret_cast<float *>(out)[q * ldo + c] = v;
@@ -397,8 +429,8 @@ gate_sym_kernel(const float *__restrict__ Uhi, const float *__restrict__ Llo, co
 }
 
 template <int P, bool VEC, bool ROOTED>
-int launch_sym_t(const float *Uhi, const float *Llo, const float *Ylo, const float *Yhi, const float *Xlo,
-                 const float *Xhi, const float *Uxhi, const float *Lxlo, int64_t Q, int64_t N, int Dp, void *out,
+int launch_sym_t(const float *Qm, const float *Qr, const float *Ym, const float *Yr, const float *Xm,
+                 const float *Xr, const float *Bm, const float *Br, int64_t Q, int64_t N, int Dp, void *out,
                  int64_t ldo, cudaStream_t st) {
     const int nchunks = (Dp + KC - 1) / KC;
     const size_t smem = (nchunks > 1 ? 2 : 1) * sizeof(SymStage);
@@ -410,7 +442,7 @@ int launch_sym_t(const float *Uhi, const float *Llo, const float *Ylo, const flo
         set_error(DTWLB_EINVAL, "bound pass: problem too large (%lld tiles)", (long long)tiles);
         return DTWLB_EINVAL;
     }
-    k<<<(unsigned)tiles, NT, smem, st>>>(Uhi, Llo, Ylo, Yhi, Xlo, Xhi, Uxhi, Lxlo, Q, N, Dp, out, ldo, (int)nqt);
+    k<<<(unsigned)tiles, NT, smem, st>>>(Qm, Qr, Ym, Yr, Xm, Xr, Bm, Br, Q, N, Dp, out, ldo, (int)nqt);
     DTWLB_LAUNCH_CHECK();
     return DTWLB_OK;
 }
@@ -445,7 +477,51 @@ __global__ void paa_sums_kernel(const float *__restrict__ x, int64_t count, int 
     (void)lo_only_down;
 }
 
+// Midpoint-radius form of the segment sums (the fused gate's operands): one thread per (row,
+// segment); directed fp64 sums s_lo = sum(lo_src) rounded down, s_hi = sum(hi_src) rounded up
+// (lo_src = hi_src = x: the point sum X_j in [s_lo, s_hi]; lo_src = L, hi_src = U: the box
+// [P(L)_j, P(U)_j] inside [s_lo, s_hi]); m = fp32(nearest) of (s_lo + s_hi) / 2 and r = fp32
+// (rounded up) of max(s_hi - m, m - s_lo), so [s_lo, s_hi] lies in [m - r, m + r].  Padding
+// segments: m = 0, r = pad_r (0 for points, FLT_MAX for boxes: "the whole line", d = 0).
+__global__ void paa_mid_kernel(const float *__restrict__ lo_src, const float *__restrict__ hi_src, int64_t count,
+                               int n, float *__restrict__ m_out, float *__restrict__ r_out, float pad_r) {
+    const int D = paa_dims(n), Dp = paa_pitch(n);
+    const int64_t total = count * Dp;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = t / Dp;
+        const int j = (int)(t - r * Dp);
+        if (j >= D) {
+            m_out[t] = 0.f;
+            r_out[t] = pad_r;
+            continue;
+        }
+        const float *lr = lo_src + r * n, *hr = hi_src + r * n;
+        const int i1 = min(n, (j + 1) * kSeg);
+        double sd = 0.0, su = 0.0;
+        for (int i = j * kSeg; i < i1; ++i) {
+            sd = __dadd_rd(sd, (double)__ldg(lr + i));
+            su = __dadd_ru(su, (double)__ldg(hr + i));
+        }
+        const float m = __double2float_rn(0.5 * sd + 0.5 * su);  // (halving is exact)
+        const double md = (double)m;
+        const double rad = fmax(__dsub_ru(su, md), __dsub_ru(md, sd));
+        m_out[t] = m;
+        r_out[t] = fminf(__double2float_ru(rad), FLT_MAX);
+    }
+}
+
 }  // namespace
+
+int launch_paa_mid(const float *lo_src, const float *hi_src, int64_t count, int n, float *m, float *r, bool box,
+                   cudaStream_t st) {
+    if (count == 0) return DTWLB_OK;
+    const int64_t total = count * paa_pitch(n);
+    const int grid = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
+    paa_mid_kernel<<<grid, 256, 0, st>>>(lo_src, hi_src, count, n, m, r, box ? FLT_MAX : 0.f);
+    DTWLB_LAUNCH_CHECK();
+    return DTWLB_OK;
+}
 
 int launch_paa_sums(const float *x, int64_t count, int n, float *lo, float *hi, cudaStream_t st) {
     if (count == 0) return DTWLB_OK;
@@ -473,17 +549,12 @@ int launch_paa_bound(const float *Uhi, const float *Llo, const float *Xlo, const
     return launch_tile<true>(Uhi, Llo, Xlo, Xhi, Q, N, paa_pitch(n), p, rooted, out, ldo, st);
 }
 
-int launch_paa_bound_rev(const float *Ylo, const float *Yhi, const float *Uxhi, const float *Lxlo, int64_t Q,
-                         int64_t N, int n, int p, bool rooted, void *out, int64_t ldo, cudaStream_t st) {
-    return launch_tile<true, true>(Ylo, Yhi, Uxhi, Lxlo, Q, N, paa_pitch(n), p, rooted, out, ldo, st);
-}
-
-int launch_paa_bound_sym(const float *Uhi, const float *Llo, const float *Ylo, const float *Yhi, const float *Xlo,
-                         const float *Xhi, const float *Uxhi, const float *Lxlo, int64_t Q, int64_t N, int n, int p,
+int launch_paa_bound_sym(const float *Qm, const float *Qr, const float *Ym, const float *Yr, const float *Xm,
+                         const float *Xr, const float *Bm, const float *Br, int64_t Q, int64_t N, int n, int p,
                          bool rooted, void *out, int64_t ldo, cudaStream_t st) {
     if (Q == 0 || N == 0) return DTWLB_OK;
     const int Dp = paa_pitch(n);  // a multiple of 4: 16-byte rows
-#define DTWLB_S(P_, R_) return launch_sym_t<P_, true, R_>(Uhi, Llo, Ylo, Yhi, Xlo, Xhi, Uxhi, Lxlo, Q, N, Dp, out, ldo, st)
+#define DTWLB_S(P_, R_) return launch_sym_t<P_, true, R_>(Qm, Qr, Ym, Yr, Xm, Xr, Bm, Br, Q, N, Dp, out, ldo, st)
     if (p == 1) { if (rooted) DTWLB_S(1, true); else DTWLB_S(1, false); }
     else { if (rooted) DTWLB_S(2, true); else DTWLB_S(2, false); }
 #undef DTWLB_S

@@ -35,15 +35,17 @@ int launch_paa_env_sums(const float *U, const float *L, int64_t count, int n, fl
 // else __half out rounded down (nn_search's gate block).
 int launch_paa_bound(const float *Uhi, const float *Llo, const float *Xlo, const float *Xhi, int64_t Q,
                      int64_t N, int n, int p, bool rooted, void *out, int64_t ldo, cudaStream_t st);
-// Reverse piecewise-sum bound (reading c20): out[q][c] = max(out[q][c],
-// sum_j d(P(y_q)_j, [P(L(x_c))_j, P(U(x_c))_j])^p * (p == 2 ? 1/s : 1)), directed rounding.
-// Ylo/Yhi: query sums [Q][Dp] (launch_paa_sums of the queries); Uxhi/Llo: candidate
-// envelope sums [N][Dp] (launch_paa_env_sums of U(x), L(x)).  Same out types as above.
-int launch_paa_bound_rev(const float *Ylo, const float *Yhi, const float *Uxhi, const float *Lxlo, int64_t Q,
-                         int64_t N, int n, int p, bool rooted, void *out, int64_t ldo, cudaStream_t st);
-// Both terms in one pass: out[q][c] = max(forward, reverse) (same rounding as the two launches above).
-int launch_paa_bound_sym(const float *Uhi, const float *Llo, const float *Ylo, const float *Yhi, const float *Xlo,
-                         const float *Xhi, const float *Uxhi, const float *Lxlo, int64_t Q, int64_t N, int n, int p,
+// Midpoint-radius segment sums [count][Dp] (the fused gate's operands, outward-rounded):
+// box = false: point sums of the rows lo_src (= hi_src); box = true: the boxes [P(L), P(U)] of
+// envelopes lo_src = L, hi_src = U (padding segments: radius FLT_MAX).
+int launch_paa_mid(const float *lo_src, const float *hi_src, int64_t count, int n, float *m, float *r, bool box,
+                   cudaStream_t st);
+// Both terms in one pass: out[q][c] = max(forward, reverse) over midpoint-radius operands
+// (launch_paa_mid): Qm/Qr the query envelope boxes, Ym/Yr the query sums [Q][Dp]; Xm/Xr the
+// candidate sums, Bm/Br the candidate envelope boxes [N][Dp].  Directed rounding: never above
+// the exact max of the two piecewise-sum bounds (readings c18, c20).
+int launch_paa_bound_sym(const float *Qm, const float *Qr, const float *Ym, const float *Yr, const float *Xm,
+                         const float *Xr, const float *Bm, const float *Br, int64_t Q, int64_t N, int n, int p,
                          bool rooted, void *out, int64_t ldo, cudaStream_t st);
 
 // LB_Keogh^p of Q <= kStreamMaxQ queries against every database row in ONE streaming pass

@@ -592,8 +592,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     // A host database with the pre-filter (the e2e path): it is copied in chunks on a side stream
     // and the database-side setup and the first block's gate run chunk by chunk as the chunks
     // land, so the host->device copy hides behind the gate (bench e2e); else one copy up front
-    static const bool gate_split = [] { const char *e = getenv("DTWLB_GATE_SPLIT"); return e && atoi(e); }();
-    const bool chunked = db_host && prefilter && !(opts && opts->db_env) && !gate_split &&
+    const bool chunked = db_host && prefilter && !(opts && opts->db_env) &&
                          ws().get_copy_stream() != nullptr;
     if (db_host && !chunked)
         DTWLB_CUDA(cudaMemcpyAsync(const_cast<float *>(db), db_host, sizeof(float) * N * n, cudaMemcpyHostToDevice, st));
@@ -629,14 +628,15 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
             DTWLB_LAUNCH_CHECK();
         }
     }
-    // piecewise sums: database [2][N][Dp] (lo, hi), query envelope [2][Q][Dp] (Uhi, Llo)
+    // piecewise sums in midpoint-radius form (the fused gate's operands, launch_paa_mid):
+    // database sums [2][N][Dp] (m, r), query envelope boxes [2][Q][Dp] (m, r)
     const int Dp = paa_pitch(n);
     float *xpaa = nullptr, *qpaa = nullptr;
     if (prefilter) {
         DTWLB_TRY(wsget(S_PAA, (size_t)2 * N * Dp, &xpaa));
         DTWLB_TRY(wsget(S_QPAA, (size_t)2 * Q * Dp, &qpaa));
-        if (!chunked) DTWLB_TRY(launch_paa_sums(db, N, n, xpaa, xpaa + (size_t)N * Dp, st));
-        DTWLB_TRY(launch_paa_env_sums(U, L, Q, n, qpaa, qpaa + (size_t)Q * Dp, st));
+        if (!chunked) DTWLB_TRY(launch_paa_mid(db, db, N, n, xpaa, xpaa + (size_t)N * Dp, false, st));
+        DTWLB_TRY(launch_paa_mid(L, U, Q, n, qpaa, qpaa + (size_t)Q * Dp, true, st));
     }
     const bool generic_dtw = w > 64;
     // row+column cascade of the w <= 32 DTW kernel (reading c21; C(i) = i + col_c0).  Off by
@@ -668,15 +668,15 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         if (!chunked) DTWLB_TRY(launch_envelope(db, n, w, e, e + (size_t)N * n, N, st));
         dbenv = e;
     }
-    // symmetric gate (reading c20): reverse piecewise sums P(U(x)) up, P(L(x)) down [2][N][Dp]
-    // and P(y) down / up [2][Q][Dp]
+    // symmetric gate (reading c20): the candidate envelope boxes [P(L(x)), P(U(x))] [2][N][Dp] and
+    // the query sums P(y) [2][Q][Dp], midpoint-radius form
     float *rpaa = nullptr;
     if (prefilter) {
         DTWLB_TRY(wsget(S_RPAA, (size_t)2 * N * Dp + (size_t)2 * Q * Dp, &rpaa));
         if (!chunked)
-            DTWLB_TRY(launch_paa_env_sums(dbenv, dbenv + (size_t)N * n, N, n, rpaa, rpaa + (size_t)N * Dp, st));
+            DTWLB_TRY(launch_paa_mid(dbenv + (size_t)N * n, dbenv, N, n, rpaa, rpaa + (size_t)N * Dp, true, st));
         float *yp = rpaa + (size_t)2 * N * Dp;
-        DTWLB_TRY(launch_paa_sums(queries, Q, n, yp, yp + (size_t)Q * Dp, st));
+        DTWLB_TRY(launch_paa_mid(queries, queries, Q, n, yp, yp + (size_t)Q * Dp, false, st));
     }
     tm.mark();  // 1
 
@@ -828,10 +828,11 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
             DTWLB_CUDA(cudaEventRecord(e_c, cs));
             DTWLB_CUDA(cudaStreamWaitEvent(st, e_c, 0));
             cudaEventDestroy(e_c);
-            DTWLB_TRY(launch_paa_sums(db + r0 * n, cnt, n, xpaa + r0 * Dp, xpaa + (size_t)N * Dp + r0 * Dp, st));
+            DTWLB_TRY(launch_paa_mid(db + r0 * n, db + r0 * n, cnt, n, xpaa + r0 * Dp, xpaa + (size_t)N * Dp + r0 * Dp,
+                                     false, st));
             DTWLB_TRY(launch_envelope(db + r0 * n, n, w, ex + r0 * n, ex + (size_t)N * n + r0 * n, cnt, st));
-            DTWLB_TRY(launch_paa_env_sums(ex + r0 * n, ex + (size_t)N * n + r0 * n, cnt, n, rpaa + r0 * Dp,
-                                          rpaa + (size_t)N * Dp + r0 * Dp, st));
+            DTWLB_TRY(launch_paa_mid(ex + (size_t)N * n + r0 * n, ex + r0 * n, cnt, n, rpaa + r0 * Dp,
+                                     rpaa + (size_t)N * Dp + r0 * Dp, true, st));
             const cudaEvent_t g0 = stats ? rec() : nullptr;
             DTWLB_TRY(launch_paa_bound_sym(qpaa, qpaa + (size_t)Q * Dp, yp, yp + (size_t)Q * Dp, xpaa + r0 * Dp,
                                            xpaa + (size_t)N * Dp + r0 * Dp, rpaa + r0 * Dp,
@@ -853,15 +854,10 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
         if (stats) ev0 = rec();
         if (prefilter) {
             // symmetric gate: max of the forward and the reverse piecewise-sum bounds (readings c18,
-            // c20), one fused tile pass (DTWLB_GATE_SPLIT=1: two launches, the second max-combining)
+            // c20), one fused tile pass
             const float *yp = rpaa + (size_t)2 * N * Dp;
             if (qb0 == 0 && qn == gate0_qn) {
                 // (computed chunk by chunk with the database copy, above)
-            } else if (gate_split) {
-                DTWLB_TRY(launch_paa_bound(qpaa + qb0 * Dp, qpaa + (size_t)Q * Dp + qb0 * Dp, xpaa,
-                                           xpaa + (size_t)N * Dp, qn, N, n, p, false, beta1, ldb, st));
-                DTWLB_TRY(launch_paa_bound_rev(yp + qb0 * Dp, yp + (size_t)Q * Dp + qb0 * Dp, rpaa,
-                                               rpaa + (size_t)N * Dp, qn, N, n, p, false, beta1, ldb, st));
             } else {
                 DTWLB_TRY(launch_paa_bound_sym(qpaa + qb0 * Dp, qpaa + (size_t)Q * Dp + qb0 * Dp, yp + qb0 * Dp,
                                                yp + (size_t)Q * Dp + qb0 * Dp, xpaa, xpaa + (size_t)N * Dp, rpaa,

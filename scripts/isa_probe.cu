@@ -50,6 +50,12 @@ __global__ void probe(float *out, float s0, float s1, long long *cycles) {
                 const float d0 = fmaxf(fmaxf(u.x, l.x), 0.f), d1 = fmaxf(fmaxf(u.y, l.y), 0.f);
                 p[j].x = __fmaf_rd(d1, d1, __fmaf_rd(d0, d0, p[j].x));
             }
+            if constexpr (OP == 12) {  // midpoint-form gate element: FADD.RZ, FADD.RM |.|, FADD |.|, FFMA.RM
+                const float t1 = __fsub_rz(a[j], b[j]);
+                const float t2 = __fsub_rd(fabsf(t1), s1);
+                const float t3 = t2 + fabsf(t2);
+                b[j] = __fmaf_rd(t3, t3, b[j]);
+            }
             if constexpr (OP == 8) {  // DTW cell: FADD, FMNMX3, FFMA
                 float t = s0 - b[j];
                 a[j] = fmaf(t, t, fminf(fminf(a[j], b[(j + 1) & 7]), a[(j + 7) & 7]));
@@ -117,5 +123,6 @@ int main() {
     run<9>("FMNMX (max/min swap, 2 ops)", 16, 16);
     run<11>("gate element pair (FADD2 x2, FMNMX3 x2, FFMA x2) [elements]", 48, 16);
     run<10>("LB_Improved element (6 ops) [elements]", 48, 8);
+    run<12>("midpoint gate element (FADD.RZ, FADD.RM, FADD, FFMA.RM) [elements]", 32, 8);
     return 0;
 }
