@@ -54,7 +54,7 @@ __device__ __forceinline__ unsigned long long wband_cells(int r, int n, int w) {
 //      true : column coordinates (cell e of lane t = column tS + e), w >= n - 1 only.
 // yp: padded query rows [rows][LPW], yp[u] = y[u - padL] (+inf outside [0, n)).
 template <int S>
-constexpr int wide_min_blocks() { return S <= 16 ? 4 : (S <= 32 ? 3 : 2); }
+constexpr int wide_min_blocks() { return S <= 32 ? 4 : 2; }  // (S = 25: 128 registers, 16 warps per SM)
 // lanes t == 0 of every group of KW lanes
 template <int KW>
 __host__ __device__ constexpr unsigned group_leads() { return KW == 8 ? 0x01010101u : 0x11111111u; }
@@ -365,12 +365,19 @@ int launch_wide_t(const DtwArgs &a, const float *yp, int LPW, int padL, cudaStre
     int dev = 0, nsm = 148;
     DTWLB_CUDA(cudaGetDevice(&dev));
     DTWLB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    // enough warps to hold every pair of the round (32 / KW per warp), at most the resident
-    // CTAs x 4 warps per SM
+    // enough warps to hold every pair of the round (32 / KW per warp), at most the CTAs that are
+    // resident at once (register-limited: 4 per SM at S = 25, more than the launch bound's minimum)
+    auto kern = dtw_wide_kernel<KW, S, P, WALK, COL>;
+    static int resident = 0;
+    if (resident == 0) {
+        int nb = 0;
+        DTWLB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NTW, 0));
+        resident = std::max(nb, 1);
+    }
     const int64_t warps = std::min<int64_t>(ceil_div(std::max<int64_t>(a.total, 1), 32 / KW),
-                                            (int64_t)nsm * 4 * wide_min_blocks<S>());
+                                            (int64_t)nsm * (NTW / 32) * resident);
     const int64_t grid = ceil_div(warps * 32, NTW);
-    dtw_wide_kernel<KW, S, P, WALK, COL><<<(unsigned)grid, NTW, 0, st>>>(a, yp, LPW, padL);
+    kern<<<(unsigned)grid, NTW, 0, st>>>(a, yp, LPW, padL);
     DTWLB_LAUNCH_CHECK();
     return DTWLB_OK;
 }
