@@ -54,7 +54,7 @@ __device__ __forceinline__ unsigned long long wband_cells(int r, int n, int w) {
 //      true : column coordinates (cell e of lane t = column tS + e), w >= n - 1 only.
 // yp: padded query rows [rows][LPW], yp[u] = y[u - padL] (+inf outside [0, n)).
 template <int S>
-constexpr int wide_min_blocks() { return S <= 32 ? 4 : 2; }  // (S = 25: 128 registers, 16 warps per SM)
+constexpr int wide_min_blocks() { return S <= 25 ? 5 : (S <= 32 ? 4 : 2); }  // (S = 25: 128 registers, 16 warps per SM)
 // lanes t == 0 of every group of KW lanes
 template <int KW>
 __host__ __device__ constexpr unsigned group_leads() { return KW == 8 ? 0x01010101u : 0x11111111u; }
