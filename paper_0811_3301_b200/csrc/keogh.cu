@@ -285,7 +285,8 @@ int launch_tile(const float *U, const float *L, const float *db, const float *db
 // value never exceeds the exact one: t1 = m_x - m_b toward zero (|t1| <= |exact|), t2 = |t1| - R
 // rounded down, t3 = t2 + |t2| = 2 max(t2, 0) (exact), acc += t3^p rounded down; the total is
 // scaled by 2^-p (exact) -- the same bound as max(Xlo - Uhi, Llo - Xhi, 0), whose two terms are
-// (t1 sign-split) |m_x - m_b| - R.
+// (t1 sign-split) |m_x - m_b| - R.  The three subtractions of two elements issue as three packed
+// FADD2 (mid_elem2).
 struct SymStage {
     float X[TC][KP], X2[TC][KP];    // candidate segment sums: midpoint, radius            (forward)
     float XR[TC][KP], XR2[TC][KP];  // candidate envelope boxes [P(L(x)), P(U(x))]: m, r   (reverse)
@@ -293,13 +294,16 @@ struct SymStage {
     float UR[TQ][KP], LR[TQ][KP];   // query segment sums: midpoint, radius                (reverse)
 };
 
+// Two elements per step: the three subtractions as packed FADD2 (per component the same IEEE
+// operation, rounding mode and |.| / negation operand modifiers as FADD): 3 FADD2 + 2 FFMA = 5
+// issue slots per two elements instead of 8 (the FP32 pipe still does 4 ops per element).
 template <int P>
-__device__ __forceinline__ float mid_elem(float acc, float mx, float mb, float R) {
-    const float t1 = __fsub_rz(mx, mb);         // |t1| <= |mx - mb|
-    const float t2 = __fsub_rd(fabsf(t1), R);   // <= |mx - mb| - R
-    const float t3 = t2 + fabsf(t2);            // 2 max(t2, 0), exact
-    if constexpr (P == 1) return __fadd_rd(acc, t3);
-    else return __fmaf_rd(t3, t3, acc);
+__device__ __forceinline__ float mid_elem2(float acc, float2 mx, float2 mb, float2 R) {
+    const float2 t1 = __fadd2_rz(mx, make_float2(-mb.x, -mb.y));                      // |t1| <= |mx - mb|
+    const float2 t2 = __fadd2_rd(make_float2(fabsf(t1.x), fabsf(t1.y)), make_float2(-R.x, -R.y));  // <= |mx - mb| - R
+    const float2 t3 = __fadd2_rn(t2, make_float2(fabsf(t2.x), fabsf(t2.y)));           // 2 max(t2, 0), exact
+    if constexpr (P == 1) return __fadd_rd(__fadd_rd(acc, t3.x), t3.y);
+    else return __fmaf_rd(t3.y, t3.y, __fmaf_rd(t3.x, t3.x, acc));
 }
 
 template <int P, bool VEC, bool ROOTED>
@@ -375,10 +379,10 @@ gate_sym_kernel(const float *__restrict__ Qm, const float *__restrict__ Qr, cons
 #pragma unroll
                     for (int r = 0; r < 4; ++r) {
                         float t = acc[r][j];
-                        t = mid_elem<P>(t, xv.x, mv[r].x, rv[r].x);
-                        t = mid_elem<P>(t, xv.y, mv[r].y, rv[r].y);
-                        t = mid_elem<P>(t, xv.z, mv[r].z, rv[r].z);
-                        t = mid_elem<P>(t, xv.w, mv[r].w, rv[r].w);
+                        t = mid_elem2<P>(t, make_float2(xv.x, xv.y), make_float2(mv[r].x, mv[r].y),
+                                         make_float2(rv[r].x, rv[r].y));
+                        t = mid_elem2<P>(t, make_float2(xv.z, xv.w), make_float2(mv[r].z, mv[r].w),
+                                         make_float2(rv[r].z, rv[r].w));
                         acc[r][j] = t;
                     }
                 }
@@ -394,10 +398,10 @@ gate_sym_kernel(const float *__restrict__ Qm, const float *__restrict__ Qr, cons
 #pragma unroll
                     for (int r = 0; r < 4; ++r) {
                         float t = accr[r][j];
-                        t = mid_elem<P>(t, yv[r].x, bm.x, br.x);
-                        t = mid_elem<P>(t, yv[r].y, bm.y, br.y);
-                        t = mid_elem<P>(t, yv[r].z, bm.z, br.z);
-                        t = mid_elem<P>(t, yv[r].w, bm.w, br.w);
+                        t = mid_elem2<P>(t, make_float2(yv[r].x, yv[r].y), make_float2(bm.x, bm.y),
+                                         make_float2(br.x, br.y));
+                        t = mid_elem2<P>(t, make_float2(yv[r].z, yv[r].w), make_float2(bm.z, bm.w),
+                                         make_float2(br.z, br.w));
                         accr[r][j] = t;
                     }
                 }
