@@ -179,34 +179,59 @@ __global__ void __launch_bounds__(256) topk_merge_kernel(DtwArgs a) {
 constexpr int kChunk4 = 256;
 
 template <int WB, int P, bool EXACT>
-__device__ __forceinline__ void four_rows(float (&B)[2 * WB + 2], const float (&Y)[(2 * WB + 4 + 3) / 4 * 4],
+__device__ __forceinline__ void four_rows(float (&B)[2 * WB + 2], const float2 (&Y2)[(2 * WB + 4 + 3) / 4 * 2],
                                           const float (&x)[4], int w2) {
     constexpr int NB = 2 * WB + 1;
     // skew 2: at step d, row r computes band cell e = d - 2r.  Its up (row r-1, cell e+1)
     // and diagonal (row r-1, cell e) neighbours came out of row r-1 one and two steps
-    // earlier (h1, h2), its left neighbour is its own previous cell (pl); y index e + r.
+    // earlier (h1, h2), its left neighbour is its own previous cell (pl); y index e + r = d - r.
+    // The four rows of a step read the consecutive y[d - 3 .. d]; on odd steps (y[d-1], y[d]) and
+    // (y[d-3], y[d-2]) are register pairs of the window Y2[k] = (Y[2k], Y[2k+1]), so the differences
+    // of rows (1, 0) and (3, 2) issue as two packed FADD2 against the x pairs (x0, x1), (x2, x3)
+    // read swapped (same IEEE operation per component); even steps stay scalar (their pairs
+    // would need a misaligned (x2, x1)): 3 instead of 4 issue slots per four differences.
+    const float2 x01 = make_float2(x[0], x[1]), x23 = make_float2(x[2], x[3]);
     float pl0 = kInf, pl1 = kInf, pl2 = kInf, pl3 = kInf;
     float h1_0 = kInf, h2_0 = kInf, h1_1 = kInf, h2_1 = kInf, h1_2 = kInf, h2_2 = kInf;
 #pragma unroll
     for (int d = 0; d < NB + 6; ++d) {
+        const bool a0 = d < NB, a1 = d >= 2 && d - 2 < NB, a2 = d >= 4 && d - 4 < NB, a3 = d >= 6;
+        float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+        if (d & 1) {
+            if (a0 || a1) {  // (x0 - y[d], x1 - y[d-1])
+                const float2 v = Y2[(d - 1) / 2];
+                const float2 r = __fadd2_rn(x01, make_float2(-v.y, -v.x));
+                t0 = r.x; t1 = r.y;
+            }
+            if ((a2 || a3) && d >= 3) {  // (x2 - y[d-2], x3 - y[d-3])
+                const float2 v = Y2[(d - 3) / 2];
+                const float2 r = __fadd2_rn(x23, make_float2(-v.y, -v.x));
+                t2 = r.x; t3 = r.y;
+            }
+        } else {
+            if (a0) t0 = x[0] - Y2[d / 2].x;
+            if (a1) t1 = x[1] - Y2[(d - 2) / 2].y;
+            if (a2) t2 = x[2] - Y2[(d - 2) / 2].x;
+            if (a3) t3 = x[3] - Y2[(d - 4) / 2].y;
+        }
         float c0 = kInf, c1 = kInf, c2 = kInf;
-        if (d < NB) {  // row 0, cell d: up = B[d+1], diag = B[d]
-            c0 = cell<P>(min3f(B[d], B[d + 1], pl0), x[0] - Y[d]);
+        if (a0) {  // row 0, cell d: up = B[d+1], diag = B[d]
+            c0 = cell<P>(min3f(B[d], B[d + 1], pl0), t0);
             if (!EXACT && d > w2) c0 = kInf;
             pl0 = c0;
         }
-        if (d >= 2 && d - 2 < NB) {  // row 1, cell d-2
-            c1 = cell<P>(min3f(h2_0, h1_0, pl1), x[1] - Y[d - 1]);
+        if (a1) {  // row 1, cell d-2
+            c1 = cell<P>(min3f(h2_0, h1_0, pl1), t1);
             if (!EXACT && d - 2 > w2) c1 = kInf;
             pl1 = c1;
         }
-        if (d >= 4 && d - 4 < NB) {  // row 2, cell d-4
-            c2 = cell<P>(min3f(h2_1, h1_1, pl2), x[2] - Y[d - 2]);
+        if (a2) {  // row 2, cell d-4
+            c2 = cell<P>(min3f(h2_1, h1_1, pl2), t2);
             if (!EXACT && d - 4 > w2) c2 = kInf;
             pl2 = c2;
         }
-        if (d >= 6) {  // row 3, cell d-6 (stored: B becomes row i+3)
-            float c3 = cell<P>(min3f(h2_2, h1_2, pl3), x[3] - Y[d - 3]);
+        if (a3) {  // row 3, cell d-6 (stored: B becomes row i+3)
+            float c3 = cell<P>(min3f(h2_2, h1_2, pl3), t3);
             if (!EXACT && d - 6 > w2) c3 = kInf;
             pl3 = c3;
             B[d - 6] = c3;
@@ -318,7 +343,8 @@ dtw4_kernel(DtwArgs a) {
     const float *xr = nullptr, *yr = nullptr;
     float thr = kInf, thr_n = kInf, beta_n = 0.f;
     int i = 0;
-    float B[NB + 1], Y[YG ? 1 : NY];
+    float B[NB + 1];
+    float2 Y2[YG ? 1 : NY / 2];  // the y window as register pairs: Y2[k] = (Y[2k], Y[2k+1])
     float xv[8];  // x of rows i .. i+7 (staged in the slot one 8-row step ahead)
     // cascading abandon: rest = LB_Keogh^p terms of the rows not yet computed
     const bool casc = WALK && (a.b1 != nullptr || a.b1h != nullptr);
@@ -345,7 +371,8 @@ dtw4_kernel(DtwArgs a) {
 #pragma unroll
                         for (int d = 0; d < NY; d += 4) {
                             const float4 v = *reinterpret_cast<const float4 *>(slot + d);
-                            Y[d] = v.x; Y[d + 1] = v.y; Y[d + 2] = v.z; Y[d + 3] = v.w;
+                            Y2[d / 2] = make_float2(v.x, v.y);
+                            Y2[d / 2 + 1] = make_float2(v.z, v.w);
                         }
                     }
                     const float4 x0 = *reinterpret_cast<const float4 *>(slot + XA);
@@ -529,15 +556,16 @@ dtw4_kernel(DtwArgs a) {
 #pragma unroll
                     for (int t = 0; t < 4; ++t) xv[t] = xv[t + 4];
                 } else {
-                    four_rows<WB, P, EXACT>(B, Y, x4, w2);
+                    four_rows<WB, P, EXACT>(B, Y2, x4, w2);
                     i += 4;
 #pragma unroll
                     for (int t = 0; t < 4; ++t) xv[t] = xv[t + 4];
                     // shift the y window by four and append y[i + w + 1 .. i + w + 4] (next block)
 #pragma unroll
-                    for (int d = 0; d + 4 < NY; ++d) Y[d] = Y[d + 4];
+                    for (int k = 0; k + 2 < NY / 2; ++k) Y2[k] = Y2[k + 2];
                     const float4 v = __ldg(reinterpret_cast<const float4 *>(yr + (kYPadL - w - sh) + i + NY - 4));
-                    Y[NY - 4] = v.x; Y[NY - 3] = v.y; Y[NY - 2] = v.z; Y[NY - 1] = v.w;
+                    Y2[NY / 2 - 2] = make_float2(v.x, v.y);
+                    Y2[NY / 2 - 1] = make_float2(v.z, v.w);
                 }
             }
             if (i + 4 > n && i < n && i - i0 < 8) {  // tail rows (n % 4 != 0): one row at a time
@@ -545,7 +573,7 @@ dtw4_kernel(DtwArgs a) {
                     float prev = kInf;
 #pragma unroll
                     for (int d = 0; d < NB; ++d) {
-                        const float yd = YG ? ybase[(kYPadL - w) + i + d] : Y[YG ? 0 : d];
+                        const float yd = YG ? ybase[(kYPadL - w) + i + d] : ((d & 1) ? Y2[YG ? 0 : d >> 1].y : Y2[YG ? 0 : d >> 1].x);
                         float c = cell<P>(min3f(B[d], B[d + 1], prev), __ldg(xr + i) - yd);
                         if (!EXACT && d > w2) c = kInf;
                         B[d] = c;
@@ -554,8 +582,8 @@ dtw4_kernel(DtwArgs a) {
                     ++i;
                     if constexpr (!YG) {
 #pragma unroll
-                        for (int d = 0; d + 1 < NY; ++d) Y[d] = Y[d + 1];
-                        Y[NY - 1] = __ldg(yr + (kYPadL - w - sh) + i + NY - 1);
+                        for (int k = 0; k + 1 < NY / 2; ++k) Y2[k] = make_float2(Y2[k].y, Y2[k + 1].x);
+                        Y2[NY / 2 - 1] = make_float2(Y2[NY / 2 - 1].y, __ldg(yr + (kYPadL - w - sh) + i + NY - 1));
                     }
                 }
             }
