@@ -35,16 +35,6 @@ __device__ __forceinline__ float cell(float m, float t) {
     else return fmaf(t, t, m);
 }
 
-// LB_Keogh term of row i: d(x_i, [L(y)_i, U(y)_i])^p.  Every banded path visits row i
-// in some column j with |i-j| <= w, at cost |x_i - y_j|^p >= this term, so the sum of
-// the terms of the rows not yet computed bounds what the path still has to pay
-// (cascading abandon, reading c19).
-// +-beta1 of the pair (LB_Keogh^p; the survivor kernel stored -rd(beta1) as __half with the
-// pre-filter, the dense LB_Keogh pass +beta1 as float without it); callers take |.|
-__device__ __forceinline__ float b1_at(const DtwArgs &a, int64_t idx) {
-    return a.b1 ? __ldg(a.b1 + idx) : __half2float(a.b1h[idx]);
-}
-
 // In-band cells of rows 0 .. r-1 of the n x n table: sum_i (min(n-1, i+w) - max(0, i-w) + 1)
 // = r(2w+1) - (left clip) - (right clip); band_cells(n, n, w) = n(2w+1) - w(w+1).  (w <= n-1)
 __device__ __forceinline__ unsigned long long band_cells(int r, int n, int w) {
@@ -61,6 +51,10 @@ __device__ __forceinline__ float col_lb(float y, float ux, float lx, float lu, f
     return P == 1 ? d : d * d;
 }
 
+// LB_Keogh term of row i: d(x_i, [L(y)_i, U(y)_i])^p.  Every banded path visits row i in some
+// column j with |i-j| <= w, at cost |x_i - y_j|^p >= this term, so the sum of the terms of the
+// rows not yet computed bounds what the path still has to pay (cascading abandon, DESIGN.md
+// reading c19); the pair's total (+-beta1) comes from the gate slot the survivor kernel wrote.
 template <int P>
 __device__ __forceinline__ float row_lb(float x, float u, float l) {
     const float d = max3f(x - u, l - x, 0.f);
@@ -76,19 +70,6 @@ __device__ __forceinline__ void stage_rows8(float *dst, const float *r, int i0, 
     } else {
 #pragma unroll
         for (int t = 0; t < 8; ++t) cp_async4(dst + t, i0 + t < n ? r + i0 + t : r, i0 + t < n ? 4 : 0);
-    }
-}
-
-// 8 values v[i0 .. i0+7] of a row of length n (fill beyond n); vector loads when aligned
-__device__ __forceinline__ void load8(float (&v)[8], const float *__restrict__ r, int i0, int n, float fill) {
-    if (((n & 3) == 0) && i0 + 8 <= n) {
-        const float4 a = __ldg(reinterpret_cast<const float4 *>(r + i0));
-        const float4 b = __ldg(reinterpret_cast<const float4 *>(r + i0 + 4));
-        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-        v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-    } else {
-#pragma unroll
-        for (int t = 0; t < 8; ++t) v[t] = i0 + t < n ? __ldg(r + i0 + t) : fill;
     }
 }
 
