@@ -129,7 +129,7 @@ typedef struct nn_opts {
     int32_t flags;         /* DTWLB_KEOGH_ONLY: skip the LB_Improved pass (Alg. 2);
                               DTWLB_NO_PREFILTER: LB_Keogh over every pair (Alg. 3
                               literally) instead of the piecewise-sum pre-filter;
-                              DTWLB_NO_CASCADE, DTWLB_NO_STREAM: see below          */
+                              DTWLB_NO_CASCADE, DTWLB_NO_STREAM, DTWLB_NO_ABANDON: see below */
     /* Database-sharded search: called once per query block after the
      * first (best-first) range, with thr = DEVICE pointer to the block's count
      * thresholds tau_q^p (1+eps) (+inf until k results), stream-ordered on `stream`.
@@ -169,6 +169,8 @@ typedef struct nn_opts {
 #define DTWLB_NO_PREFILTER 2
 #define DTWLB_NO_CASCADE 4   /* DTW abandons on the row minimum alone (no LB_Keogh suffix) */
 #define DTWLB_NO_STREAM 8    /* Q <= 8: use the tiled bound pass instead of the streaming one */
+#define DTWLB_NO_ABANDON 16  /* no early abandon inside DTW: every pair the bounds pass runs to its last row
+                                (the pruning by LB_Keogh / LB_Improved before DTW is unchanged); same k-NN */
 
 /* Counters of one nn_search call (host struct, filled on return). */
 typedef struct nn_stats {

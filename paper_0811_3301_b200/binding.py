@@ -20,6 +20,7 @@ KEOGH_ONLY = 1
 NO_PREFILTER = 2
 NO_CASCADE = 4
 NO_STREAM = 8
+NO_ABANDON = 16
 MAX_K = 1024
 
 
@@ -197,7 +198,7 @@ def dtw_band(x: torch.Tensor, y: torch.Tensor, w: int, p: int) -> torch.Tensor:
 
 
 def _opts(eps, index_base, query_block, keogh_only, prefilter=True, cascade=True, exchange=None, stream=True,
-          db_env=None, shards=0, exchange_walk=0, nccl_comm=None):
+          db_env=None, shards=0, exchange_walk=0, nccl_comm=None, abandon=True):
     o = NnOpts()
     o.nccl_comm = nccl_comm.handle if isinstance(nccl_comm, Communicator) else nccl_comm
     o.shards = shards
@@ -208,7 +209,7 @@ def _opts(eps, index_base, query_block, keogh_only, prefilter=True, cascade=True
     o.index_base = index_base
     o.query_block = query_block
     o.flags = (KEOGH_ONLY if keogh_only else 0) | (0 if prefilter else NO_PREFILTER) | \
-        (0 if cascade else NO_CASCADE) | (0 if stream else NO_STREAM)
+        (0 if cascade else NO_CASCADE) | (0 if stream else NO_STREAM) | (0 if abandon else NO_ABANDON)
     o.db_env = db_env.data_ptr() if db_env is not None else None
     return o
 
@@ -216,7 +217,7 @@ def _opts(eps, index_base, query_block, keogh_only, prefilter=True, cascade=True
 def nn_search(queries, db, w: int, p: int, k: int, *, eps: float = 1e-3, index_base: int = 0,
               query_block: int = 0, keogh_only: bool = False, prefilter: bool = True, cascade: bool = True,
               stream: bool = True, db_env=None, exchange=None, out=None, shards: int = 0,
-              exchange_walk: int = 0, nccl_comm=None, return_stats: bool = False):
+              exchange_walk: int = 0, nccl_comm=None, abandon: bool = True, return_stats: bool = False):
     """Exact k-NN under banded DTW_p.  Returns (idx int64 [Q][k], dist float32 [Q][k]).
 
     queries/db may be CUDA tensors (device path) or host tensors / numpy arrays
@@ -233,6 +234,8 @@ def nn_search(queries, db, w: int, p: int, k: int, *, eps: float = 1e-3, index_b
     inside the last range's DTW walk (after its rounds 2, 4, 6): a block then makes
     1 + exchange_walk calls on every shard.  ``nccl_comm`` (a ``Communicator``) makes the library
     itself min-reduce the thresholds at those points with NCCL, instead of ``exchange``.
+    ``abandon=False`` (DTWLB_NO_ABANDON) runs every DTW the bounds pass to its last row (no early
+    abandon inside DTW; same k-NN).
     """
     host = not (isinstance(queries, torch.Tensor) and queries.is_cuda)
     if host:
@@ -256,7 +259,7 @@ def nn_search(queries, db, w: int, p: int, k: int, *, eps: float = 1e-3, index_b
         if tuple(db_env.shape) != (2, N, n):
             raise ValueError(f"db_env must be [2][N][n] = [2][{N}][{n}], got {tuple(db_env.shape)}")
     o = _opts(eps, index_base, query_block, keogh_only, prefilter, cascade, cb, stream, db_env, shards,
-              exchange_walk, nccl_comm)
+              exchange_walk, nccl_comm, abandon)
     st = NnStats()
     _check(load().nn_search(queries.data_ptr(), Q, db.data_ptr(), N, n, w, p, k, idx.data_ptr(),
                             dist.data_ptr(), ctypes.byref(o), ctypes.byref(st) if return_stats else None,

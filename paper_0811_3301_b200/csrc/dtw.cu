@@ -605,7 +605,7 @@ dtw4_kernel(DtwArgs a) {
                 else a.res[item] = rootp<P>(r);
                 st = kFree;
             } else {
-                if (band_min<WB>(B) + rest > thr) {
+                if (!a.no_abandon && band_min<WB>(B) + rest > thr) {
                     if constexpr (!WALK) a.res[item] = kInf;
                     cells_done += band_cells(i, n, w);
                     ++n_abandon;  // early abandon (readings c15, c19, c21)
@@ -679,7 +679,7 @@ __global__ void dtw_generic_kernel(DtwArgs a, const float *__restrict__ yraw, fl
             prev = v;
             rmin = fminf(rmin, v);
         }
-        if (rmin > thr) {
+        if (!a.no_abandon && rmin > thr) {
             if constexpr (!WALK) a.res[item] = kInf;
             if (a.cells) atomicAdd(a.cells, band_cells(i + 1, n, w));
             if (a.abandoned) atomicAdd(a.abandoned, 1ull);

@@ -316,7 +316,7 @@ dtw_wide_kernel(DtwArgs a, const float *__restrict__ yp, int LPW, int padL) {
                     if (casc) m += fmaxf(__shfl_sync(FULL, rest_snap, lane & ~(KW - 1)), 0.f);
                     if (busy && ph >= KW + 6) {
                         thr = fminf(thr, *reinterpret_cast<volatile float *>(a.thr + qy));
-                        if (m > thr) {
+                        if (!a.no_abandon && m > thr) {
                             if (t == 0) {
                                 ++n_abandon;
                                 n_cells += wband_cells(ph - KW + 2, n, w);  // rows 0 .. ph-KW+1 done

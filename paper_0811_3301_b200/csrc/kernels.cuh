@@ -151,6 +151,8 @@ struct DtwArgs {
     // caught up).  yq, LUq, ULq: [Qb][n] y, U(L(y)), L(U(y)); Uxdb, Lxdb: [N][n] U(x), L(x).
     int col_c0;
     const float *yq, *LUq, *ULq, *Uxdb, *Lxdb;
+    // WALK: no early abandon (nn_opts DTWLB_NO_ABANDON): every started pair runs to its last row
+    bool no_abandon;
     // WALK: completed pairs are merged into the query's top-k (keys (DTW^p bits << 32 | c),
     // ascending, [Qb][k]) under a per-query lock, and thr[q] follows the k-th key
     unsigned long long *topk;

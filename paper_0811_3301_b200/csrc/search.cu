@@ -565,6 +565,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     }
     // DTW early abandon on rowmin + LB_Keogh terms of the remaining rows (reading c19)
     const bool cascade = !(opts && (opts->flags & DTWLB_NO_CASCADE));
+    const bool no_abandon = opts && (opts->flags & DTWLB_NO_ABANDON);
     w = std::min(w, n - 1);
     Timer tm(stats != nullptr, st);
     tm.mark();  // 0
@@ -1011,6 +1012,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                         if (tot2[0] == 0) { walking = false; break; }
                     }
                     DtwArgs da{};
+                    da.no_abandon = no_abandon;
                     da.ysh = ysh;
                     da.ysh_stride_s = (int64_t)Q * LP;
                     da.LP = LP;

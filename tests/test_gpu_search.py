@@ -139,6 +139,25 @@ def test_cascade_and_prefilter_switches(cuda_ok, name):
     assert st["dtw_evaluated"] <= st["improved_evaluated"] <= st["keogh_evaluated"] <= 24 * 6000
 
 
+@pytest.mark.parametrize("name,w", [("C2p2", None), ("C2p1", None), ("C2p2", 100)])
+def test_no_abandon_same_knn(cuda_ok, name, w):
+    """DTWLB_NO_ABANDON: without early abandoning every DTW the bounds pass runs to
+    its last row -- the k-NN is bit-identical (abandoning only skips pairs that cannot enter the
+    top-k, reading c15), no pair is abandoned, and every started pair's cells are all computed.
+    Covers the register-band kernel and (w = 100) the four-lanes-per-pair wide kernel."""
+    from paper_0811_3301_b200 import nn_search
+    c = datagen.CONFIGS[name]
+    qs, db = datagen.make(c, Q=16, N=3000)
+    w = c.w if w is None else w
+    g_idx, g_dist = check(qs, db, w, c.p, 3, brute=False)
+    i2, d2, st = nn_search(dev(qs), dev(db), w, c.p, 3, abandon=False, return_stats=True)
+    assert np.array_equal(i2.cpu().numpy(), g_idx) and np.array_equal(d2.cpu().numpy(), g_dist)
+    assert st["dtw_abandoned"] == 0
+    assert st["dtw_cells_computed"] == st["dtw_cells_nominal"] > 0
+    _, _, st1 = nn_search(dev(qs), dev(db), w, c.p, 3, return_stats=True)
+    assert st1["dtw_cells_computed"] < st["dtw_cells_computed"]
+
+
 def test_threshold_exchange_callback(cuda_ok):
     """The sharded path's exchange hook (a7): called once per query block after the first
     range with a CUDA view of the block's thresholds; lowering them to any value >= the
