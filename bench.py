@@ -406,8 +406,12 @@ def run_ours(args, cfg):
                                                   "entry through the SM's 128 B/clk data path",
                                           }
         if dtw_kernel_ms > 0:
+            # w > 64: the four-lanes-per-pair kernel where it has an instantiation (csrc/dtw_wide.cu
+            # wide_plan: band segments of 51 cells, w in {100, 101}; or unconstrained with n <= 256)
+            wide = cfg.w > 64 and ((2 * cfg.w + 1 + 3) // 4 == 51 or (cfg.w >= cfg.n - 1 and cfg.n <= 256))
             kern["dtw_kernel"] = {"kernel": "dtw4_kernel (banded DTW walk)" if cfg.w <= 64 else
-                                  "dtw_generic_kernel (banded DTW walk, w > 64)",
+                                  ("dtw_wide_kernel (banded DTW walk, four lanes per pair)" if wide else
+                                   "dtw_generic_kernel (banded DTW walk, w > 64)"),
                                   "bound": "alu", "ms": dtw_kernel_ms, "work": 3.0 * cells_cmp / 1e12,
                                   "unit": "Tlane-op/s", "peak": peak,
                                   "note": "3 slots per in-band DTW cell actually computed (kernel counter, early "

@@ -998,11 +998,14 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                     static const int env_d0 = [] { const char *e = getenv("DTWLB_D0"); return e ? atoi(e) : 0; }();
                     // batch per query and round: kD0 << (round * gs).  The first round stays small (its
                     // pairs run with tau = +inf: none is abandoned, and every completed pair is merged
-                    // into the query's top-k under its lock); with few queries a round is
-                    // latency-bound (one pair's DTW is a ~n-step chain), so later batches grow 8x per
-                    // round instead of 2x (fewer, fuller rounds)
+                    // into the query's top-k under its lock); later batches grow 8x per round: a round
+                    // costs its launches, its merge and the tail of its longest pair (a ~n-step
+                    // chain), so fewer, fuller rounds win although tau tightens less often between
+                    // them (measured, DESIGN.md a3: C5 267.8 -> 265.5 ms, C4 43.0 -> 41.7, C3 w = 100
+                    // 56.6 -> 47.3; 2x growth was the default for more than 64 queries before)
                     const int d0 = env_d0 > 0 ? env_d0 : kD0;
-                    const int gs = qn <= 64 ? 3 : 1;
+                    static const int env_gs = [] { const char *e = getenv("DTWLB_WALK_GS"); return e ? atoi(e) : 0; }();
+                    const int gs = env_gs > 0 ? env_gs : 3;
                     plan_kernel<<<1, 1024, 0, st>>>(s, (int)qn, list, rcap, loff_r, sorted, d0, gs);
                     DTWLB_LAUNCH_CHECK();
                     int tot2[2] = {0, 0};
