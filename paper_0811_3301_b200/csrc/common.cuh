@@ -91,6 +91,23 @@ __device__ __forceinline__ unsigned long long pack_key(float d, uint32_t idx) {
     return (static_cast<unsigned long long>(__float_as_uint(d)) << 32) | idx;
 }
 
+// Candidate-list keys (survivor kernel -> sort -> DTW walk) carry, in the low kKeyPosBits bits
+// of their bound word, the key's append position within its sort run (runs are kRun =
+// 2^kKeyPosBits keys), so the walk can find the pair's abandon schedule after the sort.  The
+// bound is the word with those bits cleared: a truncation of a non-negative float, so never
+// above the exact bound (reading c22).
+constexpr int kKeyPosBits = 12;
+constexpr uint32_t kKeyPosMask = (1u << kKeyPosBits) - 1u;
+__device__ __forceinline__ unsigned long long pack_list_key(float d, uint32_t idx, int pos) {
+    d = fmaxf(d, 0.0f);
+    const uint32_t hi = (__float_as_uint(d) & ~kKeyPosMask) | ((uint32_t)pos & kKeyPosMask);
+    return (static_cast<unsigned long long>(hi) << 32) | idx;
+}
+__device__ __forceinline__ float key_bound(unsigned long long key) {
+    return __uint_as_float((uint32_t)(key >> 32) & ~kKeyPosMask);
+}
+__device__ __forceinline__ int key_pos(unsigned long long key) { return (int)((uint32_t)(key >> 32) & kKeyPosMask); }
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Start of query q's key list: exact-count lists (per-query offsets) or fixed capacity.

@@ -276,8 +276,9 @@ struct Dtw4Cfg {
     // the refill for rows 0..7, then one step ahead); [SL - 2, SL) the pair's (q, c)
     static constexpr int XA = NY + 4 > 40 ? NY + 4 : 40;  // (YG: the gate word sits at [0])
     static constexpr int SL = XA + 28;
+    // per warp chunk: keys, schedule indices (reading c22), queries
     static constexpr size_t smem = (size_t)NT * SL * sizeof(float) +
-                                   (size_t)(NT / 32) * kChunk4 * (sizeof(unsigned long long) + sizeof(int));
+                                   (size_t)(NT / 32) * kChunk4 * (2 * sizeof(unsigned long long) + sizeof(int));
 };
 
 // Lane states of dtw4_kernel
@@ -297,14 +298,15 @@ dtw4_kernel(DtwArgs a) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     float *slot = dsm + (size_t)threadIdx.x * SL;  // this lane's staging slot
     unsigned long long *ckey = reinterpret_cast<unsigned long long *>(dsm + (size_t)NT * SL) + wid * kChunk4;
+    long long *crec = reinterpret_cast<long long *>(dsm + (size_t)NT * SL) + (NT / 32) * kChunk4 + wid * kChunk4;
     int *cq = reinterpret_cast<int *>(reinterpret_cast<unsigned long long *>(dsm + (size_t)NT * SL) +
-                                      (NT / 32) * kChunk4) + wid * kChunk4;
+                                      2 * (NT / 32) * kChunk4) + wid * kChunk4;
     const int n = a.n, w = EXACT ? WB : a.w, w2 = 2 * w;
     const int sh = (kYPadL - w) & 3;  // alignment class of (i - w) for i % 4 == 0
     // YG, WALK: the padded row of the query of the warp's current chunk staged in shared
     // memory (lanes on that query read their y values there, others from global/L1)
     float *wrow = reinterpret_cast<float *>(reinterpret_cast<int *>(reinterpret_cast<unsigned long long *>(
-                      dsm + (size_t)NT * SL) + (NT / 32) * kChunk4) + (NT / 32) * kChunk4) + (size_t)wid * a.LP;
+                      dsm + (size_t)NT * SL) + 2 * (NT / 32) * kChunk4) + (NT / 32) * kChunk4) + (size_t)wid * a.LP;
     int staged_q = -1;
     bool ysm = false;           // this lane's y row is the staged one
     const float *ybase = nullptr;  // YG: start of this lane's padded y row (shared or global)
@@ -329,6 +331,11 @@ dtw4_kernel(DtwArgs a) {
     float xv[8];  // x of rows i .. i+7 (staged in the slot one 8-row step ahead)
     // cascading abandon: rest = LB_Keogh^p terms of the rows not yet computed
     const bool casc = WALK && (a.b1 != nullptr || a.b1h != nullptr);
+    // column schedule (reading c22, with the row cascade): the pair's 32 fp16 words written by
+    // the survivor kernel, copied into the slot's [0, 16) (the y window / gate word, free once
+    // the lane is active) at activation: word 0 joins rest at the first test, word k is
+    // subtracted at the test after 8k rows
+    const bool recm = casc && a.rec != nullptr;
     // row+column cascade (reading c21): the gate word holds rest0 = LB_Improved^p minus the
     // column terms of [0, col_c0) (rest0_kernel); each step subtracts its rows' LB_Keogh terms
     // and the column terms of [C(i0), C(i0 + 8)), C(i) = i + col_c0
@@ -370,6 +377,11 @@ dtw4_kernel(DtwArgs a) {
                         rest_n = a.b1 ? __uint_as_float(wv) : __half2float(__ushort_as_half(hb));
                     }
                     rest = fabsf(rest_n);
+                    if (recm) {
+                        const __half *rp = a.rec + crec[item - cbeg] * 32;
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) cp_async16(slot + 4 * m, rp + 8 * m, 16);
+                    }
                     st = kActive;
                     ++n_started;
                 }
@@ -411,7 +423,10 @@ dtw4_kernel(DtwArgs a) {
                             const int64_t j = a.pos[q] + (it - a.item_off[q]);
                             DCHECK(j >= 0 && (a.loff ? a.loff[q] + j < a.loff[q + 1] : j < a.cap), "dtw4 item %lld q=%d j=%lld",
                                    (long long)it, q, (long long)j);
-                            ckey[lane + 32 * t] = a.list[list_base(a.loff, a.cap, q) + j];
+                            const int64_t lb = list_base(a.loff, a.cap, q);
+                            const unsigned long long key = a.list[lb + j];
+                            ckey[lane + 32 * t] = key;
+                            if (recm) crec[lane + 32 * t] = __ldg(a.rec_off + q) + (j & ~(int64_t)kKeyPosMask) + key_pos(key);
                             cq[lane + 32 * t] = q;
                         }
                     }
@@ -433,7 +448,7 @@ dtw4_kernel(DtwArgs a) {
                     reinterpret_cast<int *>(slot)[SL - 2] = (int)qy;
                     reinterpret_cast<uint32_t *>(slot)[SL - 1] = (uint32_t)c;
                     DCHECK(c < a.Ndb, "dtw4 key c=%lld q=%lld", (long long)c, (long long)qy);
-                    beta_n = __uint_as_float((uint32_t)(key >> 32));
+                    beta_n = key_bound(key);
                     thr_n = *reinterpret_cast<volatile float *>(a.thr + qy);
                     if (casc) {
                         // +-beta1: the 4-byte word holding it -> slot[NY]
@@ -605,6 +620,11 @@ dtw4_kernel(DtwArgs a) {
                 else a.res[item] = rootp<P>(r);
                 st = kFree;
             } else {
+                if (recm) {  // (n % 4 == 0: i = i0 + 8 here)
+                    const __half *hs = reinterpret_cast<const __half *>(slot);
+                    if (i == 8) rest += __half2float(hs[0]);
+                    rest -= __half2float(hs[i >> 3]);
+                }
                 if (!a.no_abandon && band_min<WB>(B) + rest > thr) {
                     if constexpr (!WALK) a.res[item] = kInf;
                     cells_done += band_cells(i, n, w);
@@ -655,7 +675,7 @@ __global__ void dtw_generic_kernel(DtwArgs a, const float *__restrict__ yraw, fl
         const int64_t j = a.pos[lo] + (item - a.item_off[lo]);
         const unsigned long long key = a.list[list_base(a.loff, a.cap, lo) + j];
         cand = (uint32_t)(key & 0xffffffffu);
-        const float beta = __uint_as_float((uint32_t)(key >> 32));
+        const float beta = key_bound(key);
         thr = *reinterpret_cast<volatile float *>(a.thr + lo);
         if (beta > thr) return;
         if (a.started) atomicAdd(a.started, 1ull);

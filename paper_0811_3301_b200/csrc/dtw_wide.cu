@@ -132,7 +132,7 @@ dtw_wide_kernel(DtwArgs a, const float *__restrict__ yp, int LPW, int padL) {
                         const int64_t j = a.pos[qy] + (item - a.item_off[qy]);
                         const unsigned long long key = a.list[list_base(a.loff, a.cap, qy) + j];
                         cand = (uint32_t)(key & 0xffffffffu);
-                        beta = __uint_as_float((uint32_t)(key >> 32));
+                        beta = key_bound(key);
                         thr = *reinterpret_cast<volatile float *>(a.thr + qy);
                         xr = a.db + (int64_t)cand * n;
                         yr = yp + (int64_t)qy * LPW;

@@ -408,21 +408,90 @@ __device__ __forceinline__ void read_group(const int *lst, int g, int (&li)[8]) 
 }
 
 // Append the keys of the lanes with `pass` (one lane per survivor) to query q's list.
-__device__ __forceinline__ void append_keys(const ImprovedArgs &a, int64_t q, bool pass, float beta, int64_t c,
-                                            int lane) {
+// Returns the key's list position on the passing lanes (-1 elsewhere).
+__device__ __forceinline__ int append_keys(const ImprovedArgs &a, int64_t q, bool pass, float beta, int64_t c,
+                                           int lane) {
     const unsigned bal = __ballot_sync(0xffffffffu, pass);
-    if (!bal) return;
+    if (!bal) return -1;
     int base = 0;
     if (lane == 0) base = atomicAdd(a.list_len + q, __popc(bal));
     base = __shfl_sync(0xffffffffu, base, 0);
+    int pos = -1;
     if (pass) {
-        const int pos = base + __popc(bal & ((1u << lane) - 1));
+        pos = base + __popc(bal & ((1u << lane) - 1));
         DCHECK(a.loff ? a.loff[q] + pos < a.loff[q + 1] : pos < a.cap, "list append q=%lld pos=%d", (long long)q, pos);
-        a.list[list_base(a.loff, a.cap, q) + pos] = pack_key(beta, (uint32_t)c);
+        a.list[list_base(a.loff, a.cap, q) + pos] = pack_list_key(beta, (uint32_t)c, pos);
     }
+    return pos;
 }
 
-template <int P, int EPL, bool B1X, bool KO, bool DENSE>
+// Column part of the DTW walk's abandon schedule for one appended pair (DESIGN.md reading
+// c22), written to dst[0..32) as fp16: dst[0] = rd(sum_{c >= 4 c0b} beta2_c) and, for
+// k = 0..30, dst[1 + k] = ru(E[k]), E[k] = sum_{c in [8k, 8k + 8) + 4 c0b} beta2_c, with
+// beta2_c = d(y_c, [L(H)_c, U(H)_c])^p (the closed form above) and 4 c0b >= w.  The walk adds
+// dst[0] to its row cascade (+-beta1 minus the computed rows' LB_Keogh terms) at its first
+// test and subtracts E[k] after rows 8k .. 8k+7: after 8(k+1) rows the column part is <= the
+// sum over columns >= 8(k+1) + w, which every completion visits (no computed row reaches
+// them), and each of its cells (r, c) costs at least the row term of r plus the column term
+// of c (Theorem 1's split), so rowmin + rest bounds DTW^p.  cb0 / cb1: this lane's
+// column terms of the 4-sample blocks lane and lane + 32 (phase 2's per-block partials).
+template <int NV>
+__device__ __forceinline__ void write_col_schedule(float cb0, float cb1, int c0b, __half *dst, int lane) {
+    float h = (lane >= c0b ? cb0 : 0.f) + (NV == 2 && lane + 32 >= c0b ? cb1 : 0.f);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    // pairs of blocks (m, m + 1) at lane m, then lane l >= 1 fetches the pair at 2(l-1) + c0b
+    const int nx = (lane + 1) & 31;
+    const float n0 = __shfl_sync(0xffffffffu, cb0, nx);
+    const float n1 = NV == 2 ? __shfl_sync(0xffffffffu, cb1, nx) : 0.f;
+    const float pc0 = cb0 + (lane == 31 ? n1 : n0);
+    const float pc1 = cb1 + (lane == 31 ? 0.f : n1);
+    const int bc = 2 * lane - 2 + c0b;
+    const float e0 = __shfl_sync(0xffffffffu, pc0, bc & 31);
+    float e;
+    if constexpr (NV == 2) {
+        const float e1 = __shfl_sync(0xffffffffu, pc1, bc & 31);
+        e = bc < 32 ? e0 : (bc < 64 ? e1 : 0.f);
+    } else {
+        e = bc < 32 ? e0 : 0.f;
+    }
+    dst[lane] = lane == 0 ? __float2half_rd(h) : __float2half_ru(e);
+}
+
+// p2_group keeping this lane's per-block partials: c0[u] / c1[u] = the column terms of
+// survivor u over the lane's blocks lane / lane + 32 (REC, NV <= 2)
+template <int W, int P, int NV, int NPAD>
+__device__ __forceinline__ float p2_group_keep(const float *sU, const float *sL, const int (&li)[8],
+                                               const float4 (&yq)[NV], const float4 (&luq)[NV],
+                                               const float4 (&ulq)[NV], float (&c0)[4], float (&c1)[4],
+                                               int lane) {
+    static_assert(W <= 4 && NV <= 2, "REC groups are at most 4 wide");
+    float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        const float4 y = yq[v], lu = luq[v], ul = ulq[v];
+#pragma unroll
+        for (int u = 0; u < W; ++u) {
+            const int off = li[u] * NPAD + 4 * lane + 128 * v;
+            const float4 ux = *reinterpret_cast<const float4 *>(sU + off);
+            const float4 lx = *reinterpret_cast<const float4 *>(sL + off);
+            float t = 0.f;
+            t = accp<P>(t, max3f(y.x - fmaxf(ux.x, lu.x), fminf(lx.x, ul.x) - y.x, 0.f));
+            t = accp<P>(t, max3f(y.y - fmaxf(ux.y, lu.y), fminf(lx.y, ul.y) - y.y, 0.f));
+            t = accp<P>(t, max3f(y.z - fmaxf(ux.z, lu.z), fminf(lx.z, ul.z) - y.z, 0.f));
+            t = accp<P>(t, max3f(y.w - fmaxf(ux.w, lu.w), fminf(lx.w, ul.w) - y.w, 0.f));
+            if (v == 0) c0[u] = t; else c1[u] = t;
+            s[u] += t;
+        }
+    }
+    if constexpr (NV == 1) {
+#pragma unroll
+        for (int u = 0; u < W; ++u) c1[u] = 0.f;
+    }
+    return reduceW<W>(s, lane);
+}
+
+template <int P, int EPL, bool B1X, bool KO, bool DENSE, bool REC>
 __global__ void __launch_bounds__(ImpCfg<EPL, B1X>::NT, 1)
 improved_kernel(ImprovedArgs a, int Ct) {
     constexpr int NT = ImpCfg<EPL, B1X>::NT;
@@ -674,12 +743,20 @@ improved_kernel(ImprovedArgs a, int Ct) {
         } else if constexpr (!KO) {
             if (!PREFETCH && n2) load_p2<EPL, B1X, KO>(cur, a, q, lane);
             evals2 += n2;
+            // abandon schedules (reading c22): the appended pairs' (local row, list position)
+            // go to lst1 / b1w (free after phase 1), then one warp pass per pair
+            static_assert(!REC || (B1X && !DENSE && NV <= 2), "abandon schedules: pre-filtered LIST mode, n <= 256");
+            __half *rq = nullptr;  // (REC) this query's schedules
+            if constexpr (REC) rq = a.rec + __ldg(a.rec_off + q) * 32;
             auto phase2 = [&](auto wc, int g) {
                 constexpr int W = decltype(wc)::value;
                 constexpr int SH = W == 8 ? 2 : (W == 4 ? 3 : (W == 2 ? 4 : 5));
                 int li[8];
                 read_group<W>(lst2, g, li);
-                const float b2 = p2_group<W, P, NV, NPAD>(sU, sL, li, cur.y, cur.lu, cur.ul, lane);
+                float kc0[4], kc1[4];  // (REC) per-block column partials of the group
+                float b2;
+                if constexpr (REC) b2 = p2_group_keep<W, P, NV, NPAD>(sU, sL, li, cur.y, cur.lu, cur.ul, kc0, kc1, lane);
+                else b2 = p2_group<W, P, NV, NPAD>(sU, sL, li, cur.y, cur.lu, cur.ul, lane);
                 const int us = lane >> SH;
                 const int myl = W == 1 ? li[0] : lst2[g + us];
                 float b1;
@@ -696,11 +773,31 @@ improved_kernel(ImprovedArgs a, int Ct) {
                 if constexpr (DENSE) {
                     if (lead) a.dense[q * a.ldd + c0 + myl] = rootp<P>(beta);
                 } else {
-                    append_keys(a, q, lead && beta <= cur.thr, beta, c0 + myl, lane);
+                    const bool pass = lead && beta <= cur.thr;
+                    const int pos = append_keys(a, q, pass, beta, c0 + myl, lane);
+                    if constexpr (REC) {
+                        // the passing survivors' schedules, one warp pass each, from the
+                        // partials every lane still holds
+                        unsigned bal = __ballot_sync(0xffffffffu, pass);
+                        while (bal) {
+                            const int src = __ffs(bal) - 1;
+                            bal &= bal - 1;
+                            const int u = src >> SH;
+                            const int ps = __shfl_sync(0xffffffffu, pos, src);
+                            float v0 = kc0[0], v1 = kc1[0];
+#pragma unroll
+                            for (int t = 1; t < W; ++t)
+                                if (u == t) { v0 = kc0[t]; v1 = kc1[t]; }
+                            write_col_schedule<NV>(v0, v1, a.rec_c0b, rq + (int64_t)ps * 32, lane);
+                        }
+                    } else {
+                        (void)pos;
+                    }
                 }
             };
             int g = 0;
-            for (; n2 - g >= 7; g += 8) phase2(std::integral_constant<int, 8>{}, g);
+            if constexpr (!REC)
+                for (; n2 - g >= 7; g += 8) phase2(std::integral_constant<int, 8>{}, g);
             for (; n2 - g >= 3; g += 4) phase2(std::integral_constant<int, 4>{}, g);
             if (n2 - g == 2) phase2(std::integral_constant<int, 2>{}, g);
             else if (n2 - g == 1) phase2(std::integral_constant<int, 1>{}, g);
@@ -754,7 +851,10 @@ int launch_imp_t(const ImprovedArgs &a, int64_t ntiles, cudaStream_t st) {
     // staged rows: at most 64 candidates and 192 KB (3 arrays) / 128 KB (2 arrays)
     const int Ct = std::min(64, 16384 / NPAD);
     const size_t smem = (size_t)arrays * Ct * NPAD * sizeof(float) + (size_t)(NT / 32) * 296 * sizeof(int);
-    auto k = improved_kernel<P, EPL, B1X, KO, DENSE>;
+    auto k = improved_kernel<P, EPL, B1X, KO, DENSE, false>;
+    if constexpr (B1X && !KO && !DENSE && EPL <= 8) {
+        if (a.rec) k = improved_kernel<P, EPL, B1X, KO, DENSE, true>;  // + abandon schedules (c22)
+    }
     DTWLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t grid = ntiles * (64 / Ct);
     k<<<(unsigned)grid, NT, smem, st>>>(a, Ct);

@@ -82,7 +82,14 @@ struct ImprovedArgs {
     int64_t cap;
     const int64_t *loff;           // [Qb + 1] per-query list offsets (exact-count lists), or NULL
     int *list_len;                 // [Qb]
-    int *q_count;                  // [Qb] select: gate survivors of the range per query (or NULL)
+    // LIST mode with xdb, n <= 256 (reading c22): if set, the key query q appends at position
+    // j of its list gets the column part of its DTW abandon schedule at rec[32 (rec_off[q] + j)
+    // ..) (32 fp16: the column suffix from 4 rec_c0b rounded down, then 31 sums of 8 columns
+    // rounded up; rec_off: per-query offsets of capacity >= the list's); rec_c0b = ceil(w / 4)
+    __half *rec;
+    const int64_t *rec_off;
+    int rec_c0b;
+    int *q_count;                 // [Qb] select: gate survivors of the range per query (or NULL)
     // DENSE mode output
     float *dense;                  // [Qb][ldd], rooted
     int64_t ldd;
@@ -151,6 +158,12 @@ struct DtwArgs {
     // caught up).  yq, LUq, ULq: [Qb][n] y, U(L(y)), L(U(y)); Uxdb, Lxdb: [N][n] U(x), L(x).
     int col_c0;
     const float *yq, *LUq, *ULq, *Uxdb, *Lxdb;
+    // WALK, dtw4_kernel with the row cascade (b1h), n % 4 == 0 (reading c22): if set, the
+    // column schedules the survivor kernel wrote (ImprovedArgs::rec / rec_off); the key at
+    // sorted list position j of query q was appended at position (j & ~kKeyPosMask) +
+    // key_pos(key) (runs of 2^kKeyPosBits keys are sorted in place).  Exclusive with col_c0
+    const __half *rec;
+    const int64_t *rec_off;
     // WALK: no early abandon (nn_opts DTWLB_NO_ABANDON): every started pair runs to its last row
     bool no_abandon;
     // WALK: completed pairs are merged into the query's top-k (keys (DTW^p bits << 32 | c),

@@ -113,7 +113,7 @@ std::mutex &ws_mutex() {
 
 enum Slot {
     S_QSTAGE, S_DBSTAGE, S_ENV, S_QPAD, S_YSH, S_DBENV, S_BETA1, S_LIST, S_RES, S_STATE, S_TOPK,
-    S_OUTSTAGE, S_SCRATCH, S_TMP, S_MASK, S_PAA, S_QPAA, S_RPAA, S_SNAP, S_COUNT
+    S_OUTSTAGE, S_SCRATCH, S_TMP, S_MASK, S_PAA, S_QPAA, S_RPAA, S_SNAP, S_COUNT, S_REC
 };
 
 template <typename T>
@@ -189,6 +189,7 @@ __global__ void __launch_bounds__(512) sample_threshold_kernel(const T *__restri
 // 32-bit bound bits with the candidate index as payload; 512 threads x 8 keys = one run.
 // Non-negative float bits order like the floats; equal bounds keep their list order.
 constexpr int kRun = 4096;
+static_assert(kRun == 1 << kKeyPosBits, "list keys carry their position within a sort run");
 constexpr int kSortThreads = 512, kSortItems = kRun / kSortThreads;
 // Runs of the range's lists, built on the device (no host round trip): run t = (query,
 // index) with t over sum_q ceil(len_q / kRun); the count goes to *nruns.  One CTA.
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(256) rest0_kernel(const unsigned long long *__
         if (j < m) {
             const unsigned long long key = lq[j];
             c = (uint32_t)(key & 0xffffffffu);
-            beta = __uint_as_float((uint32_t)(key >> 32));
+            beta = key_bound(key);
             if (mine) {
                 const float4 ux = __ldg(reinterpret_cast<const float4 *>(Ux + (int64_t)c * n + 4 * src));
                 const float4 lx = __ldg(reinterpret_cast<const float4 *>(Lx + (int64_t)c * n + 4 * src));
@@ -448,7 +449,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(QState s, int Qb, const unsi
                 s.rnd[q] += 1;
                 const float thr = *reinterpret_cast<volatile float *>(s.thr + q);
                 const unsigned long long *lq = list + list_base(loff, cap, q);
-                while (pos < len && __uint_as_float((uint32_t)(lq[pos] >> 32)) > thr)
+                while (pos < len && key_bound(lq[pos]) > thr)
                     pos = (pos / kRun + 1) * kRun;
             }
             s.pos[q] = pos;
@@ -646,6 +647,12 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
     static const bool env_col = [] { const char *e = getenv("DTWLB_COLCASC"); return e && atoi(e); }();
     const int col_c0 =
         (prefilter && !keogh_only && cascade && env_col && w <= 32 && n % 4 == 0) ? (w + 3) / 4 * 4 : 0;
+    // abandon schedules (reading c22): the survivor kernel writes each appended pair's
+    // precomputed row + column suffix bounds, the w <= 64 walk kernel abandons on them (no
+    // per-step envelope gathers).  DTWLB_NO_SCHEDULE=1 keeps the row-only cascade (b1h)
+    static const bool env_nosched = [] { const char *e = getenv("DTWLB_NO_SCHEDULE"); return e && atoi(e); }();
+    const bool sched = prefilter && !keogh_only && cascade && !env_nosched && !generic_dtw && col_c0 == 0 &&
+                       n % 4 == 0 && n <= 256 && (p == 1 || p == 2);
     const int LP = dtw_padded_len(n);
     float *ysh = nullptr;
     if (!generic_dtw) {
@@ -721,6 +728,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
 
     float *beta1;
     unsigned long long *list = nullptr;  // the range's exact-count key lists (pool, S_LIST)
+    __half *srec = nullptr;              // the range's abandon schedules (S_REC), or NULL
     {   // float, or __half with the pre-filter
         void *g = nullptr;
         DTWLB_TRY(ws().get(S_BETA1, (size_t)Qb * ldb * gate_elem, &g));
@@ -953,10 +961,33 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 ia.list = list;
                 ia.cap = rcap;
                 ia.loff = loff_r;
+                // schedules at the exact per-query offsets s.loff (gate survivors), whatever the
+                // key lists' layout
+                srec = nullptr;
+                if (sched && wsget(S_REC, (size_t)std::max<int64_t>(total, 1) * 32, &srec) != DTWLB_OK) {
+                    cudaGetLastError();  // no room: this range keeps the row-only cascade
+                    srec = nullptr;
+                }
+                ia.rec = srec;
+                ia.rec_off = s.loff;
+                static const bool env_rowonly = [] { const char *e = getenv("DTWLB_SCHED_ROWONLY"); return e && atoi(e); }();
+                ia.rec_c0b = env_rowonly ? 64 : (w + 3) / 4;  // (64: no column terms -- measurement)
                 DTWLB_TRY(launch_survivor(ia, p, keogh_only, false, st));
             }
             // ---- a3: sort each query's list in runs (run list built on the device) ----
             if (stats) span(ev_s0, ev_s1, &ms_survivor);
+            {
+                static const bool dbg_keys = [] { const char *e = getenv("DTWLB_DEBUG_ROUNDS"); return e && atoi(e); }();
+                if (stats && dbg_keys) {  // (debug: the range's appended keys; syncs)
+                    std::vector<int> lens((size_t)qn);
+                    DTWLB_CUDA(cudaMemcpyAsync(lens.data(), s.len, sizeof(int) * qn, cudaMemcpyDeviceToHost, st));
+                    DTWLB_CUDA(cudaStreamSynchronize(st));
+                    long long sum = 0;
+                    for (int v : lens) sum += v;
+                    fprintf(stderr, "[dtwlb] range %d: %lld keys appended, schedules %s\n", macro, sum,
+                            srec ? "on" : "off");
+                }
+            }
             static const bool nosort2 = [] { const char *e = getenv("DTWLB_NOSORT2"); return e && atoi(e); }();
             const bool sorted = !(nosort2 && macro > 0);
             if (sorted || col_c0 > 0) {
@@ -1047,6 +1078,8 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                     da.abandoned = s.stat + 3;
                     da.started = s.stat + 1;
                     da.queue = reinterpret_cast<unsigned *>(s.counters + 4);
+                    da.rec = srec;  // (the schedules of this range's keys, or NULL)
+                    da.rec_off = s.loff;
                     if (cascade) {  // cascading abandon with the pair's LB_Keogh row terms
                         if (prefilter) da.b1h = reinterpret_cast<const __half *>(beta1);
                         else da.b1 = beta1;
