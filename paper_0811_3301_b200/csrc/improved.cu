@@ -435,38 +435,17 @@ __device__ __forceinline__ int append_keys(const ImprovedArgs &a, int64_t q, boo
 // them), and each of its cells (r, c) costs at least the row term of r plus the column term
 // of c (Theorem 1's split), so rowmin + rest bounds DTW^p.  cb0 / cb1: this lane's
 // column terms of the 4-sample blocks lane and lane + 32 (phase 2's per-block partials).
-template <int NV>
-__device__ __forceinline__ void write_col_schedule(float cb0, float cb1, int c0b, __half *dst, int lane) {
-    float h = (lane >= c0b ? cb0 : 0.f) + (NV == 2 && lane + 32 >= c0b ? cb1 : 0.f);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
-    // pairs of blocks (m, m + 1) at lane m, then lane l >= 1 fetches the pair at 2(l-1) + c0b
-    const int nx = (lane + 1) & 31;
-    const float n0 = __shfl_sync(0xffffffffu, cb0, nx);
-    const float n1 = NV == 2 ? __shfl_sync(0xffffffffu, cb1, nx) : 0.f;
-    const float pc0 = cb0 + (lane == 31 ? n1 : n0);
-    const float pc1 = cb1 + (lane == 31 ? 0.f : n1);
-    const int bc = 2 * lane - 2 + c0b;
-    const float e0 = __shfl_sync(0xffffffffu, pc0, bc & 31);
-    float e;
-    if constexpr (NV == 2) {
-        const float e1 = __shfl_sync(0xffffffffu, pc1, bc & 31);
-        e = bc < 32 ? e0 : (bc < 64 ? e1 : 0.f);
-    } else {
-        e = bc < 32 ? e0 : 0.f;
-    }
-    dst[lane] = lane == 0 ? __float2half_rd(h) : __float2half_ru(e);
-}
-
 // p2_group keeping this lane's per-block partials: c0[u] / c1[u] = the column terms of
-// survivor u over the lane's blocks lane / lane + 32 (REC, NV <= 2)
+// survivor u over the lane's blocks lane / lane + 32 (REC, NV <= 2); hd: like the return value
+// (lane l: survivor l >> (5 - log2 W)) but over the head blocks [0, c0b) only
 template <int W, int P, int NV, int NPAD>
 __device__ __forceinline__ float p2_group_keep(const float *sU, const float *sL, const int (&li)[8],
                                                const float4 (&yq)[NV], const float4 (&luq)[NV],
                                                const float4 (&ulq)[NV], float (&c0)[4], float (&c1)[4],
-                                               int lane) {
+                                               int c0b, float &hd, int lane) {
     static_assert(W <= 4 && NV <= 2, "REC groups are at most 4 wide");
     float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float h[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
         const float4 y = yq[v], lu = luq[v], ul = ulq[v];
@@ -480,7 +459,7 @@ __device__ __forceinline__ float p2_group_keep(const float *sU, const float *sL,
             t = accp<P>(t, max3f(y.y - fmaxf(ux.y, lu.y), fminf(lx.y, ul.y) - y.y, 0.f));
             t = accp<P>(t, max3f(y.z - fmaxf(ux.z, lu.z), fminf(lx.z, ul.z) - y.z, 0.f));
             t = accp<P>(t, max3f(y.w - fmaxf(ux.w, lu.w), fminf(lx.w, ul.w) - y.w, 0.f));
-            if (v == 0) c0[u] = t; else c1[u] = t;
+            if (v == 0) { c0[u] = t; h[u] = lane < c0b ? t : 0.f; } else { c1[u] = t; }
             s[u] += t;
         }
     }
@@ -488,7 +467,31 @@ __device__ __forceinline__ float p2_group_keep(const float *sU, const float *sL,
 #pragma unroll
         for (int u = 0; u < W; ++u) c1[u] = 0.f;
     }
+    hd = reduceW<W>(h, lane);
     return reduceW<W>(s, lane);
+}
+
+// Column part of the DTW walk's abandon schedule for one appended pair (DESIGN.md reading
+// c22), written to dst[0..32) as fp16: dst[0] = h0 = rd(sum_{c >= 4 c0b} beta2_c) and, for
+// k = 0..30, dst[1 + k] = ru(E[k]), E[k] = sum_{c in [8k, 8k + 8) + 4 c0b} beta2_c, with
+// beta2_c = d(y_c, [L(H)_c, U(H)_c])^p (the closed form above) and 4 c0b >= w.  The walk adds
+// dst[0] to its row cascade (+-beta1 minus the computed rows' LB_Keogh terms) at its first
+// test and subtracts E[k] after rows 8k .. 8k+7: after 8(k+1) rows the column part is <= the
+// sum over columns >= 8(k+1) + w, which every completion visits (no computed row reaches
+// them), and each of its cells (r, c) costs at least the row term of r plus the column term
+// of c (Theorem 1's split), so rowmin + rest bounds DTW^p.  pc0 / pc1: this lane's
+// pair sums of the 4-sample blocks (b, b + 1), b = lane + 32 v; block b starts word
+// 1 + (b - c0b) / 2 when b - c0b is even; the words past the last block are 0.
+template <int NV>
+__device__ __forceinline__ void write_col_schedule(float pc0, float pc1, float h0, int c0b, __half *dst, int lane) {
+    const int d0 = lane - c0b;
+    if (d0 >= 0 && !(d0 & 1)) dst[1 + (d0 >> 1)] = __float2half_ru(pc0);
+    if constexpr (NV == 2) {
+        const int d1 = d0 + 32;
+        if (!(d1 & 1) && d1 <= 60) dst[1 + (d1 >> 1)] = __float2half_ru(pc1);
+    }
+    if (lane >= 1 && 2 * (lane - 1) + c0b >= 32 * NV) dst[lane] = __float2half_rz(0.f);
+    if (lane == 0) dst[0] = __float2half_rd(h0);
 }
 
 template <int P, int EPL, bool B1X, bool KO, bool DENSE, bool REC>
@@ -753,10 +756,12 @@ improved_kernel(ImprovedArgs a, int Ct) {
                 constexpr int SH = W == 8 ? 2 : (W == 4 ? 3 : (W == 2 ? 4 : 5));
                 int li[8];
                 read_group<W>(lst2, g, li);
-                float kc0[4], kc1[4];  // (REC) per-block column partials of the group
+                float kc0[4], kc1[4], hd = 0.f;  // (REC) per-block column partials, head sums
                 float b2;
-                if constexpr (REC) b2 = p2_group_keep<W, P, NV, NPAD>(sU, sL, li, cur.y, cur.lu, cur.ul, kc0, kc1, lane);
-                else b2 = p2_group<W, P, NV, NPAD>(sU, sL, li, cur.y, cur.lu, cur.ul, lane);
+                if constexpr (REC)
+                    b2 = p2_group_keep<W, P, NV, NPAD>(sU, sL, li, cur.y, cur.lu, cur.ul, kc0, kc1, a.rec_c0b, hd, lane);
+                else
+                    b2 = p2_group<W, P, NV, NPAD>(sU, sL, li, cur.y, cur.lu, cur.ul, lane);
                 const int us = lane >> SH;
                 const int myl = W == 1 ? li[0] : lst2[g + us];
                 float b1;
@@ -779,16 +784,29 @@ improved_kernel(ImprovedArgs a, int Ct) {
                         // the passing survivors' schedules, one warp pass each, from the
                         // partials every lane still holds
                         unsigned bal = __ballot_sync(0xffffffffu, pass);
-                        while (bal) {
-                            const int src = __ffs(bal) - 1;
-                            bal &= bal - 1;
-                            const int u = src >> SH;
-                            const int ps = __shfl_sync(0xffffffffu, pos, src);
-                            float v0 = kc0[0], v1 = kc1[0];
+                        if (bal) {
+                            // pair sums of adjacent blocks for the whole group (independent shuffles)
+                            const int nx = (lane + 1) & 31;
 #pragma unroll
-                            for (int t = 1; t < W; ++t)
-                                if (u == t) { v0 = kc0[t]; v1 = kc1[t]; }
-                            write_col_schedule<NV>(v0, v1, a.rec_c0b, rq + (int64_t)ps * 32, lane);
+                            for (int t = 0; t < W; ++t) {
+                                const float n0 = __shfl_sync(0xffffffffu, kc0[t], nx);
+                                const float n1 = NV == 2 ? __shfl_sync(0xffffffffu, kc1[t], nx) : 0.f;
+                                kc0[t] += lane == 31 ? n1 : n0;
+                                kc1[t] += lane == 31 ? 0.f : n1;
+                            }
+                            const float h0 = b2 - hd;  // (lead lanes: their survivor's column suffix)
+                            do {
+                                const int src = __ffs(bal) - 1;
+                                bal &= bal - 1;
+                                const int u = src >> SH;
+                                const int ps = __shfl_sync(0xffffffffu, pos, src);
+                                const float hu = __shfl_sync(0xffffffffu, h0, src);
+                                float v0 = kc0[0], v1 = kc1[0];
+#pragma unroll
+                                for (int t = 1; t < W; ++t)
+                                    if (u == t) { v0 = kc0[t]; v1 = kc1[t]; }
+                                write_col_schedule<NV>(v0, v1, hu, a.rec_c0b, rq + (int64_t)ps * 32, lane);
+                            } while (bal);
                         }
                     } else {
                         (void)pos;

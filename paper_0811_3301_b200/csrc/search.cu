@@ -970,8 +970,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 }
                 ia.rec = srec;
                 ia.rec_off = s.loff;
-                static const bool env_rowonly = [] { const char *e = getenv("DTWLB_SCHED_ROWONLY"); return e && atoi(e); }();
-                ia.rec_c0b = env_rowonly ? 64 : (w + 3) / 4;  // (64: no column terms -- measurement)
+                ia.rec_c0b = (w + 3) / 4;  // (w <= 64: <= 16)
                 DTWLB_TRY(launch_survivor(ia, p, keogh_only, false, st));
             }
             // ---- a3: sort each query's list in runs (run list built on the device) ----
