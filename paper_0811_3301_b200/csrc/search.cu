@@ -964,7 +964,7 @@ int nn_search_impl(const float *queries_in, int64_t Q, const float *db_in, int64
                 // schedules at the exact per-query offsets s.loff (gate survivors), whatever the
                 // key lists' layout
                 srec = nullptr;
-                if (sched && wsget(S_REC, (size_t)std::max<int64_t>(total, 1) * 32, &srec) != DTWLB_OK) {
+                if (sched && total < (1LL << 31) && wsget(S_REC, (size_t)std::max<int64_t>(total, 1) * 32, &srec) != DTWLB_OK) {
                     cudaGetLastError();  // no room: this range keeps the row-only cascade
                     srec = nullptr;
                 }
