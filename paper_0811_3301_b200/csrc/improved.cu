@@ -784,12 +784,15 @@ improved_kernel(ImprovedArgs a, int Ct) {
                     if (lead) a.dense[q * a.ldd + c0 + myl] = rootp<P>(beta);
                 } else {
                     const bool pass = lead && beta <= cur.thr;
-                    const int pos = append_keys(a, q, pass, beta, c0 + myl, lane);
                     if constexpr (REC) {
-                        // the passing survivors' schedules, one warp pass each, from the
-                        // partials every lane still holds
+                        // append_keys inlined: the pair-sum shuffles (independent of the list
+                        // position) issue between the atomic and the first use of its result, and
+                        // the list base reuses the schedule offset when both are the exact-count
+                        // offsets (no second dependent load)
                         unsigned bal = __ballot_sync(0xffffffffu, pass);
                         if (bal) {
+                            int base = 0;
+                            if (lane == 0) base = atomicAdd(a.list_len + q, __popc(bal));
                             // pair sums of adjacent blocks for the whole group (independent shuffles)
                             const int nx = (lane + 1) & 31;
 #pragma unroll
@@ -800,6 +803,16 @@ improved_kernel(ImprovedArgs a, int Ct) {
                                 kc1[t] += lane == 31 ? 0.f : n1;
                             }
                             const float h0 = b2 - hd;  // (lead lanes: their survivor's column suffix)
+                            base = __shfl_sync(0xffffffffu, base, 0);
+                            int pos = -1;
+                            if (pass) {
+                                pos = base + __popc(bal & lt);
+                                const int64_t lb = a.loff == a.rec_off ? (int64_t)roff_c : list_base(a.loff, a.cap, q);
+                                DCHECK(a.loff ? a.loff[q] + pos < a.loff[q + 1] : pos < a.cap, "list append q=%lld pos=%d", (long long)q, pos);
+                                a.list[lb + pos] = pack_list_key(beta, (uint32_t)(c0 + myl), pos);
+                            }
+                            // the passing survivors' schedules, one warp pass each, from the
+                            // partials every lane still holds
                             do {
                                 const int src = __ffs(bal) - 1;
                                 bal &= bal - 1;
@@ -814,7 +827,7 @@ improved_kernel(ImprovedArgs a, int Ct) {
                             } while (bal);
                         }
                     } else {
-                        (void)pos;
+                        append_keys(a, q, pass, beta, c0 + myl, lane);
                     }
                 }
             };
