@@ -494,6 +494,12 @@ __device__ __forceinline__ void write_col_schedule(float pc0, float pc1, float h
     if (lane == 0) dst[0] = __float2half_rd(h0);
 }
 
+// the look-ahead entry's 64-bit survivor mask as two words, loaded by volatile asm straight into the
+// loop-carried registers (a C++ load went to a scratch pair and was moved into place at once)
+__device__ __forceinline__ void ld_mask2(const unsigned *p, unsigned &lo, unsigned &hi) {
+    asm volatile("ld.global.v2.u32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "l"(p));
+}
+
 template <int P, int EPL, bool B1X, bool KO, bool DENSE, bool REC>
 __global__ void __launch_bounds__(ImpCfg<EPL, B1X>::NT, 1)
 improved_kernel(ImprovedArgs a, int Ct) {
@@ -607,10 +613,15 @@ improved_kernel(ImprovedArgs a, int Ct) {
     // ahead, so the next entry's query-row loads do not wait on its index load
     constexpr bool IDX_AHEAD = ONE_CTA;
     int q_ah = 0;
-    unsigned long long m_ah = 0;
-    if (IDX_AHEAD && e + NW < cnt) { q_ah = eq[e + NW]; m_ah = em[e + NW]; }
+    unsigned m_ah_lo = 0, m_ah_hi = 0;  // (two 32-bit words: see below)
+    // (the mask as two 32-bit words at a clamped index: as one 64-bit value the compiler loaded it into
+    // a scratch pair and moved it into place at once -- a full L2 wait per entry, 9.8 % of the kernel's
+    // stall samples on that one MOV, `profiles/r02zl_C5_improved_kernel_1_sass_top.txt`)
+    const unsigned *em32 = reinterpret_cast<const unsigned *>(em);
+    if (IDX_AHEAD) { const int ia = min(e + NW, cnt - 1); q_ah = eq[ia]; ld_mask2(em32 + 2 * ia, m_ah_lo, m_ah_hi); }
     while (true) {
         unsigned long long mn = 0;
+        unsigned t_lo = 0, t_hi = 0;  // the look-ahead mask in flight; becomes m_ah at the end of the iteration
         int en = e + NW;
         if (!ONE_CTA && subs != 1) en = seek(en, mn);
         const bool more = en < cnt;
@@ -618,8 +629,8 @@ improved_kernel(ImprovedArgs a, int Ct) {
         if (more) {
             if constexpr (IDX_AHEAD) {
                 qn = q_ah;
-                mn = m_ah;
-                if (en + NW < cnt) { q_ah = eq[en + NW]; m_ah = em[en + NW]; }
+                mn = ((unsigned long long)m_ah_hi << 32) | m_ah_lo;
+                { const int ia = min(en + NW, cnt - 1); q_ah = eq[ia]; ld_mask2(em32 + 2 * ia, t_lo, t_hi); }
             } else {
                 qn = eq[en];
                 if (ONE_CTA || subs == 1) mn = em[en];
@@ -872,6 +883,7 @@ improved_kernel(ImprovedArgs a, int Ct) {
         e = en;
         qe = qn;
         mcur = mn;
+        if constexpr (IDX_AHEAD) { m_ah_lo = t_lo; m_ah_hi = t_hi; }
     }
     if (lane == 0) {
         if (a.n_eval && evals2) atomicAdd(a.n_eval, evals2);
