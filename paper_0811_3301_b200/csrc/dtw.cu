@@ -324,7 +324,7 @@ dtw4_kernel(DtwArgs a) {
     int st = kFree;
     int item = 0;
     const float *xr = nullptr, *yr = nullptr;
-    float thr = kInf, thr_n = kInf, beta_n = 0.f;
+    float thr = kInf, beta_n = 0.f;
     int i = 0;
     float B[NB + 1];
     float2 Y2[YG ? 1 : NY / 2];  // the y window as register pairs: Y2[k] = (Y[2k], Y[2k+1])
@@ -351,6 +351,7 @@ dtw4_kernel(DtwArgs a) {
         if (__any_sync(0xffffffffu, st == kPending)) {
             cp_wait<0>();
             if (st == kPending) {
+                const float thr_n = slot[NY + 1];
                 if (beta_n > thr_n) {
                     if constexpr (!WALK) a.res[item] = kInf;  // (WALK: pruned by its bound)
                     st = kFree;
@@ -449,7 +450,12 @@ dtw4_kernel(DtwArgs a) {
                     reinterpret_cast<uint32_t *>(slot)[SL - 1] = (uint32_t)c;
                     DCHECK(c < a.Ndb, "dtw4 key c=%lld q=%lld", (long long)c, (long long)qy);
                     beta_n = key_bound(key);
-                    thr_n = *reinterpret_cast<volatile float *>(a.thr + qy);
+                    // tau of the pair's query: copied into the slot's padding word [NY + 1] with the
+                    // refill (as a register load its address pair was overwritten right after it, and
+                    // that IMAD held 6.4 % of the stall samples waiting on the load's operand read,
+                    // `profiles/r02zl_C5_dtw4_kernel_10_sass_top.txt`; in the walk tau changes only
+                    // between launches, and a stale tau is larger, never wrong)
+                    cp_async4(slot + NY + 1, a.thr + qy, 4);
                     if (casc) {
                         // +-beta1: the 4-byte word holding it -> slot[NY]
                         const int64_t gi = qy * a.ldb + c;
@@ -461,7 +467,7 @@ dtw4_kernel(DtwArgs a) {
                 } else {
                     c = qy = item;
                     beta_n = 0.f;
-                    thr_n = kInf;
+                    slot[NY + 1] = kInf;
                 }
                 xr = a.db + c * n;
                 yr = a.ysh + (int64_t)sh * a.ysh_stride_s + qy * a.LP;
